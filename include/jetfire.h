@@ -1,0 +1,146 @@
+/*
+ * jetfire.h — C ABI of libjetfire.so, the B200 (sm_100a) INT8 data-flow hot path.
+ *
+ * Each entry point replaces one function of the reference's Python module
+ * `int8flow` (arXiv 2403.12422 CPU reference, /root/reference/pkg/src/int8flow);
+ * the reference interface it stands in for is cited beside it.
+ *
+ * Conventions (all entry points):
+ *   - every pointer is a DEVICE pointer to row-major, contiguous memory
+ *     (unless a leading dimension argument says otherwise);
+ *   - a BlockQuantTensor [n x c] is two buffers: int8 codes q[n*c] in
+ *     [-127,127] and float32 scales s[(n/32)*(c/32)], every scale on the
+ *     binary16 grid (qtensor.py:73-105).  The block size is fixed at 32;
+ *   - `stream` is a cudaStream_t; every kernel is enqueued on it, nothing
+ *     synchronizes, nothing allocates device memory;
+ *   - the return value is a host-side status: 0 = enqueued, nonzero = shape /
+ *     argument / launch error (message via jf_last_error());
+ *   - data-dependent errors (non-finite input, binary16 scale overflow) are
+ *     reported asynchronously by OR-ing JF_EFLAG_* bits into *err (a device
+ *     int32 the caller zeroes); the host checks it when it synchronizes and
+ *     raises the reference's ValueError texts (qtensor.py:189,210).
+ *   - dimension arguments are int64; all of n, c, d, k must be multiples of 32.
+ */
+#ifndef JETFIRE_H_
+#define JETFIRE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *jf_stream_t; /* == cudaStream_t */
+
+#define JF_OK 0
+#define JF_ERR_ARG 1
+#define JF_ERR_LAUNCH 2
+#define JF_ERR_UNSUPPORTED 3
+
+#define JF_EFLAG_NONFINITE 1 /* "input contains non-finite values" */
+#define JF_EFLAG_OVERFLOW 2  /* "scale overflows the binary16 range" */
+
+/* GEMM promotion modes (qgemm.py:183-229). */
+#define JF_MODE_EXACT 0 /* acc = fl(acc + fl(fl(P*sa)*sb)): bit-exact with the reference */
+#define JF_MODE_FAST 1  /* acc = fl(acc + fl(P*(sa*sb))): one rounding less, |err| <= 1e-6 rel */
+
+/* GEMM output kinds (qgemm.py:266-279). */
+#define JF_OUT_INT8 0     /* requantized codes + scales (quantize=True) */
+#define JF_OUT_F32 1      /* raw FP32 accumulator (+bias) (quantize=False) */
+#define JF_OUT_INT8_DEQ 2 /* codes + scales AND their dequantized FP32 (QuantLinear dW path) */
+
+int jf_version(void);
+const char *jf_last_error(void);
+int jf_sm_count(void);
+
+/* K1 — quantize_per_block(x, 32)  [qtensor.py:219-246]
+ * x: [n x c] float32 (or bfloat16 bits) with row stride ldx elements. */
+int jf_quantize_f32(const float *x, int64_t n, int64_t c, int64_t ldx, int8_t *q, float *s,
+                    int32_t *err, jf_stream_t stream);
+int jf_quantize_bf16(const uint16_t *x, int64_t n, int64_t c, int64_t ldx, int8_t *q, float *s,
+                     int32_t *err, jf_stream_t stream);
+
+/* K2 — dequantize(xq)  [qtensor.py:249-255]; exact.  y: [n x c] float32 / bfloat16 bits. */
+int jf_dequantize_f32(const int8_t *q, const float *s, int64_t n, int64_t c, float *y,
+                      jf_stream_t stream);
+int jf_dequantize_bf16(const int8_t *q, const float *s, int64_t n, int64_t c, uint16_t *y,
+                       jf_stream_t stream);
+
+/* BlockQuantTensor.transposed()  [qtensor.py:130-136]: qt [c x n], st [c/32 x n/32]. */
+int jf_transpose(const int8_t *q, const float *s, int64_t n, int64_t c, int8_t *qt, float *st,
+                 jf_stream_t stream);
+
+/* K3 — block_mm_forward  [qgemm.py:282-309]:  Y[n x d] = X[n x c] . W[d x c]^T (+ bias[d]). */
+int jf_gemm_fwd(const int8_t *x, const float *xs, const int8_t *w, const float *ws,
+                const float *bias, int64_t n, int64_t c, int64_t d, int32_t mode,
+                int32_t out_kind, int8_t *yq, float *ys, float *yf, int32_t *err,
+                jf_stream_t stream);
+
+/* K4 — block_mm_grad_input  [qgemm.py:312-333]:  dX[n x c] = dY[n x d] . W[d x c].
+ * wt: optional W^T codes [c x d] with scales [c/32 x d/32] (NULL: transposed internally
+ * into `scratch`, which must then hold c*d + 4*(c/32)*(d/32) bytes). */
+int jf_gemm_dgrad(const int8_t *dy, const float *dys, const int8_t *w, const float *ws,
+                  const int8_t *wt, const float *wts, int64_t n, int64_t d, int64_t c,
+                  int32_t mode, int32_t out_kind, int8_t *dxq, float *dxs, float *dxf,
+                  void *scratch, int32_t *err, jf_stream_t stream);
+
+/* K5 — block_mm_grad_weight  [qgemm.py:336-357]:  dW[d x c] = dY[n x d]^T . X[n x c].
+ * scratch: >= (n*d + n*c) + 4*((n/32)*(d/32) + (n/32)*(c/32)) bytes (operand transposes). */
+int jf_gemm_wgrad(const int8_t *dy, const float *dys, const int8_t *x, const float *xs,
+                  int64_t n, int64_t d, int64_t c, int32_t mode, int32_t out_kind,
+                  int8_t *dwq, float *dws, float *dwf, void *scratch, int32_t *err,
+                  jf_stream_t stream);
+
+/* Scratch bytes jf_gemm_dgrad / jf_gemm_wgrad need for the given shape. */
+size_t jf_gemm_scratch_bytes(int32_t which /*1=dgrad,2=wgrad*/, int64_t n, int64_t d, int64_t c);
+
+/* Debug: exact int32 partial sums of K chunk `kblk`: P = A[:, 32k:32k+32] . B[32k:32k+32, :]
+ * for A [m x k] codes and B given as Bt [n x k] codes (both K-major).  Computed by the same
+ * tcgen05 kind::i8 MMA as the GEMMs (micro_mm_16, qgemm.py:168-180). */
+int jf_gemm_partials(const int8_t *a, const int8_t *bt, int64_t m, int64_t n, int64_t k,
+                     int64_t kblk, int32_t *p, jf_stream_t stream);
+
+/* K6 — add_forward(x1q, x2q, width)  [qnonlinear.py:246-267] + RowStats [:103-144].
+ * b/bs may be NULL: the second operand is zeros_like(a) (qtensor.py:258-264).
+ * mean/sumsq: [n x c/width] float32. */
+int jf_add_stats(const int8_t *a, const float *as, const int8_t *b, const float *bs, int64_t n,
+                 int64_t c, int64_t width, int8_t *yq, float *ys, float *mean, float *sumsq,
+                 int32_t *err, jf_stream_t stream);
+
+/* K7 — layernorm_forward  [qnonlinear.py:300-330]; writes mu/inv_std [n] (LayerNormContext). */
+int jf_ln_fwd(const int8_t *x, const float *xs, const float *mean, const float *sumsq,
+              int64_t n, int64_t c, int64_t width, const float *gamma, const float *beta,
+              float eps, int8_t *yq, float *ys, float *mu, float *inv_std, int32_t *err,
+              jf_stream_t stream);
+
+/* K8 — layernorm_backward  [qnonlinear.py:333-355]; dgamma/dbeta [c] float32.
+ * workspace: >= jf_ln_bwd_workspace_bytes(n, c) bytes. */
+int jf_ln_bwd(const int8_t *x, const float *xs, const float *mu, const float *inv_std,
+              const int8_t *dy, const float *dys, const float *gamma, int64_t n, int64_t c,
+              int8_t *dxq, float *dxs, float *dgamma, float *dbeta, void *workspace,
+              int32_t *err, jf_stream_t stream);
+size_t jf_ln_bwd_workspace_bytes(int64_t n, int64_t c);
+
+/* K9 / K10 — gelu_forward / gelu_backward  [qnonlinear.py:150-175]. */
+int jf_gelu_fwd(const int8_t *x, const float *xs, int64_t n, int64_t c, int8_t *yq, float *ys,
+                int32_t *err, jf_stream_t stream);
+int jf_gelu_bwd(const int8_t *x, const float *xs, const int8_t *dy, const float *dys, int64_t n,
+                int64_t c, int8_t *dxq, float *dxs, int32_t *err, jf_stream_t stream);
+
+/* K11 — dbias = dequantize(dY).sum(axis=0)  [qlayers.py:180]; out [c] float32.
+ * workspace: >= jf_colsum_workspace_bytes(n, c) bytes. */
+int jf_colsum(const int8_t *q, const float *s, int64_t n, int64_t c, float *out,
+              void *workspace, jf_stream_t stream);
+size_t jf_colsum_workspace_bytes(int64_t n, int64_t c);
+
+/* Dropout by scale folding  [qnonlinear.py:207-240]: codes zeroed where keep[i]==0,
+ * scales snapped f16(s * keep_factor).  keep: [n x c] uint8 (the materialized mask). */
+int jf_dropout(const int8_t *q, const float *s, const uint8_t *keep, float keep_factor,
+               int64_t n, int64_t c, int8_t *oq, float *os, int32_t *err, jf_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* JETFIRE_H_ */

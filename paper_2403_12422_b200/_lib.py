@@ -1,0 +1,109 @@
+"""ctypes binding of libjetfire.so (the C ABI declared in include/jetfire.h).
+
+The product path has no CPU fallback: if the shared library or a CUDA
+device is missing, every op raises ``JetfireUnavailable``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libjetfire.so")
+
+JF_EFLAG_NONFINITE = 1
+JF_EFLAG_OVERFLOW = 2
+MODE_EXACT = 0
+MODE_FAST = 1
+OUT_INT8 = 0
+OUT_F32 = 1
+OUT_INT8_DEQ = 2
+
+
+class JetfireUnavailable(RuntimeError):
+    """libjetfire.so or a CUDA device is missing (there is no CPU fallback)."""
+
+
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_I32 = ctypes.c_int32
+_F32 = ctypes.c_float
+_SZ = ctypes.c_size_t
+
+# name -> (restype, argtypes); mirrors include/jetfire.h exactly
+SIGNATURES = {
+    "jf_version": (ctypes.c_int, []),
+    "jf_last_error": (ctypes.c_char_p, []),
+    "jf_sm_count": (ctypes.c_int, []),
+    "jf_quantize_f32": (ctypes.c_int, [_P, _I64, _I64, _I64, _P, _P, _P, _P]),
+    "jf_quantize_bf16": (ctypes.c_int, [_P, _I64, _I64, _I64, _P, _P, _P, _P]),
+    "jf_dequantize_f32": (ctypes.c_int, [_P, _P, _I64, _I64, _P, _P]),
+    "jf_dequantize_bf16": (ctypes.c_int, [_P, _P, _I64, _I64, _P, _P]),
+    "jf_transpose": (ctypes.c_int, [_P, _P, _I64, _I64, _P, _P, _P]),
+    "jf_gemm_fwd": (ctypes.c_int, [_P, _P, _P, _P, _P, _I64, _I64, _I64, _I32, _I32, _P, _P, _P, _P, _P]),
+    "jf_gemm_dgrad": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I32, _I32, _P, _P, _P,
+                                     _P, _P, _P]),
+    "jf_gemm_wgrad": (ctypes.c_int, [_P, _P, _P, _P, _I64, _I64, _I64, _I32, _I32, _P, _P, _P, _P, _P, _P]),
+    "jf_gemm_scratch_bytes": (_SZ, [_I32, _I64, _I64, _I64]),
+    "jf_gemm_partials": (ctypes.c_int, [_P, _P, _I64, _I64, _I64, _I64, _P, _P]),
+    "jf_add_stats": (ctypes.c_int, [_P, _P, _P, _P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P]),
+    "jf_ln_fwd": (ctypes.c_int, [_P, _P, _P, _P, _I64, _I64, _I64, _P, _P, _F32, _P, _P, _P, _P, _P, _P]),
+    "jf_ln_bwd": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P]),
+    "jf_ln_bwd_workspace_bytes": (_SZ, [_I64, _I64]),
+    "jf_gelu_fwd": (ctypes.c_int, [_P, _P, _I64, _I64, _P, _P, _P, _P]),
+    "jf_gelu_bwd": (ctypes.c_int, [_P, _P, _P, _P, _I64, _I64, _P, _P, _P, _P]),
+    "jf_colsum": (ctypes.c_int, [_P, _P, _I64, _I64, _P, _P, _P]),
+    "jf_colsum_workspace_bytes": (_SZ, [_I64, _I64]),
+    "jf_dropout": (ctypes.c_int, [_P, _P, _P, _F32, _I64, _I64, _P, _P, _P, _P]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load_library(path: str = LIB_PATH):
+    """Load and type the shared library (no CUDA device needed)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise JetfireUnavailable(
+                f"{path} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+            )
+        lib = ctypes.CDLL(path)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        extra = getattr(lib, "jf_set_gemm_magic", None)
+        if extra is not None:
+            extra.restype = None
+            extra.argtypes = [ctypes.c_int]
+        _lib = lib
+        return lib
+
+
+def lib():
+    """The library, after checking a CUDA device exists (fails loudly otherwise)."""
+    if not torch.cuda.is_available():
+        raise JetfireUnavailable("no CUDA device: the Jetfire B200 path has no CPU fallback")
+    return load_library()
+
+
+def ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def stream_handle() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        msg = _lib.jf_last_error().decode(errors="replace") if _lib is not None else ""
+        raise RuntimeError(f"libjetfire {what} failed (status {rc}): {msg}")

@@ -1,0 +1,277 @@
+// common.cuh — shared device helpers for libjetfire (sm_100a only).
+//
+// Numerics follow the reference bit-for-bit (see oracle/int8flow_oracle.py):
+// no FMA contraction (explicit __f*_rn intrinsics; the library is built
+// with -fmad=false as a second guard), IEEE division in the quantizer,
+// round-half-even via __float2int_rn, binary16 RNE scale snapping.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/jetfire.h"
+
+#define JF_DEV __device__ __forceinline__
+
+namespace jf {
+
+constexpr int kBlock = 32;
+constexpr int kQmax = 127;
+
+// ── error word ──────────────────────────────────────────────────────────
+JF_DEV void raise_flags(int32_t *err, int flags) {
+  if (flags && err) atomicOr(err, flags);
+}
+
+// ── quantizer scale rule (qtensor.py:198-211) ──────────────────────────
+// amax_bits: bit pattern of max|x| over the block, computed as an integer
+// max of (bits & 0x7fffffff): any NaN/Inf makes it >= 0x7f800000, which is
+// how np.abs(...).max() propagates non-finite values (qtensor.py:239-241).
+JF_DEV float block_scale(uint32_t amax_bits, int &flags) {
+  if (amax_bits >= 0x7f800000u) {
+    flags |= JF_EFLAG_NONFINITE;
+    return 1.0f;
+  }
+  if (amax_bits == 0u) return 1.0f;  // all-zero block -> scale 1
+  const float am = __uint_as_float(amax_bits);
+  const float raw = __fdiv_rn(am, 127.0f);
+  const float s = __half2float(__float2half_rn(raw));  // binary16 RNE snap
+  if (isinf(s)) {
+    flags |= JF_EFLAG_OVERFLOW;
+    return 1.0f;
+  }
+  return s == 0.0f ? 5.9604644775390625e-08f /* 2**-24 */ : s;
+}
+
+// q = clip(rint(x / s), -127, 127) with a true IEEE division (qtensor.py:243-245)
+JF_DEV int quant_code(float x, float s) {
+  int q = __float2int_rn(__fdiv_rn(x, s));
+  q = q > kQmax ? kQmax : q;
+  q = q < -kQmax ? -kQmax : q;
+  return q;
+}
+
+JF_DEV uint32_t abs_bits(float x) { return __float_as_uint(x) & 0x7fffffffu; }
+
+// pack 4 codes into one 32-bit word (little-endian byte order = column order)
+JF_DEV uint32_t pack4(int a, int b, int c, int d) {
+  return (uint32_t)(a & 0xff) | ((uint32_t)(b & 0xff) << 8) | ((uint32_t)(c & 0xff) << 16) |
+         ((uint32_t)(d & 0xff) << 24);
+}
+
+JF_DEV float code_at(uint32_t word, int i) {
+  return (float)(int8_t)((word >> (8 * i)) & 0xffu);
+}
+
+// ── numpy float32 pairwise summation (documented in the oracle) ─────────
+// Sum of v[0..n) read through an accessor, in numpy's exact order.
+template <typename Get>
+JF_DEV float pairwise_leaf(Get get, int base, int n) {
+  if (n < 8) {
+    float r = 0.0f;
+    for (int i = 0; i < n; ++i) r = __fadd_rn(r, get(base + i));
+    return r;
+  }
+  float r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = get(base + j);
+  int i = 8;
+  const int lim = n - (n % 8);
+  for (; i < lim; i += 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = __fadd_rn(r[j], get(base + i + j));
+  }
+  float res = __fadd_rn(__fadd_rn(__fadd_rn(r[0], r[1]), __fadd_rn(r[2], r[3])),
+                        __fadd_rn(__fadd_rn(r[4], r[5]), __fadd_rn(r[6], r[7])));
+  for (; i < n; ++i) res = __fadd_rn(res, get(base + i));
+  return res;
+}
+
+// Full recursion (n > 128 splits at n2 = n/2 - (n/2)%8).  Depth is small
+// (log2(n/128)); written iteratively via an explicit stack.
+template <typename Get>
+JF_DEV float pairwise_sum(Get get, int base, int n) {
+  if (n <= 128) return pairwise_leaf(get, base, n);
+  // post-order evaluation with an explicit stack of (base, n, state)
+  struct Frame {
+    int base, n, state;
+    float left;
+  };
+  Frame st[24];
+  int sp = 0;
+  st[0] = {base, n, 0, 0.0f};
+  float ret = 0.0f;
+  while (true) {
+    Frame &f = st[sp];
+    if (f.n <= 128) {
+      ret = pairwise_leaf(get, f.base, f.n);
+      if (sp == 0) return ret;
+      --sp;
+      continue;  // ret flows to parent
+    }
+    int n2 = f.n / 2;
+    n2 -= n2 % 8;
+    if (f.state == 0) {
+      f.state = 1;
+      st[++sp] = {f.base, n2, 0, 0.0f};
+    } else if (f.state == 1) {
+      f.left = ret;
+      f.state = 2;
+      st[++sp] = {f.base + n2, f.n - n2, 0, 0.0f};
+    } else {
+      ret = __fadd_rn(f.left, ret);
+      if (sp == 0) return ret;
+      --sp;
+    }
+  }
+}
+
+// ── PTX wrappers: mbarrier, TMA, tcgen05 ───────────────────────────────
+JF_DEV uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+JF_DEV void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+JF_DEV void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+JF_DEV void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+JF_DEV void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+JF_DEV bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+JF_DEV void mbar_wait(uint64_t *bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+
+JF_DEV void tma_load_2d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+JF_DEV void prefetch_tmap(const CUtensorMap *map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+JF_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+JF_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// TMEM allocation (whole warp).  Writes the base address to smem *dst.
+JF_DEV void tmem_alloc(uint32_t *dst, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                   smem_u32(dst)),
+               "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+
+JF_DEV void tmem_dealloc(uint32_t addr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(addr), "r"(ncols)
+               : "memory");
+}
+
+// tcgen05.mma kind::i8, A and B from shared memory descriptors, D (int32) in TMEM.
+JF_DEV void mma_i8_ss(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                      uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// Arrive on an mbarrier once all previously issued tcgen05 async ops of this thread complete.
+JF_DEV void mma_commit(uint64_t *bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+
+JF_DEV void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+JF_DEV void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// 32 lanes x 32 consecutive 32-bit columns: thread i gets TMEM lane (base_lane + i).
+JF_DEV void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+
+// Fill 32 consecutive columns of the warp's 32 lanes with one 32-bit value
+// (4 x .x8 stores: only 8 registers of the constant are live).
+JF_DEV void tmem_fill_32x32b_x32(uint32_t taddr, uint32_t v) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %1, %1, %1, %1, %1, %1, %1};" ::"r"(
+            taddr + 8 * k),
+        "r"(v)
+        : "memory");
+}
+
+// ── UMMA descriptors ───────────────────────────────────────────────────
+// Shared-memory matrix descriptor (sm_100 "version 1"), 128B swizzle.
+//   bits [0,14)  start address >> 4
+//   bits [16,30) leading byte offset >> 4
+//   bits [32,46) stride byte offset >> 4
+//   bits [46,48) version = 1
+//   bits [61,64) layout: 2 = SWIZZLE_128B
+JF_DEV uint64_t smem_desc_sw128(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3fffu);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3fffu) << 16;
+  d |= (uint64_t)((sbo_bytes >> 4) & 0x3fffu) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+// Instruction descriptor for kind::i8: s8 x s8 -> s32, M x N, operand majors.
+__host__ __device__ constexpr uint32_t idesc_i8(int m, int n, int a_mn_major, int b_mn_major) {
+  return (2u << 4)                        // D format: S32
+         | (1u << 7)                      // A: signed 8-bit
+         | (1u << 10)                     // B: signed 8-bit
+         | ((uint32_t)a_mn_major << 15)   // A major
+         | ((uint32_t)b_mn_major << 16)   // B major
+         | ((uint32_t)(n >> 3) << 17)     // N / 8
+         | ((uint32_t)(m >> 4) << 24);    // M / 16
+}
+
+}  // namespace jf

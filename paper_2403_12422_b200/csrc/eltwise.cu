@@ -1,0 +1,530 @@
+// eltwise.cu — K6..K11: the INT8-in / INT8-out memory-bound operators.
+//
+// Every kernel reads INT8 codes + block scales, computes in FP32 in the
+// reference's exact operation order (qnonlinear.py), and requantizes per
+// 32x32 block in registers before writing INT8 back: no FP16/FP32
+// activation ever reaches HBM.  Reductions mirror numpy's float32
+// pairwise order (see oracle.pairwise_sum) so codes, scales and statistics
+// are bit-exact; column (axis-0) parameter-gradient sums are reduced
+// strip-wise (tolerance).
+#include "tile.cuh"
+
+namespace jf {
+
+// ── K6: residual Add + RowStats (qnonlinear.py:246-267, :134-144) ───────
+// Stats of the FP32 sum y (before requantization), per (row, width block):
+// mean = fl(pairwise(y)/w), sumsq = pairwise(fl(y*y)).  y is staged in smem
+// (row stride 257 floats: conflict-free column walks).
+__global__ void __launch_bounds__(kTileThreads) add_stats_kernel(
+    const int8_t *__restrict__ a, const float *__restrict__ as, const int8_t *__restrict__ b,
+    const float *__restrict__ bs, int64_t n, int64_t c, int width, int tile_w, int8_t *yq,
+    float *ys, float *mean, float *sumsq, int32_t *err) {
+  extern __shared__ float ysm[];  // [32][257]
+  __shared__ uint32_t red[64];
+  TilePos t = tile_pos(n, c);
+  t.c0 = (int64_t)blockIdx.x * tile_w;
+  t.active = (8 * t.lane < tile_w) && (t.col() < c);
+  float v[4][8];
+  float w2[4][8];
+  load_deq(t, a, as, v);
+  if (b != nullptr) {
+    load_deq(t, b, bs, w2);
+    if (t.active) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[i][j] = __fadd_rn(v[i][j], w2[i][j]);
+    }
+  } else if (t.active) {
+    // Add(x, zeros_like(x)): x + 0.0 (turns -0.0 into +0.0 exactly like numpy)
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[i][j] = __fadd_rn(v[i][j], 0.0f);
+  }
+  if (t.active) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) ysm[(4 * t.warp + i) * 257 + 8 * t.lane + j] = v[i][j];
+  }
+  __syncthreads();
+  // one thread per (row, stats block): row = tid % 32, block = tid / 32 (+ 8k)
+  const int64_t valid_w = min((int64_t)tile_w, c - t.c0);
+  const int nblk = (int)(valid_w / width);
+  const int64_t cw = c / width;
+  for (int item = threadIdx.x; item < 32 * nblk; item += kTileThreads) {
+    const int row = item & 31, blk = item >> 5;
+    const float *base = ysm + row * 257 + blk * width;
+    const float s1 = pairwise_sum([&](int k) { return base[k]; }, 0, width);
+    const float s2 = pairwise_sum([&](int k) { return __fmul_rn(base[k], base[k]); }, 0, width);
+    const int64_t oi = (t.r0 + row) * cw + t.c0 / width + blk;
+    mean[oi] = __fdiv_rn(s1, (float)width);
+    sumsq[oi] = s2;
+  }
+  quant_store(t, v, yq, ys, red, err);
+}
+
+// ── K7: LayerNorm forward (qnonlinear.py:300-330) ──────────────────────
+// Per-row moments from the Add statistics: 8 lanes per row reproduce the
+// 8-accumulator pairwise sum over the c/width block means / sums of squares.
+JF_DEV float pairwise_small_8lanes(const float *__restrict__ p, int nb, int sub) {
+  // valid for 8 <= nb <= 128; lanes sub=0..7 of an aligned 8-lane group
+  float r = p[sub];
+  const int lim = nb - (nb % 8);
+  for (int i = 8; i < lim; i += 8) r = __fadd_rn(r, p[i + sub]);
+  r = __fadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 1));
+  r = __fadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 2));
+  r = __fadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 4));
+  for (int i = lim; i < nb; ++i) r = __fadd_rn(r, p[i]);
+  return r;
+}
+
+__global__ void __launch_bounds__(256) ln_moments_kernel(const float *__restrict__ mean,
+                                                         const float *__restrict__ sumsq,
+                                                         int64_t n, int64_t c, int nb, float eps,
+                                                         float *mu, float *inv_std) {
+  const int64_t row = (int64_t)blockIdx.x * 32 + (threadIdx.x >> 3);
+  const int sub = threadIdx.x & 7;
+  if (row >= n) return;  // whole 8-lane groups exit together
+  const float *pm = mean + row * nb;
+  const float *ps = sumsq + row * nb;
+  float sm, ss;
+  if (nb >= 8 && nb <= 128) {
+    sm = pairwise_small_8lanes(pm, nb, sub);
+    ss = pairwise_small_8lanes(ps, nb, sub);
+  } else {
+    sm = pairwise_sum([&](int k) { return pm[k]; }, 0, nb);
+    ss = pairwise_sum([&](int k) { return ps[k]; }, 0, nb);
+  }
+  if (sub == 0) {
+    const float m = __fdiv_rn(sm, (float)nb);                          // row_mean
+    float var = __fsub_rn(__fdiv_rn(ss, (float)c), __fmul_rn(m, m));   // row_var
+    var = var > 0.0f ? var : 0.0f;  // np.maximum(var, 0.0) (NaN cannot occur: finite stats)
+    const float sd = __fsqrt_rn(__fadd_rn(var, eps));
+    mu[row] = m;
+    inv_std[row] = __fdiv_rn(1.0f, sd);
+  }
+}
+
+__global__ void __launch_bounds__(kTileThreads) ln_fwd_kernel(
+    const int8_t *__restrict__ x, const float *__restrict__ xs, const float *__restrict__ mu,
+    const float *__restrict__ inv_std, const float *__restrict__ gamma,
+    const float *__restrict__ beta, int64_t n, int64_t c, int8_t *yq, float *ys, int32_t *err) {
+  __shared__ uint32_t red[64];
+  const TilePos t = tile_pos(n, c);
+  float v[4][8];
+  load_deq(t, x, xs, v);
+  if (t.active) {
+    float g[8], bb[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      g[j] = __ldg(gamma + t.col() + j);
+      bb[j] = __ldg(beta + t.col() + j);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float m = __ldg(mu + t.row(i)), is = __ldg(inv_std + t.row(i));
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float xh = __fmul_rn(__fsub_rn(v[i][j], m), is);
+        v[i][j] = __fadd_rn(__fmul_rn(g[j], xh), bb[j]);
+      }
+    }
+  }
+  quant_store(t, v, yq, ys, red, err);
+}
+
+// ── K8: LayerNorm backward (qnonlinear.py:333-355) ─────────────────────
+// Pass A (per row): m1 = mean(dxhat), m2 = mean(dxhat*xhat) over C in numpy's
+// pairwise tree.  The tree of a row is "perfect" (all leaves at one depth)
+// for every C used here; leaf i goes to lane i*L/32.. and the butterfly over
+// lanes reproduces the upper levels.  Non-perfect C falls back to lane 0.
+struct LnRowArgs {
+  const int8_t *x;
+  const float *xs;
+  const float *mu, *inv_std;
+  const int8_t *dy;
+  const float *dys;
+  const float *gamma;
+  int64_t n, c;
+};
+
+JF_DEV void ln_row_vals(const LnRowArgs &A, int64_t row, int64_t col, float mrow, float isrow,
+                        float &dxhat, float &xhat) {
+  const int64_t cb = A.c >> 5;
+  const float sx = __ldg(A.xs + (row >> 5) * cb + (col >> 5));
+  const float sd = __ldg(A.dys + (row >> 5) * cb + (col >> 5));
+  const float xv = __fmul_rn((float)A.x[row * A.c + col], sx);
+  const float dv = __fmul_rn((float)A.dy[row * A.c + col], sd);
+  xhat = __fmul_rn(__fsub_rn(xv, mrow), isrow);
+  dxhat = __fmul_rn(dv, __ldg(A.gamma + col));
+}
+
+__global__ void __launch_bounds__(256) ln_bwd_rows_kernel(LnRowArgs A, int depth, int perfect,
+                                                          float *m1, float *m2) {
+  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= A.n) return;
+  const float mr = __ldg(A.mu + row), ir = __ldg(A.inv_std + row);
+  auto g1 = [&](int k) {
+    float d, h;
+    ln_row_vals(A, row, k, mr, ir, d, h);
+    return d;
+  };
+  auto g2 = [&](int k) {
+    float d, h;
+    ln_row_vals(A, row, k, mr, ir, d, h);
+    return __fmul_rn(d, h);
+  };
+  float s1 = 0.f, s2 = 0.f;
+  if (perfect) {
+    const int nleaf = 1 << depth;
+    const int per = nleaf > 32 ? nleaf / 32 : 1;         // leaves per lane
+    const int lanes = nleaf > 32 ? 32 : nleaf;
+    if (lane < lanes) {
+      // combine this lane's `per` consecutive leaves in tree order (per is 2^k)
+      float acc1[8], acc2[8];  // per <= 8 supported (depth <= 8)
+      for (int li = 0; li < per; ++li) {
+        const int leaf = lane * per + li;
+        int base = 0, len = (int)A.c;
+        for (int lev = depth - 1; lev >= 0; --lev) {
+          int h = len / 2;
+          h -= h % 8;
+          if ((leaf >> lev) & 1) {
+            base += h;
+            len -= h;
+          } else {
+            len = h;
+          }
+        }
+        acc1[li] = pairwise_leaf(g1, base, len);
+        acc2[li] = pairwise_leaf(g2, base, len);
+      }
+      for (int step = 1; step < per; step <<= 1)
+        for (int li = 0; li < per; li += 2 * step) {
+          acc1[li] = __fadd_rn(acc1[li], acc1[li + step]);
+          acc2[li] = __fadd_rn(acc2[li], acc2[li + step]);
+        }
+      s1 = acc1[0];
+      s2 = acc2[0];
+    }
+    for (int off = 1; off < lanes; off <<= 1) {
+      s1 = __fadd_rn(s1, __shfl_xor_sync(0xffffffffu, s1, off));
+      s2 = __fadd_rn(s2, __shfl_xor_sync(0xffffffffu, s2, off));
+    }
+  } else if (lane == 0) {
+    s1 = pairwise_sum(g1, 0, (int)A.c);
+    s2 = pairwise_sum(g2, 0, (int)A.c);
+  }
+  if (lane == 0) {
+    m1[row] = __fdiv_rn(s1, (float)A.c);
+    m2[row] = __fdiv_rn(s2, (float)A.c);
+  }
+}
+
+// Pass B (32x256 tiles): dx = inv_std * ((dxhat - m1) - xhat*m2) -> requant,
+// plus per-strip column partials of dgamma = sum(dy*xhat), dbeta = sum(dy).
+__global__ void __launch_bounds__(kTileThreads) ln_bwd_tile_kernel(
+    LnRowArgs A, const float *__restrict__ m1, const float *__restrict__ m2, int8_t *dxq,
+    float *dxs, float *part_g, float *part_b, int32_t *err) {
+  __shared__ uint32_t red[64];
+  __shared__ float colg[8][256], colb[8][256];
+  const TilePos t = tile_pos(A.n, A.c);
+  float xv[4][8], dv[4][8];
+  load_deq(t, A.x, A.xs, xv);
+  load_deq(t, A.dy, A.dys, dv);
+  float pg[8], pb[8];
+  if (t.active) {
+    float g[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      g[j] = __ldg(A.gamma + t.col() + j);
+      pg[j] = 0.f;
+      pb[j] = 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t r = t.row(i);
+      const float mr = __ldg(A.mu + r), ir = __ldg(A.inv_std + r);
+      const float a1 = __ldg(m1 + r), a2 = __ldg(m2 + r);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float xh = __fmul_rn(__fsub_rn(xv[i][j], mr), ir);
+        const float dxh = __fmul_rn(dv[i][j], g[j]);
+        const float t1 = __fsub_rn(dxh, a1);
+        const float t2 = __fmul_rn(xh, a2);
+        pg[j] = (i == 0) ? __fmul_rn(dv[i][j], xh) : __fadd_rn(pg[j], __fmul_rn(dv[i][j], xh));
+        pb[j] = (i == 0) ? dv[i][j] : __fadd_rn(pb[j], dv[i][j]);
+        xv[i][j] = __fmul_rn(ir, __fsub_rn(t1, t2));  // reuse xv as dx
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      colg[t.warp][8 * t.lane + j] = pg[j];
+      colb[t.warp][8 * t.lane + j] = pb[j];
+    }
+  }
+  quant_store(t, xv, dxq, dxs, red, err);  // contains __syncthreads
+  // rows in order: warp 0 rows 0..3, warp 1 rows 4..7, ... (sequential over warps)
+  const int col = threadIdx.x;
+  if (t.c0 + col < A.c) {
+    float sg = colg[0][col], sb = colb[0][col];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) {
+      sg = __fadd_rn(sg, colg[w][col]);
+      sb = __fadd_rn(sb, colb[w][col]);
+    }
+    part_g[(int64_t)blockIdx.y * A.c + t.c0 + col] = sg;
+    part_b[(int64_t)blockIdx.y * A.c + t.c0 + col] = sb;
+  }
+}
+
+// Sum per-strip partials over strips in order: out[j] = sum_s part[s, j].
+__global__ void __launch_bounds__(256) strip_reduce_kernel(const float *__restrict__ part,
+                                                           int64_t strips, int64_t c,
+                                                           float *out) {
+  const int64_t j = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  if (j >= c) return;
+  float acc = part[j];
+  for (int64_t s = 1; s < strips; ++s) acc = __fadd_rn(acc, part[s * c + j]);
+  out[j] = acc;
+}
+
+// ── K11: dbias partials (qlayers.py:180) ───────────────────────────────
+__global__ void __launch_bounds__(kTileThreads) colsum_tile_kernel(const int8_t *__restrict__ q,
+                                                                   const float *__restrict__ s,
+                                                                   int64_t n, int64_t c,
+                                                                   float *part) {
+  __shared__ float colp[8][256];
+  const TilePos t = tile_pos(n, c);
+  float v[4][8];
+  load_deq(t, q, s, v);
+  if (t.active) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float acc = v[0][j];
+#pragma unroll
+      for (int i = 1; i < 4; ++i) acc = __fadd_rn(acc, v[i][j]);
+      colp[t.warp][8 * t.lane + j] = acc;
+    }
+  }
+  __syncthreads();
+  const int col = threadIdx.x;
+  if (t.c0 + col < c) {
+    float acc = colp[0][col];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) acc = __fadd_rn(acc, colp[w][col]);
+    part[(int64_t)blockIdx.y * c + t.c0 + col] = acc;
+  }
+}
+
+// ── K9 / K10: GELU (qnonlinear.py:27-46, 150-175) ──────────────────────
+// cdf(x) = fl(0.5 * fl(1 + fl32(erf_f64(fl(x * 0.70710677f)))))  — scipy's
+// float32 erf is the double erf rounded (verified), so erf runs in FP64.
+JF_DEV float norm_cdf_f32(float x) {
+  const float z = __fmul_rn(x, 0.7071067811865476f);
+  const float e = __double2float_rn(erf((double)z));
+  return __fmul_rn(0.5f, __fadd_rn(1.0f, e));
+}
+
+__global__ void __launch_bounds__(kTileThreads) gelu_fwd_kernel(const int8_t *__restrict__ x,
+                                                                const float *__restrict__ xs,
+                                                                int64_t n, int64_t c, int8_t *yq,
+                                                                float *ys, int32_t *err) {
+  __shared__ uint32_t red[64];
+  const TilePos t = tile_pos(n, c);
+  float v[4][8];
+  load_deq(t, x, xs, v);
+  if (t.active) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[i][j] = __fmul_rn(v[i][j], norm_cdf_f32(v[i][j]));
+  }
+  quant_store(t, v, yq, ys, red, err);
+}
+
+// gelu'(x) = fl(fl(x * pdf) + cdf), pdf = fl(0.39894228f * exp(fl(fl(-0.5f*x)*x))).
+// numpy's SIMD expf is not correctly rounded; expf here is (<=2 ulp) — the
+// one documented tolerance-only op.
+__global__ void __launch_bounds__(kTileThreads) gelu_bwd_kernel(
+    const int8_t *__restrict__ x, const float *__restrict__ xs, const int8_t *__restrict__ dy,
+    const float *__restrict__ dys, int64_t n, int64_t c, int8_t *dxq, float *dxs, int32_t *err) {
+  __shared__ uint32_t red[64];
+  const TilePos t = tile_pos(n, c);
+  float v[4][8], d[4][8];
+  load_deq(t, x, xs, v);
+  load_deq(t, dy, dys, d);
+  if (t.active) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float xv = v[i][j];
+        const float e = expf(__fmul_rn(__fmul_rn(-0.5f, xv), xv));
+        const float pdf = __fmul_rn(0.3989422804014327f, e);
+        const float g = __fadd_rn(__fmul_rn(xv, pdf), norm_cdf_f32(xv));
+        v[i][j] = __fmul_rn(d[i][j], g);
+      }
+  }
+  quant_store(t, v, dxq, dxs, red, err);
+}
+
+// ── Dropout by scale folding (qnonlinear.py:207-220) ───────────────────
+__global__ void __launch_bounds__(256) dropout_kernel(const int8_t *__restrict__ q,
+                                                      const float *__restrict__ s,
+                                                      const uint8_t *__restrict__ keep,
+                                                      float keep_factor, int64_t n, int64_t c,
+                                                      int8_t *oq, float *os, int32_t *err) {
+  const int64_t total = n * c / 16;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 w = reinterpret_cast<const uint4 *>(q)[i];
+    const uint4 k = reinterpret_cast<const uint4 *>(keep)[i];
+    const uint32_t wv[4] = {w.x, w.y, w.z, w.w}, kv[4] = {k.x, k.y, k.z, k.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      uint32_t r = 0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if ((kv[b] >> (8 * e)) & 0xffu) r |= wv[b] & (0xffu << (8 * e));
+      o[b] = r;
+    }
+    reinterpret_cast<uint4 *>(oq)[i] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+  const int64_t nb = (n >> 5) * (c >> 5);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nb;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float v = __half2float(__float2half_rn(__fmul_rn(s[i], keep_factor)));
+    if (isinf(v)) raise_flags(err, JF_EFLAG_OVERFLOW);
+    os[i] = v;
+  }
+}
+
+}  // namespace jf
+
+using namespace jf;
+int jf_launch_check(const char *what);
+
+static bool ok_shape(int64_t n, int64_t c) { return n > 0 && c > 0 && n % 32 == 0 && c % 32 == 0; }
+
+static int gcd_i(int a, int b) { return b ? gcd_i(b, a % b) : a; }
+
+extern "C" int jf_add_stats(const int8_t *a, const float *as, const int8_t *b, const float *bs,
+                            int64_t n, int64_t c, int64_t width, int8_t *yq, float *ys,
+                            float *mean, float *sumsq, int32_t *err, jf_stream_t stream) {
+  if (!ok_shape(n, c) || width <= 0 || c % width) return JF_ERR_ARG;
+  const int w = (int)width;
+  const int l = 32 / gcd_i(32, w) * w;  // lcm(32, width)
+  if (l > kTileCols) return JF_ERR_UNSUPPORTED;
+  const int tile_w = (kTileCols / l) * l;
+  dim3 grid((unsigned)((c + tile_w - 1) / tile_w), (unsigned)(n / 32));
+  const size_t smem = 32 * 257 * sizeof(float);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(add_stats_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  add_stats_kernel<<<grid, kTileThreads, smem, (cudaStream_t)stream>>>(
+      a, as, b, bs, n, c, w, tile_w, yq, ys, mean, sumsq, err);
+  return jf_launch_check("add_stats");
+}
+
+extern "C" int jf_ln_fwd(const int8_t *x, const float *xs, const float *mean, const float *sumsq,
+                         int64_t n, int64_t c, int64_t width, const float *gamma,
+                         const float *beta, float eps, int8_t *yq, float *ys, float *mu,
+                         float *inv_std, int32_t *err, jf_stream_t stream) {
+  if (!ok_shape(n, c) || width <= 0 || c % width) return JF_ERR_ARG;
+  const int nb = (int)(c / width);
+  ln_moments_kernel<<<(unsigned)((n + 31) / 32), 256, 0, (cudaStream_t)stream>>>(
+      mean, sumsq, n, c, nb, eps, mu, inv_std);
+  int rc = jf_launch_check("ln_moments");
+  if (rc) return rc;
+  ln_fwd_kernel<<<tile_grid(n, c), kTileThreads, 0, (cudaStream_t)stream>>>(
+      x, xs, mu, inv_std, gamma, beta, n, c, yq, ys, err);
+  return jf_launch_check("ln_fwd");
+}
+
+// numpy pairwise tree of length c: perfect iff every leaf sits at one depth.
+static int pw_depth(int64_t len) {
+  if (len <= 128) return 0;
+  int64_t h = len / 2;
+  h -= h % 8;
+  const int a = pw_depth(h), b = pw_depth(len - h);
+  if (a < 0 || b < 0 || a != b) return -1;
+  return a + 1;
+}
+
+extern "C" size_t jf_ln_bwd_workspace_bytes(int64_t n, int64_t c) {
+  return (size_t)(2 * n + 2 * (n / 32) * c) * sizeof(float);
+}
+
+extern "C" int jf_ln_bwd(const int8_t *x, const float *xs, const float *mu, const float *inv_std,
+                         const int8_t *dy, const float *dys, const float *gamma, int64_t n,
+                         int64_t c, int8_t *dxq, float *dxs, float *dgamma, float *dbeta,
+                         void *workspace, int32_t *err, jf_stream_t stream) {
+  if (!ok_shape(n, c)) return JF_ERR_ARG;
+  float *ws = static_cast<float *>(workspace);
+  float *m1 = ws, *m2 = ws + n, *pg = ws + 2 * n, *pb = pg + (n / 32) * c;
+  LnRowArgs A{x, xs, mu, inv_std, dy, dys, gamma, n, c};
+  int depth = pw_depth(c);
+  int perfect = depth >= 0 && depth <= 8;
+  if (!perfect) depth = 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  ln_bwd_rows_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(A, depth, perfect, m1, m2);
+  int rc = jf_launch_check("ln_bwd_rows");
+  if (rc) return rc;
+  ln_bwd_tile_kernel<<<tile_grid(n, c), kTileThreads, 0, st>>>(A, m1, m2, dxq, dxs, pg, pb, err);
+  rc = jf_launch_check("ln_bwd_tile");
+  if (rc) return rc;
+  const unsigned g = (unsigned)((c + 255) / 256);
+  strip_reduce_kernel<<<g, 256, 0, st>>>(pg, n / 32, c, dgamma);
+  strip_reduce_kernel<<<g, 256, 0, st>>>(pb, n / 32, c, dbeta);
+  return jf_launch_check("ln_bwd_reduce");
+}
+
+extern "C" size_t jf_colsum_workspace_bytes(int64_t n, int64_t c) {
+  return (size_t)((n / 32) * c) * sizeof(float);
+}
+
+extern "C" int jf_colsum(const int8_t *q, const float *s, int64_t n, int64_t c, float *out,
+                         void *workspace, jf_stream_t stream) {
+  if (!ok_shape(n, c)) return JF_ERR_ARG;
+  float *part = static_cast<float *>(workspace);
+  cudaStream_t st = (cudaStream_t)stream;
+  colsum_tile_kernel<<<tile_grid(n, c), kTileThreads, 0, st>>>(q, s, n, c, part);
+  int rc = jf_launch_check("colsum_tile");
+  if (rc) return rc;
+  strip_reduce_kernel<<<(unsigned)((c + 255) / 256), 256, 0, st>>>(part, n / 32, c, out);
+  return jf_launch_check("colsum_reduce");
+}
+
+extern "C" int jf_gelu_fwd(const int8_t *x, const float *xs, int64_t n, int64_t c, int8_t *yq,
+                           float *ys, int32_t *err, jf_stream_t stream) {
+  if (!ok_shape(n, c)) return JF_ERR_ARG;
+  gelu_fwd_kernel<<<tile_grid(n, c), kTileThreads, 0, (cudaStream_t)stream>>>(x, xs, n, c, yq, ys,
+                                                                              err);
+  return jf_launch_check("gelu_fwd");
+}
+
+extern "C" int jf_gelu_bwd(const int8_t *x, const float *xs, const int8_t *dy, const float *dys,
+                           int64_t n, int64_t c, int8_t *dxq, float *dxs, int32_t *err,
+                           jf_stream_t stream) {
+  if (!ok_shape(n, c)) return JF_ERR_ARG;
+  gelu_bwd_kernel<<<tile_grid(n, c), kTileThreads, 0, (cudaStream_t)stream>>>(x, xs, dy, dys, n,
+                                                                              c, dxq, dxs, err);
+  return jf_launch_check("gelu_bwd");
+}
+
+extern "C" int jf_dropout(const int8_t *q, const float *s, const uint8_t *keep, float keep_factor,
+                          int64_t n, int64_t c, int8_t *oq, float *os, int32_t *err,
+                          jf_stream_t stream) {
+  if (!ok_shape(n, c)) return JF_ERR_ARG;
+  int64_t th = n * c / 16;
+  unsigned blocks = (unsigned)((th + 255) / 256 < 148 * 8 ? (th + 255) / 256 : 148 * 8);
+  dropout_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(q, s, keep, keep_factor, n, c, oq, os,
+                                                           err);
+  return jf_launch_check("dropout");
+}

@@ -1,0 +1,243 @@
+// microbench.cu — B200 pipe measurements that decide the GEMM promotion design.
+//
+// Prints one JSON line per measurement: FP32 pipe rates (FFMA, FFMA2, FMUL,
+// FADD, I2FP), TMEM ld/st bandwidth, raw tcgen05.mma kind::i8 rate, and the
+// per-element cost of each promotion variant fed from TMEM (no MMA).
+// Build: make microbench  (-> ../microbench).  Run on one B200.
+#include <stdio.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+
+using namespace jf;
+
+#define CK(x)                                                                      \
+  do {                                                                             \
+    cudaError_t e_ = (x);                                                          \
+    if (e_ != cudaSuccess) {                                                       \
+      fprintf(stderr, "%s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e_));   \
+      exit(1);                                                                     \
+    }                                                                              \
+  } while (0)
+
+constexpr int ITERS = 4096;
+
+// ── FP32 pipe rates ────────────────────────────────────────────────────
+template <int OP>
+__global__ void __launch_bounds__(1024, 1) fp_kernel(float *out, long long *cyc, float a, float b) {
+  float x[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x[i] = threadIdx.x * 0.001f + i;
+  int xi[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) xi[i] = threadIdx.x + i;
+  __syncthreads();
+  long long t0 = clock64();
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (OP == 0) x[i] = __fmaf_rn(x[i], a, b);
+      if (OP == 1) x[i] = __fmul_rn(x[i], a);
+      if (OP == 2) x[i] = __fadd_rn(x[i], b);
+      if (OP == 3) {  // I2FP chain through integers
+        x[i] = __int2float_rn(xi[i]);
+        xi[i] = __float_as_int(x[i]) ^ it;
+      }
+    }
+    if (OP == 4) {  // packed f32x2 FMA: 4 instructions = 8 FMAs
+#pragma unroll
+      for (int i = 0; i < 8; i += 2) {
+        uint64_t v = ((uint64_t)__float_as_uint(x[i + 1]) << 32) | __float_as_uint(x[i]);
+        uint64_t av = ((uint64_t)__float_as_uint(a) << 32) | __float_as_uint(a);
+        uint64_t bv = ((uint64_t)__float_as_uint(b) << 32) | __float_as_uint(b);
+        asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(v) : "l"(av), "l"(bv));
+        x[i] = __uint_as_float((uint32_t)v);
+        x[i + 1] = __uint_as_float((uint32_t)(v >> 32));
+      }
+    }
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  float s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += x[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
+// ── TMEM ld / st bandwidth, and promotion variants fed from TMEM ───────
+// 16 warps (4 per lane quarter); VARIANT: 0 = ld only, 1 = st only,
+// 2 = ld + I2F + FMUL + FMUL + FADD (exact), 3 = ld + I2F + FFMA (fast),
+// 4 = ld + st(magic) + FFMA + FADD (fast, magic), 5 = ld + st + FFMA + FMUL + FADD (exact, magic)
+template <int VARIANT>
+__global__ void __launch_bounds__(512, 1) tmem_kernel(float *out, long long *cyc, float sa, float sb) {
+  __shared__ uint32_t tbase;
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) tmem_alloc(&tbase, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t t = tbase + ((uint32_t)((warp & 3) * 32) << 16) + (warp >> 2) * 128;
+  float acc[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) acc[j] = 0.f;
+  uint32_t r[32];
+  __syncthreads();
+  long long t0 = clock64();
+  for (int it = 0; it < ITERS / 4; ++it) {
+    const uint32_t ta = t + (it & 3) * 32;
+    if (VARIANT != 1) {
+      tmem_ld_32x32b_x32(ta, r);
+      tmem_wait_ld();
+    }
+    if (VARIANT == 1 || VARIANT == 4 || VARIANT == 5) {
+      tmem_fill_32x32b_x32(ta, 0x4B400000u + it);
+      tmem_wait_st();
+    }
+    if (VARIANT == 0) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) acc[j] = __uint_as_float(__float_as_uint(acc[j]) ^ r[j]);
+    } else if (VARIANT == 2) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        acc[j] = __fadd_rn(acc[j], __fmul_rn(__fmul_rn(__int2float_rn((int)r[j]), sa), sb));
+    } else if (VARIANT == 3) {
+      const float s = sa * sb;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) acc[j] = __fmaf_rn(__int2float_rn((int)r[j]), s, acc[j]);
+    } else if (VARIANT == 4) {
+      const float s = sa * sb, ncs = -12582912.0f * s;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) acc[j] = __fadd_rn(acc[j], __fmaf_rn(__uint_as_float(r[j]), s, ncs));
+    } else if (VARIANT == 5) {
+      const float ncs = -12582912.0f * sa;
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        acc[j] = __fadd_rn(acc[j], __fmul_rn(__fmaf_rn(__uint_as_float(r[j]), sa, ncs), sb));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  long long t1 = clock64();
+  float s = 0;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) s += acc[j];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+  if (warp == 0) tmem_dealloc(tbase, 512);
+}
+
+// ── raw tcgen05.mma kind::i8 issue rate ────────────────────────────────
+template <int N>
+__global__ void __launch_bounds__(128, 1) mma_kernel(long long *cyc, int nmma) {
+  extern __shared__ uint8_t smraw[];
+  uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint32_t tbase;
+  __shared__ uint64_t bar;
+  const int warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < (128 + N) * 128 / 4; i += blockDim.x)
+    reinterpret_cast<uint32_t *>(sm)[i] = 0x01010101u * (i & 7);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc(&tbase, 512);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (threadIdx.x == 32) {
+    const uint32_t a0 = smem_u32(sm), b0 = smem_u32(sm + 128 * 128);
+    constexpr uint32_t idesc = idesc_i8(128, N, 0, 0);
+    long long t0 = clock64();
+    for (int i = 0; i < nmma; ++i) {
+      const int c = i & 3;
+      mma_i8_ss(tbase + (i & 1) * N, smem_desc_sw128(a0 + c * 32, 16, 1024),
+                smem_desc_sw128(b0 + c * 32, 16, 1024), idesc, 1u);
+    }
+    mma_commit(&bar);
+    mbar_wait(&bar, 0);
+    long long t1 = clock64();
+    cyc[blockIdx.x] = t1 - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tbase, 512);
+}
+
+static int g_sms;
+
+static double median_cycles(long long *d_cyc, int n) {
+  std::vector<long long> h(n);
+  CK(cudaMemcpy(h.data(), d_cyc, n * sizeof(long long), cudaMemcpyDeviceToHost));
+  std::sort(h.begin(), h.end());
+  return (double)h[n / 2];
+}
+
+#include <algorithm>
+
+template <int OP>
+void run_fp(const char *name, float *d_out, long long *d_cyc, double ops_per_iter_thread) {
+  fp_kernel<OP><<<g_sms, 1024>>>(d_out, d_cyc, 1.0001f, 0.5f);
+  CK(cudaDeviceSynchronize());
+  fp_kernel<OP><<<g_sms, 1024>>>(d_out, d_cyc, 1.0001f, 0.5f);
+  CK(cudaDeviceSynchronize());
+  double cyc = median_cycles(d_cyc, g_sms);
+  double ops = ops_per_iter_thread * ITERS * 1024.0;
+  printf("{\"bench\": \"%s\", \"ops_per_clk_per_sm\": %.1f, \"cycles\": %.0f}\n", name, ops / cyc, cyc);
+}
+
+template <int V>
+void run_tmem(const char *name, float *d_out, long long *d_cyc) {
+  tmem_kernel<V><<<g_sms, 512>>>(d_out, d_cyc, 0.01f, 0.02f);
+  CK(cudaDeviceSynchronize());
+  tmem_kernel<V><<<g_sms, 512>>>(d_out, d_cyc, 0.01f, 0.02f);
+  CK(cudaDeviceSynchronize());
+  double cyc = median_cycles(d_cyc, g_sms);
+  double elems = 16.0 * 32 * 32 * (ITERS / 4);  // 16 warps x 32 lanes x 32 cols per iter
+  printf("{\"bench\": \"%s\", \"elems_per_clk_per_sm\": %.1f, \"bytes_per_clk_per_sm\": %.1f, \"cycles\": %.0f}\n",
+         name, elems / cyc, elems * 4 / cyc, cyc);
+}
+
+template <int N>
+void run_mma(long long *d_cyc) {
+  const size_t smem = 1024 + (128 + N) * 128;
+  CK(cudaFuncSetAttribute(mma_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int nmma = 4096;
+  mma_kernel<N><<<g_sms, 128, smem>>>(d_cyc, nmma);
+  CK(cudaDeviceSynchronize());
+  mma_kernel<N><<<g_sms, 128, smem>>>(d_cyc, nmma);
+  CK(cudaDeviceSynchronize());
+  double cyc = median_cycles(d_cyc, g_sms);
+  double macs = 128.0 * N * 32 * nmma;
+  printf("{\"bench\": \"mma_i8_m128_n%d_k32\", \"mac_per_clk_per_sm\": %.1f, \"clk_per_mma\": %.2f}\n", N,
+         macs / cyc, cyc / nmma);
+}
+
+int main() {
+  CK(cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, 0));
+  int clk_khz = 0;
+  CK(cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0));
+  printf("{\"bench\": \"device\", \"sms\": %d, \"clock_khz_attr\": %d}\n", g_sms, clk_khz);
+  float *d_out;
+  long long *d_cyc;
+  CK(cudaMalloc(&d_out, g_sms * 1024 * sizeof(float)));
+  CK(cudaMalloc(&d_cyc, g_sms * sizeof(long long)));
+  run_fp<0>("ffma", d_out, d_cyc, 8);
+  run_fp<1>("fmul", d_out, d_cyc, 8);
+  run_fp<2>("fadd", d_out, d_cyc, 8);
+  run_fp<3>("i2fp_chain", d_out, d_cyc, 8);
+  run_fp<4>("ffma2_x2_fmas", d_out, d_cyc, 8);
+  run_tmem<0>("tmem_ld_x32", d_out, d_cyc);
+  run_tmem<1>("tmem_st_x8x4", d_out, d_cyc);
+  run_tmem<2>("promote_exact_i2f", d_out, d_cyc);
+  run_tmem<3>("promote_fast_i2f", d_out, d_cyc);
+  run_tmem<4>("promote_fast_magic", d_out, d_cyc);
+  run_tmem<5>("promote_exact_magic", d_out, d_cyc);
+  run_mma<128>(d_cyc);
+  run_mma<256>(d_cyc);
+  run_mma<64>(d_cyc);
+  return 0;
+}

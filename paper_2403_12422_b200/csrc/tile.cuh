@@ -1,0 +1,102 @@
+// tile.cuh — the 32 x 256 register tile shared by every memory-bound kernel.
+//
+// One CTA of 256 threads owns a 32-row strip x 256 columns (8 quantization
+// blocks).  Warp w holds rows 4w..4w+3, lane l holds columns 8l..8l+7 of
+// each of those rows, i.e. 32 FP32 values per thread, so every global
+// access is a fully used 256-byte row segment per warp (int8) and the
+// 32 x 32 block absmax needs one 4-lane shuffle + one cross-warp smem step.
+#pragma once
+
+#include "common.cuh"
+
+namespace jf {
+
+constexpr int kTileRows = 32;
+constexpr int kTileCols = 256;
+constexpr int kTileThreads = 256;
+
+struct TilePos {
+  int64_t r0;   // first row of the strip
+  int64_t c0;   // first column of the tile
+  int64_t n, c; // matrix shape
+  int warp, lane;
+  bool active;  // this thread's 8 columns lie inside the matrix
+
+  JF_DEV int64_t row(int i) const { return r0 + 4 * warp + i; }
+  JF_DEV int64_t col() const { return c0 + 8 * lane; }
+  JF_DEV int64_t scale_idx(int64_t r, int64_t cc) const { return (r >> 5) * (c >> 5) + (cc >> 5); }
+};
+
+JF_DEV TilePos tile_pos(int64_t n, int64_t c) {
+  TilePos t;
+  t.r0 = (int64_t)blockIdx.y * kTileRows;
+  t.c0 = (int64_t)blockIdx.x * kTileCols;
+  t.n = n;
+  t.c = c;
+  t.warp = threadIdx.x >> 5;
+  t.lane = threadIdx.x & 31;
+  t.active = t.col() < c;  // c is a multiple of 32 -> whole quant blocks
+  return t;
+}
+
+// Load 4 rows x 8 int8 codes and dequantize them (exact: code * scale).
+JF_DEV void load_deq(const TilePos &t, const int8_t *__restrict__ q, const float *__restrict__ s,
+                     float (&v)[4][8]) {
+  if (!t.active) return;
+  const float sc = __ldg(s + t.scale_idx(t.r0, t.col()));  // 4 rows share one row block
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint2 w = __ldg(reinterpret_cast<const uint2 *>(q + t.row(i) * t.c + t.col()));
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      v[i][j] = __fmul_rn(code_at(w.x, j), sc);
+      v[i][4 + j] = __fmul_rn(code_at(w.y, j), sc);
+    }
+  }
+}
+
+// Requantize the FP32 tile per 32x32 block and store codes + scales
+// (quantize_per_block semantics, qtensor.py:219-246).  `red` is >= 64 words
+// of shared memory.  Ends with the CTA synchronized (red reusable).
+JF_DEV void quant_store(const TilePos &t, const float (&v)[4][8], int8_t *__restrict__ q,
+                        float *__restrict__ s, uint32_t *red, int32_t *err) {
+  uint32_t m = 0;
+  if (t.active) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) m = max(m, abs_bits(v[i][j]));
+  }
+  m = max(m, __shfl_xor_sync(0xffffffffu, m, 1));
+  m = max(m, __shfl_xor_sync(0xffffffffu, m, 2));
+  const int qb = t.lane >> 2;
+  if ((t.lane & 3) == 0) red[t.warp * 8 + qb] = m;
+  __syncthreads();
+  uint32_t am = 0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) am = max(am, red[w * 8 + qb]);
+  int flags = 0;
+  const float sc = block_scale(am, flags);
+  if (t.active) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      uint2 w;
+      w.x = pack4(quant_code(v[i][0], sc), quant_code(v[i][1], sc), quant_code(v[i][2], sc),
+                  quant_code(v[i][3], sc));
+      w.y = pack4(quant_code(v[i][4], sc), quant_code(v[i][5], sc), quant_code(v[i][6], sc),
+                  quant_code(v[i][7], sc));
+      *reinterpret_cast<uint2 *>(q + t.row(i) * t.c + t.col()) = w;
+    }
+    if (t.warp == 0 && (t.lane & 3) == 0) {
+      s[t.scale_idx(t.r0, t.col())] = sc;
+      raise_flags(err, flags);
+    }
+  }
+  __syncthreads();
+}
+
+inline dim3 tile_grid(int64_t n, int64_t c) {
+  return dim3((unsigned)((c + kTileCols - 1) / kTileCols), (unsigned)(n / kTileRows));
+}
+
+}  // namespace jf

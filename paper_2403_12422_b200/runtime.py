@@ -1,0 +1,83 @@
+"""Runtime knobs and the asynchronous error word.
+
+Kernels that can hit a data-dependent error (non-finite input, binary16
+scale overflow — qtensor.py:189,210) OR a flag into one device int32; the
+host turns it into the reference's ``ValueError`` text.  In ``eager`` mode
+(the default, exactly the reference's behaviour) every op that can fail
+synchronizes and checks; in ``deferred`` mode the check happens at
+``check_errors()`` (once per training step), so steps stay sync-free.
+"""
+
+from __future__ import annotations
+
+import threading
+
+import torch
+
+from . import _lib
+
+_MSG_NONFINITE = "input contains non-finite values"
+_MSG_OVERFLOW = "scale overflows the binary16 range; input magnitude too large"
+
+_state = threading.local()
+_config = {"error_check": "eager", "promotion": "exact"}
+
+
+def set_error_check(mode: str) -> None:
+    """'eager' (raise from the failing call, reference semantics) or 'deferred'."""
+    if mode not in ("eager", "deferred"):
+        raise ValueError(f"error_check must be 'eager' or 'deferred', got {mode!r}")
+    _config["error_check"] = mode
+
+
+def get_error_check() -> str:
+    return _config["error_check"]
+
+
+def set_promotion(mode: str) -> None:
+    """GEMM promotion: 'exact' (bit-exact with qgemm.py) or 'fast' (one rounding less)."""
+    if mode not in ("exact", "fast"):
+        raise ValueError(f"promotion must be 'exact' or 'fast', got {mode!r}")
+    _config["promotion"] = mode
+
+
+def get_promotion() -> str:
+    return _config["promotion"]
+
+
+def promotion_code(mode: str | None) -> int:
+    m = mode or _config["promotion"]
+    if m not in ("exact", "fast"):
+        raise ValueError(f"promotion must be 'exact' or 'fast', got {m!r}")
+    return _lib.MODE_EXACT if m == "exact" else _lib.MODE_FAST
+
+
+def _word(device=None) -> torch.Tensor:
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    words = getattr(_state, "words", None)
+    if words is None:
+        words = _state.words = {}
+    w = words.get(dev.index)
+    if w is None:
+        w = words[dev.index] = torch.zeros(1, dtype=torch.int32, device=dev)
+    return w
+
+
+def err_ptr() -> int:
+    return _word().data_ptr()
+
+
+def check_errors() -> None:
+    """Synchronize on the error word; raise the reference's ValueError if set."""
+    w = _word()
+    flags = int(w.item())
+    if flags:
+        w.zero_()
+        if flags & _lib.JF_EFLAG_NONFINITE:
+            raise ValueError(_MSG_NONFINITE)
+        raise ValueError(_MSG_OVERFLOW)
+
+
+def maybe_check() -> None:
+    if _config["error_check"] == "eager":
+        check_errors()
