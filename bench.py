@@ -1,0 +1,431 @@
+#!/usr/bin/env python
+"""bench.py — Jetfire INT8 data-flow transformer block, fwd+bwd tokens/s on B200.
+
+Metric (BASELINE.json): transformer-block fwd+bwd tokens/s; per-block INT8
+GEMM TOPS vs INT8 peak.  Default workload: BASELINE config "transformer block
+hidden 4096, seq 2048" (the north star's target setting), random-init
+weights, synthetic standard-normal activations/gradients, dropout p = 0.
+
+One step = forward + backward of one TransformerBlock in the INT8 data flow
+(12 tcgen05 GEMMs + fused INT8 elementwise kernels + SDPA attention island).
+``value``: inputs already quantized in HBM.  ``e2e``: host pinned FP32 x and
+dY copied in, quantized, fwd+bwd, dX (codes+scales) copied back, per step.
+
+Multi-GPU (torchrun): data parallel over the token batch, per-rank batch
+fixed (weak scaling); the one exchange step is an NCCL all-reduce of the
+FP32 parameter gradients.  ``--impl reference`` times the CPU oracle port of
+the reference (numpy) on a bounded token sample of the same block.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "transformer-block fwd+bwd tokens/s; per-block INT8 GEMM TOPS vs INT8 peak"
+INT8_PEAK_TOPS = 4500.0  # B200 dense INT8 datasheet (no measured INT8 figure in MEASURED_PEAKS.json)
+
+WORKLOADS = {
+    # BASELINE.json configs[3]: the paper's speed-up setting, north-star target
+    "block_h4096_s2048": dict(c=4096, heads=32, hidden=16384, seq=2048, batch=2),
+    # BASELINE.json configs[1]
+    "block_h1024_s1024": dict(c=1024, heads=16, hidden=4096, seq=1024, batch=8),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="block_h4096_s2048", choices=sorted(WORKLOADS))
+    ap.add_argument("--batch", type=int, default=None, help="sequences per GPU")
+    ap.add_argument("--promotion", default="exact", choices=["exact", "fast"])
+    ap.add_argument("--attn-dtype", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--no-bf16", action="store_true", help="skip the cuBLAS BF16 block baseline")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle baseline")
+    ap.add_argument("--cpu-tokens", type=int, default=128, help="token sample for the CPU baseline")
+    return ap.parse_args()
+
+
+# ── distributed plumbing ────────────────────────────────────────────────
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ── clocks sampling during the timed region ─────────────────────────────
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+            time.sleep(0.25)
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, smax, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = max(smax, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ── the INT8 data-flow block (ours) ─────────────────────────────────────
+
+
+def build_block(jf, w, attn_dtype, seed=0):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    c, h = w["c"], w["hidden"]
+
+    def lin(d, cc):
+        wt = torch.randn((d, cc), generator=g, device="cuda") / float(np.sqrt(cc))
+        return jf.QuantLinear(wt, torch.zeros(d, device="cuda"))
+
+    cfg = jf.BlockConfig(c_model=c, heads=w["heads"], hidden=h, block=32, dropout_p=0.0)
+    ln = lambda: jf.NormParams(torch.ones(c, device="cuda"), torch.zeros(c, device="cuda"), cfg.eps)  # noqa: E731
+    blk = jf.TransformerBlock(cfg, lin(3 * c, c), lin(c, c), lin(h, c), lin(c, h), ln(), ln(),
+                              attn_dtype=attn_dtype)
+    for lyr in (blk.qkv, blk.proj, blk.mlp1, blk.mlp2):  # INT8 weights (+ transposes) built once
+        lyr.weight_q, lyr.weight_qt
+    return blk
+
+
+def allreduce_grads(grads: dict, world: int):
+    """The DP exchange step: one flat NCCL all-reduce of every FP32 parameter gradient."""
+    if world == 1:
+        return
+    import torch.distributed as dist
+
+    keys = sorted(k for k, v in grads.items() if v is not None)
+    flat = torch.cat([grads[k].reshape(-1) for k in keys])
+    dist.all_reduce(flat)
+    flat.div_(world)
+    off = 0
+    for k in keys:
+        n = grads[k].numel()
+        grads[k].copy_(flat[off:off + n].view_as(grads[k]))
+        off += n
+
+
+def run_ours(args, world, rank, local):
+    import paper_2403_12422_b200 as jf
+    from paper_2403_12422_b200 import _lib
+    from paper_2403_12422_b200.qgemm import GemmTimer
+
+    jf.require_cuda()
+    jf.set_error_check("deferred")
+    jf.set_promotion(args.promotion)
+    w = dict(WORKLOADS[args.workload])
+    if args.batch:
+        w["batch"] = args.batch
+    b, s, c = w["batch"], w["seq"], w["c"]
+    n = b * s
+    attn_dtype = torch.bfloat16 if args.attn_dtype == "bf16" else torch.float32
+    blk = build_block(jf, w, attn_dtype, seed=0)
+    g = torch.Generator(device="cuda").manual_seed(1000 + rank)
+    x = torch.randn((n, c), generator=g, device="cuda")
+    dy = 0.1 * torch.randn((n, c), generator=g, device="cuda")
+    xq = jf.quantize_per_block(x)
+    dyq = jf.quantize_per_block(dy)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        blk.forward(xq, b, s)
+        dx, grads = blk.backward(dyq)
+        allreduce_grads(grads, world)
+        return dx
+
+    for _ in range(args.warmup):
+        step()
+    jf.check_errors()
+    torch.cuda.synchronize()
+    barrier(world)
+
+    # ── timed region: K steps, inputs resident in HBM ──
+    _lib.launch_count[0] = 0
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks, GemmTimer() as gt:
+        torch.cuda.synchronize()
+        barrier(world)
+        start.record(stream)
+        for _ in range(args.steps):
+            step()
+        end.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+    launches = _lib.launch_count[0] // args.steps
+    jf.check_errors()
+    ms = max_over_ranks(start.elapsed_time(end), world)
+    ms_step = ms / args.steps
+    tokens_per_s = world * n * args.steps / (ms / 1e3)
+    gsum = gt.summary()
+    gemm_ms_step = gsum["ms"] / args.steps
+    gemm_tops = gsum["ops"] / (gsum["ms"] / 1e3) / 1e12
+
+    # ── e2e: host pinned FP32 in, dX codes + scales out, every step ──
+    hx = x.cpu().pin_memory()
+    hdy = dy.cpu().pin_memory()
+    hq = torch.empty((n, c), dtype=torch.int8).pin_memory()
+    hs = torch.empty((n // 32, c // 32), dtype=torch.float32).pin_memory()
+
+    def e2e_step():
+        dx_ = torch.empty((n, c), device="cuda")
+        dd_ = torch.empty((n, c), device="cuda")
+        dx_.copy_(hx, non_blocking=True)
+        dd_.copy_(hdy, non_blocking=True)
+        xq_ = jf.quantize_per_block(dx_)
+        dq_ = jf.quantize_per_block(dd_)
+        blk.forward(xq_, b, s)
+        gx, grads = blk.backward(dq_)
+        allreduce_grads(grads, world)
+        hq.copy_(gx.values, non_blocking=True)
+        hs.copy_(gx.scales, non_blocking=True)
+
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    jf.check_errors()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1), world)
+    e2e_val = world * n * args.steps / (e2e_ms / 1e3)
+
+    out = {
+        "metric": METRIC, "value": round(tokens_per_s, 1), "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8",
+        "data": "synthetic (standard-normal activations, 0.1*normal upstream grads, random-init weights)",
+        "config": {"workload": args.workload, "hidden": c, "heads": w["heads"], "mlp_hidden": w["hidden"],
+                   "seq_len": s, "batch_per_gpu": b, "tokens_per_gpu": n, "global_tokens": world * n,
+                   "block": 32, "promotion": args.promotion, "attention": f"torch SDPA ({args.attn_dtype})",
+                   "parallelism": f"dp{world}" if world > 1 else "single",
+                   "l2": "working set (201 MB INT8 weights + activations) larger than the 126 MB L2"},
+        "e2e": {"value": round(e2e_val, 1), "unit": "tokens/s",
+                "h2d_bytes_per_step": int(2 * n * c * 4), "d2h_bytes_per_step": int(n * c + (n * c // 1024) * 4)},
+        "gpu_launches": int(launches),
+        "gemm": {"launches_per_step": gsum["launches"] // args.steps, "ms_per_step": round(gemm_ms_step, 4),
+                 "tops": round(gemm_tops, 1), "frac_of_int8_peak": round(gemm_tops / INT8_PEAK_TOPS, 4),
+                 "share_of_step": round(gemm_ms_step / ms_step, 3)},
+    }
+    out["roofline"] = {"kernel": "gemm_i8_kernel (tcgen05 kind::i8)", "bound": "tensor",
+                       "achieved": round(gemm_tops, 1), "peak": INT8_PEAK_TOPS, "unit": "TFLOP/s",
+                       "frac": round(gemm_tops / INT8_PEAK_TOPS, 4), "traffic": None,
+                       "peak_source": "B200 dense INT8 datasheet 4.5 POPS (int ops counted as FLOP)"}
+    out["clocks"] = clocks.summary()
+    return out, blk, (xq, dyq), w
+
+
+# ── cuBLAS BF16 block of the same wiring (context baseline) ─────────────
+
+
+def bf16_block_tokens_per_s(w, steps, warmup):
+    import torch.nn.functional as F
+
+    c, h, heads, b, s = w["c"], w["hidden"], w["heads"], w["batch"], w["seq"]
+    n = b * s
+    dev, dt = "cuda", torch.bfloat16
+    g = torch.Generator(device=dev).manual_seed(0)
+
+    def p(*shape, scale=1.0):
+        return (torch.randn(shape, generator=g, device=dev) * scale).to(dt).requires_grad_(True)
+
+    P = dict(wqkv=p(3 * c, c, scale=c ** -0.5), bqkv=p(3 * c, scale=0.0), wp=p(c, c, scale=c ** -0.5),
+             bp=p(c, scale=0.0), w1=p(h, c, scale=c ** -0.5), b1=p(h, scale=0.0), w2=p(c, h, scale=h ** -0.5),
+             b2=p(c, scale=0.0), g1=torch.ones(c, device=dev, dtype=dt, requires_grad=True),
+             be1=torch.zeros(c, device=dev, dtype=dt, requires_grad=True),
+             g2=torch.ones(c, device=dev, dtype=dt, requires_grad=True),
+             be2=torch.zeros(c, device=dev, dtype=dt, requires_grad=True))
+    x = torch.randn((n, c), generator=g, device=dev).to(dt).requires_grad_(True)
+    dy = (0.1 * torch.randn((n, c), generator=g, device=dev)).to(dt)
+
+    def fwd(x):
+        a = F.layer_norm(x, (c,), P["g1"], P["be1"])
+        qkv = F.linear(a, P["wqkv"], P["bqkv"]).view(b, s, 3, heads, c // heads)
+        q, k, v = (qkv[:, :, i].transpose(1, 2) for i in range(3))
+        o = F.scaled_dot_product_attention(q, k, v, is_causal=True).transpose(1, 2).reshape(n, c)
+        hh = x + F.linear(o, P["wp"], P["bp"])
+        m = F.gelu(F.linear(F.layer_norm(hh, (c,), P["g2"], P["be2"]), P["w1"], P["b1"]), approximate="none")
+        return hh + F.linear(m, P["w2"], P["b2"])
+
+    def step():
+        out = fwd(x)
+        out.backward(dy)
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(steps):
+        step()
+    e.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(e)
+    return n * steps / (ms / 1e3), ms / steps
+
+
+# ── CPU oracle (the reference's algorithm, numpy port) ──────────────────
+
+
+def cpu_block_sample(w, tokens, reps=1):
+    """Time oracle block fwd+bwd on `tokens` tokens of the workload's block dims."""
+    from oracle import int8flow_oracle as O
+
+    rng = np.random.default_rng(0)
+    c, h, heads = w["c"], w["hidden"], w["heads"]
+    seq = min(tokens, w["seq"])
+    batch = max(1, tokens // seq)
+    p = O.block_weight_cache(O.block_init(rng, c, h))
+    xq, xs = O.quantize(rng.standard_normal((batch * seq, c)).astype(np.float32))
+    dq, ds = O.quantize((0.1 * rng.standard_normal((batch * seq, c))).astype(np.float32))
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        _, saved = O.block_forward(p, xq, xs, batch, seq, heads)
+        O.block_backward(p, saved, dq, ds)
+        times.append(time.perf_counter() - t0)
+    t = min(times)
+    return {"value": round(batch * seq / t, 2), "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
+            "sample": f"oracle (numpy port of int8flow) block fwd+bwd, {batch}x{seq} tokens at "
+                      f"hidden {c}/mlp {h}, OpenBLAS threads = all host cores, best of {reps}",
+            "seconds": round(t, 3)}
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return None
+    w = dict(WORKLOADS[args.workload])
+    tokens = args.cpu_tokens
+    for _ in range(args.warmup):
+        cpu_block_sample(w, tokens)
+    vals = [cpu_block_sample(w, tokens)["value"] for _ in range(args.steps)]
+    v = statistics.median(vals)
+    cb = cpu_block_sample(w, tokens)
+    cb["value"] = v
+    return {"metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(1e3 * tokens / v, 2), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int8", "impl": "reference",
+            "data": "synthetic", "config": {"workload": args.workload, "tokens_per_step": tokens,
+                                            "parallelism": "cpu"},
+            "cpu_baseline": cb, "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                                        "d2h_bytes_per_step": 0}}
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        out = run_reference(args, world, rank)
+        if out is not None:
+            print(json.dumps(out), flush=True)
+        return
+    out, blk, _, w = run_ours(args, world, rank, local)
+    if rank == 0:
+        if not args.no_bf16:
+            wb = dict(w)
+            tps, ms = bf16_block_tokens_per_s(wb, args.steps, args.warmup)
+            out["bf16_baseline"] = {"value": round(tps * world, 1), "unit": "tokens/s", "ms_per_step": round(ms, 4),
+                                    "what": "same block wiring in torch BF16 (cuBLAS linear, F.layer_norm, "
+                                            "exact-erf GELU, SDPA), fwd+bwd autograd, 1 GPU",
+                                    "int8_over_bf16": round(out["value"] / (tps * world), 3)}
+        if world == 1 and not args.no_cpu:
+            out["cpu_baseline"] = cpu_block_sample(w, args.cpu_tokens)
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

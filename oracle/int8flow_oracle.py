@@ -277,15 +277,20 @@ def column_sum(q, s):
 # ── layer orchestration (qlayers.py) ────────────────────────────────────
 
 
+def _weight_codes(w):
+    """QuantLinear.weight_q (qlayers.py:139-143): a cached (codes, scales) pair or a master to quantize."""
+    return w if isinstance(w, tuple) else quantize(w)
+
+
 def linear_forward(xq, xs, w_master, bias):
-    """QuantLinear.forward (qlayers.py:139-163): quantize master, GEMM fwd."""
-    wq, ws = quantize(w_master)
+    """QuantLinear.forward (qlayers.py:149-163): INT8 weight, GEMM fwd + bias + requant."""
+    wq, ws = _weight_codes(w_master)
     return mm_forward(xq, xs, wq, ws, bias)
 
 
 def linear_backward(xq, xs, w_master, dyq, dys, has_bias=True):
     """QuantLinear.backward (qlayers.py:165-181) -> (dxq, dxs, dW fp32, dbias)."""
-    wq, ws = quantize(w_master)
+    wq, ws = _weight_codes(w_master)
     dxq, dxs = mm_grad_input(dyq, dys, wq, ws)
     dwq, dws = mm_grad_weight(dyq, dys, xq, xs)
     dbias = column_sum(dyq, dys) if has_bias else None
@@ -331,3 +336,81 @@ def attention_f32_backward(dout, saved, batch, seq, heads):
     dq = ds @ k
     dk = ds.transpose(0, 1, 3, 2) @ q
     return np.concatenate([merge(dq), merge(dk), merge(dv)], axis=1).astype(np.float32)
+
+
+# ── TransformerBlock orchestration (qlayers.py:329-427), dropout p = 0 ───
+
+
+def block_init(rng, c, hidden):
+    """Parameters drawn exactly like TransformerBlock.initialize (qlayers.py:287-303)."""
+    def lin(d, cc):
+        return (rng.standard_normal((d, cc)) / np.sqrt(cc)).astype(np.float32), np.zeros(d, np.float32)
+
+    p = {}
+    p["qkv.w"], p["qkv.b"] = lin(3 * c, c)
+    p["proj.w"], p["proj.b"] = lin(c, c)
+    p["mlp1.w"], p["mlp1.b"] = lin(hidden, c)
+    p["mlp2.w"], p["mlp2.b"] = lin(c, hidden)
+    for k in ("ln1", "ln2"):
+        p[k + ".gamma"], p[k + ".beta"] = np.ones(c, np.float32), np.zeros(c, np.float32)
+    return p
+
+
+def block_weight_cache(p):
+    """Quantize the four master weights once (the reference caches weight_q per layer)."""
+    q = dict(p)
+    for k in ("qkv.w", "proj.w", "mlp1.w", "mlp2.w"):
+        q[k] = quantize(p[k])
+    return q
+
+
+def block_forward(p, xq, xs, batch, seq, heads, eps=1e-5):
+    """INT8 data-flow forward; returns ((out_q, out_s), saved) (qlayers.py:329-383).
+
+    ``p`` holds FP32 masters or, via block_weight_cache, cached (codes, scales) weights.
+    """
+    c = xq.shape[1]
+    width = 64 if c % 64 == 0 else BLOCK
+    a1q, a1s, m1_, ss1 = add_forward(xq, xs, np.zeros_like(xq), np.ones_like(xs), width)
+    l1q, l1s, mu1, inv1 = layernorm_forward(a1q, a1s, m1_, ss1, width, p["ln1.gamma"], p["ln1.beta"], eps)
+    qkvq, qkvs = linear_forward(l1q, l1s, p["qkv.w"], p["qkv.b"])
+    att, asave = attention_f32(dequantize(qkvq, qkvs), batch, seq, heads)
+    atq, ats = quantize(att)
+    prq, prs = linear_forward(atq, ats, p["proj.w"], p["proj.b"])
+    hq, hs, m2_, ss2 = add_forward(a1q, a1s, prq, prs, width)
+    l2q, l2s, mu2, inv2 = layernorm_forward(hq, hs, m2_, ss2, width, p["ln2.gamma"], p["ln2.beta"], eps)
+    g1q, g1s = linear_forward(l2q, l2s, p["mlp1.w"], p["mlp1.b"])
+    gq, gs = gelu_forward(g1q, g1s)
+    g2q, g2s = linear_forward(gq, gs, p["mlp2.w"], p["mlp2.b"])
+    oq, os_, _, _ = add_forward(hq, hs, g2q, g2s, width)
+    saved = dict(a1=(a1q, a1s, mu1, inv1), l1=(l1q, l1s), asave=asave, at=(atq, ats), h=(hq, hs, mu2, inv2),
+                 l2=(l2q, l2s), g1=(g1q, g1s), g=(gq, gs), width=width, batch=batch, seq=seq, heads=heads)
+    return (oq, os_), saved
+
+
+def block_backward(p, saved, dyq, dys):
+    """INT8 data-flow backward (qlayers.py:385-427) -> ((dx_q, dx_s), grads)."""
+    w = saved["width"]
+    gq, gs = saved["g"]
+    dgq, dgs, dw_m2, db_m2 = linear_backward(gq, gs, p["mlp2.w"], dyq, dys)
+    g1q, g1s = saved["g1"]
+    dm1q, dm1s = gelu_backward(g1q, g1s, dgq, dgs)
+    l2q, l2s = saved["l2"]
+    dl2q, dl2s, dw_m1, db_m1 = linear_backward(l2q, l2s, p["mlp1.w"], dm1q, dm1s)
+    hq, hs, mu2, inv2 = saved["h"]
+    dhbq, dhbs, dg2, db2 = layernorm_backward(hq, hs, mu2, inv2, dl2q, dl2s, p["ln2.gamma"])
+    dhq, dhs, _, _ = add_forward(dhbq, dhbs, dyq, dys, w)
+    atq, ats = saved["at"]
+    daq, das, dw_pr, db_pr = linear_backward(atq, ats, p["proj.w"], dhq, dhs)
+    dqkv = attention_f32_backward(dequantize(daq, das), saved["asave"], saved["batch"], saved["seq"],
+                                  saved["heads"])
+    dqq, dqs = quantize(dqkv)
+    l1q, l1s = saved["l1"]
+    dl1q, dl1s, dw_qkv, db_qkv = linear_backward(l1q, l1s, p["qkv.w"], dqq, dqs)
+    a1q, a1s, mu1, inv1 = saved["a1"]
+    dabq, dabs, dg1, db1 = layernorm_backward(a1q, a1s, mu1, inv1, dl1q, dl1s, p["ln1.gamma"])
+    dxq, dxs, _, _ = add_forward(dabq, dabs, dhq, dhs, w)
+    grads = {"qkv.w": dw_qkv, "qkv.b": db_qkv, "proj.w": dw_pr, "proj.b": db_pr, "mlp1.w": dw_m1,
+             "mlp1.b": db_m1, "mlp2.w": dw_m2, "mlp2.b": db_m2, "ln1.gamma": dg1, "ln1.beta": db1,
+             "ln2.gamma": dg2, "ln2.beta": db2}
+    return (dxq, dxs), grads

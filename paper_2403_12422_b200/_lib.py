@@ -47,7 +47,8 @@ SIGNATURES = {
     "jf_gemm_fwd": (ctypes.c_int, [_P, _P, _P, _P, _P, _I64, _I64, _I64, _I32, _I32, _P, _P, _P, _P, _P]),
     "jf_gemm_dgrad": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I32, _I32, _P, _P, _P,
                                      _P, _P, _P]),
-    "jf_gemm_wgrad": (ctypes.c_int, [_P, _P, _P, _P, _I64, _I64, _I64, _I32, _I32, _P, _P, _P, _P, _P, _P]),
+    "jf_gemm_wgrad": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I32, _I32, _P, _P, _P, _P, _P,
+                                     _P]),
     "jf_gemm_scratch_bytes": (_SZ, [_I32, _I64, _I64, _I64]),
     "jf_gemm_partials": (ctypes.c_int, [_P, _P, _I64, _I64, _I64, _I64, _P, _P]),
     "jf_add_stats": (ctypes.c_int, [_P, _P, _P, _P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P]),
@@ -103,7 +104,17 @@ def stream_handle() -> int:
     return torch.cuda.current_stream().cuda_stream
 
 
+# kernels each C entry point enqueues (for bench.py's gpu_launches tally)
+KERNELS_PER_CALL = {
+    "quantize": 1, "dequantize": 1, "transpose": 1, "gemm_fwd": 1, "gemm_dgrad": 1, "gemm_wgrad": 1,
+    "gemm_partials": 1, "add_stats": 1, "ln_fwd": 2, "ln_bwd": 4, "gelu_fwd": 1, "gelu_bwd": 1,
+    "colsum": 2, "dropout": 1,
+}
+launch_count = [0]
+
+
 def check(rc: int, what: str) -> None:
+    launch_count[0] += KERNELS_PER_CALL.get(what, 1)
     if rc != 0:
         msg = _lib.jf_last_error().decode(errors="replace") if _lib is not None else ""
         raise RuntimeError(f"libjetfire {what} failed (status {rc}): {msg}")

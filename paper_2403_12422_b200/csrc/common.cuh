@@ -246,6 +246,31 @@ JF_DEV void tmem_fill_32x32b_x32(uint32_t taddr, uint32_t v) {
         : "memory");
 }
 
+// ── packed FP32x2 arithmetic (sm_100 FFMA2 / FMUL2 / FADD2) ───────────
+// Two IEEE fp32 operations per instruction, each correctly rounded exactly
+// like its scalar __f*_rn counterpart (no contraction across the pair).
+JF_DEV void ffma2_rn(float &d0, float &d1, float a0, float a1, float b0, float b1, float c0, float c1) {
+  asm("{\n\t.reg .b64 a, b, c, d;\n\t"
+      "mov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\tmov.b64 c, {%6, %7};\n\t"
+      "fma.rn.f32x2 d, a, b, c;\n\tmov.b64 {%0, %1}, d;\n\t}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
+}
+JF_DEV void fmul2_rn(float &d0, float &d1, float a0, float a1, float b0, float b1) {
+  asm("{\n\t.reg .b64 a, b, d;\n\t"
+      "mov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
+      "mul.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;\n\t}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+JF_DEV void fadd2_rn(float &d0, float &d1, float a0, float a1, float b0, float b1) {
+  asm("{\n\t.reg .b64 a, b, d;\n\t"
+      "mov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
+      "add.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;\n\t}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+
 // ── UMMA descriptors ───────────────────────────────────────────────────
 // Shared-memory matrix descriptor (sm_100 "version 1"), 128B swizzle.
 //   bits [0,14)  start address >> 4

@@ -38,7 +38,6 @@ constexpr int kCtrlWarps = 2;  // TMA warp + MMA warp; epilogue warps use lane q
 constexpr int kThreads = (kCtrlWarps + kEpiWarps) * 32;
 constexpr uint32_t kStageBytesA = BM * BK;
 constexpr uint32_t kStageBytesB = BN * BK;
-constexpr uint32_t kMagic = 0x4B400000u;  // bits of 1.5 * 2**23
 
 enum OutKind { OUT_INT8 = 0, OUT_F32 = 1, OUT_INT8_DEQ = 2, OUT_I32 = 3 };
 
@@ -54,6 +53,7 @@ struct Params {
   float *yf;   // FP32 output (OUT_F32 / OUT_INT8_DEQ) — int32 for OUT_I32
   int32_t *err;
   int out_kind;
+  float zero;  // always 0.0f; opaque to ptxas (blocks FMUL2+FADD2 contraction)
 };
 
 struct Smem {
@@ -66,8 +66,8 @@ struct Smem {
 
 constexpr size_t kSmemBytes = 1024 /*align slack*/ + kStages * (kStageBytesA + kStageBytesB) + 256;
 
-template <bool kFast, bool kMagic>
-__global__ void __maxnreg__(112)
+template <bool kFast>
+__global__ void __maxnreg__(96)
     gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const Params p) {
   extern __shared__ uint8_t smem_raw[];
@@ -103,14 +103,6 @@ __global__ void __maxnreg__(112)
   tc_fence_after();
   const uint32_t tmem = S.tmem_base;
 
-  if (kMagic && warp >= kCtrlWarps) {
-    // preset every TMEM buffer to the int->float magic so the MMA can
-    // accumulate onto it (P + 0x4B400000 == bits of 1.5*2^23 + P)
-    const int lq = warp & 3, cg = (warp - kCtrlWarps) >> 2;
-    for (int b = 0; b < kTmemBufs; ++b)
-      tmem_fill_32x32b_x32(tmem + ((uint32_t)(lq * 32) << 16) + b * BN + cg * 32, kMagic);
-    tmem_wait_st();
-  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -154,7 +146,7 @@ __global__ void __maxnreg__(112)
             tc_fence_after();
             const uint64_t ad = smem_desc_sw128(a0 + c * 32, 16, 1024);
             const uint64_t bd = smem_desc_sw128(b0 + c * 32, 16, 1024);
-            mma_i8_ss(tmem + buf * BN, ad, bd, idesc, kMagic ? 1u : 0u);
+            mma_i8_ss(tmem + buf * BN, ad, bd, idesc, 0u);  // fresh int32 partial per chunk
             mma_commit(&S.tfull[buf]);
           }
           mma_commit(&S.empty[stage]);
@@ -196,10 +188,6 @@ __global__ void __maxnreg__(112)
         const uint32_t taddr = tmem + t_lane + buf * BN + cg * 32;
         tmem_ld_32x32b_x32(taddr, r);
         tmem_wait_ld();
-        if (kMagic) {
-          tmem_fill_32x32b_x32(taddr, kMagic);
-          tmem_wait_st();
-        }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&S.tempty[buf]);
@@ -210,36 +198,26 @@ __global__ void __maxnreg__(112)
 #pragma unroll
             for (int j = 0; j < 32; j += 4)
               *reinterpret_cast<int4 *>(dst + j) =
-                  make_int4((int)(r[j] - (kMagic ? kMagic : 0u)), (int)(r[j + 1] - (kMagic ? kMagic : 0u)),
-                            (int)(r[j + 2] - (kMagic ? kMagic : 0u)), (int)(r[j + 3] - (kMagic ? kMagic : 0u)));
+                  make_int4((int)r[j], (int)r[j + 1], (int)r[j + 2], (int)r[j + 3]);
           }
           continue;
         }
         if (kFast) {
           const float s = __fmul_rn(sa, sb);  // exact: 11 x 11 significant bits
-          if (kMagic) {
-            const float ncs = __fmul_rn(-12582912.0f, s);  // exact
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-              acc[j] = __fadd_rn(acc[j], __fmaf_rn(__uint_as_float(r[j]), s, ncs));
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) acc[j] = __fmaf_rn(__int2float_rn((int)r[j]), s, acc[j]);
-          }
+          for (int j = 0; j < 32; j += 2)
+            ffma2_rn(acc[j], acc[j + 1], __int2float_rn((int)r[j]), __int2float_rn((int)r[j + 1]), s, s,
+                     acc[j], acc[j + 1]);
         } else {
-          if (kMagic) {
-            const float ncs = __fmul_rn(-12582912.0f, sa);  // exact: 2 x 11 bits
+          // packed f32x2, every op an IEEE-rounded fp32 op in the reference order.
+          // ptxas contracts mul.rn.f32x2 + add.rn.f32x2 into FFMA2 (not equivalent);
+          // an fma with a runtime +0 addend is a correctly rounded product it cannot fuse.
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const float t = __fmaf_rn(__uint_as_float(r[j]), sa, ncs);  // == fl(P*sa)
-              acc[j] = __fadd_rn(acc[j], __fmul_rn(t, sb));
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const float t = __fmul_rn(__int2float_rn((int)r[j]), sa);
-              acc[j] = __fadd_rn(acc[j], __fmul_rn(t, sb));
-            }
+          for (int j = 0; j < 32; j += 2) {
+            float t0, t1;
+            fmul2_rn(t0, t1, __int2float_rn((int)r[j]), __int2float_rn((int)r[j + 1]), sa, sa);
+            ffma2_rn(t0, t1, t0, t1, sb, sb, p.zero, p.zero);
+            fadd2_rn(acc[j], acc[j + 1], acc[j], acc[j + 1], t0, t1);
           }
         }
       }
@@ -306,18 +284,6 @@ int jf_num_sms();
 bool jf_make_tmap_i8(CUtensorMap *map, const void *ptr, int64_t rows, int64_t cols, int64_t ld,
                      int box_cols, int box_rows);
 
-static int g_gemm_variant = -1;  // -1: from env JF_GEMM_VARIANT
-
-static int gemm_variant() {
-  if (g_gemm_variant < 0) {
-    const char *e = getenv("JF_GEMM_MAGIC");
-    g_gemm_variant = (e && e[0] == '0') ? 0 : 1;
-  }
-  return g_gemm_variant;
-}
-
-extern "C" void jf_set_gemm_magic(int on) { g_gemm_variant = on ? 1 : 0; }
-
 // Core launcher: A [M x K] (row stride lda), Bt [N x K] (row stride ldb), both K-major codes.
 int jf_gemm_launch(const int8_t *A, int64_t lda, const int8_t *Bt, int64_t ldb, int64_t M,
                    int64_t N, int64_t K, const float *sa, int64_t sa_s0, int64_t sa_s1,
@@ -332,15 +298,13 @@ int jf_gemm_launch(const int8_t *A, int64_t lda, const int8_t *Bt, int64_t ldb, 
   CUtensorMap ta, tb;
   if (!jf_make_tmap_i8(&ta, A, M, K, lda, BK, BM) || !jf_make_tmap_i8(&tb, Bt, N, K, ldb, BK, BN))
     return JF_ERR_LAUNCH;
-  Params p{M, N, K, sa, sa_s0, sa_s1, sb, sb_s0, sb_s1, bias, yq, ys, (float *)yf, err, out_kind};
+  Params p{M, N, K, sa, sa_s0, sa_s1, sb, sb_s0, sb_s1, bias, yq, ys, (float *)yf, err, out_kind, 0.0f};
   const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   const int grid = (int)(tiles < jf_num_sms() ? tiles : jf_num_sms());
-  const bool magic = gemm_variant() == 1;
   const bool fast = mode == JF_MODE_FAST;
-  auto kern = fast ? (magic ? gemm_i8_kernel<true, true> : gemm_i8_kernel<true, false>)
-                   : (magic ? gemm_i8_kernel<false, true> : gemm_i8_kernel<false, false>);
-  static bool attr_done[4] = {false, false, false, false};
-  const int ki = (fast ? 2 : 0) + (magic ? 1 : 0);
+  auto kern = fast ? gemm_i8_kernel<true> : gemm_i8_kernel<false>;
+  static bool attr_done[2] = {false, false};
+  const int ki = fast ? 1 : 0;
   if (!attr_done[ki]) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes) !=
         cudaSuccess)
@@ -383,16 +347,23 @@ extern "C" int jf_gemm_dgrad(const int8_t *dy, const float *dys, const int8_t *w
 }
 
 extern "C" int jf_gemm_wgrad(const int8_t *dy, const float *dys, const int8_t *x, const float *xs,
-                             int64_t n, int64_t d, int64_t c, int32_t mode, int32_t out_kind,
-                             int8_t *dwq, float *dws, float *dwf, void *scratch, int32_t *err,
-                             jf_stream_t stream) {
-  if (scratch == nullptr) return JF_ERR_ARG;
-  int8_t *dyt = static_cast<int8_t *>(scratch);  // [d x n]
-  int8_t *xt = dyt + n * d;                       // [c x n]
-  int rc = jf_transpose(dy, nullptr, n, d, dyt, nullptr, stream);
-  if (rc) return rc;
-  rc = jf_transpose(x, nullptr, n, c, xt, nullptr, stream);
-  if (rc) return rc;
+                             const int8_t *dyt, const int8_t *xt, int64_t n, int64_t d, int64_t c,
+                             int32_t mode, int32_t out_kind, int8_t *dwq, float *dws, float *dwf,
+                             void *scratch, int32_t *err, jf_stream_t stream) {
+  int8_t *s8 = static_cast<int8_t *>(scratch);
+  if (dyt == nullptr) {
+    if (scratch == nullptr) return JF_ERR_ARG;
+    int rc = jf_transpose(dy, nullptr, n, d, s8, nullptr, stream);  // [d x n]
+    if (rc) return rc;
+    dyt = s8;
+  }
+  if (xt == nullptr) {
+    if (scratch == nullptr) return JF_ERR_ARG;
+    int8_t *t = s8 + n * d;
+    int rc = jf_transpose(x, nullptr, n, c, t, nullptr, stream);  // [c x n]
+    if (rc) return rc;
+    xt = t;
+  }
   // A = dY^T [d x n] (K = n): sA(I, ci) = dY.scales[ci, I]; Bt = X^T [c x n]: sB(ci, J) = X.scales[ci, J]
   return jf_gemm_launch(dyt, n, xt, n, d, c, n, dys, 1, d / 32, xs, 1, c / 32, nullptr, mode,
                         out_kind, dwq, dws, dwf, err, (cudaStream_t)stream);

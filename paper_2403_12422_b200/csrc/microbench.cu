@@ -111,6 +111,23 @@ __global__ void __launch_bounds__(512, 1) tmem_kernel(float *out, long long *cyc
       const float s = sa * sb, ncs = -12582912.0f * s;
 #pragma unroll
       for (int j = 0; j < 32; ++j) acc[j] = __fadd_rn(acc[j], __fmaf_rn(__uint_as_float(r[j]), s, ncs));
+    } else if (VARIANT == 6) {  // fast, packed: I2F + FFMA2
+      const float s = sa * sb;
+#pragma unroll
+      for (int j = 0; j < 32; j += 2)
+        ffma2_rn(acc[j], acc[j + 1], __int2float_rn((int)r[j]), __int2float_rn((int)r[j + 1]), s, s,
+                 acc[j], acc[j + 1]);
+    } else if (VARIANT == 7) {  // exact, packed: I2F + FMUL2 + FMUL2 + FADD2
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) {
+        float t0, t1;
+        fmul2_rn(t0, t1, __int2float_rn((int)r[j]), __int2float_rn((int)r[j + 1]), sa, sa);
+        fmul2_rn(t0, t1, t0, t1, sb, sb);
+        fadd2_rn(acc[j], acc[j + 1], acc[j], acc[j + 1], t0, t1);
+      }
+    } else if (VARIANT == 8) {  // I2F only (throughput of the conversion pipe)
+#pragma unroll
+      for (int j = 0; j < 32; ++j) acc[j] = __int_as_float(__float_as_int(acc[j]) ^ __float_as_int(__int2float_rn((int)r[j])));
     } else if (VARIANT == 5) {
       const float ncs = -12582912.0f * sa;
 #pragma unroll
@@ -236,6 +253,9 @@ int main() {
   run_tmem<3>("promote_fast_i2f", d_out, d_cyc);
   run_tmem<4>("promote_fast_magic", d_out, d_cyc);
   run_tmem<5>("promote_exact_magic", d_out, d_cyc);
+  run_tmem<6>("promote_fast_i2f_ffma2", d_out, d_cyc);
+  run_tmem<7>("promote_exact_i2f_packed", d_out, d_cyc);
+  run_tmem<8>("i2f_plus_lop", d_out, d_cyc);
   run_mma<128>(d_cyc);
   run_mma<256>(d_cyc);
   run_mma<64>(d_cyc);

@@ -145,6 +145,46 @@ def micro_mm_16(a, bt):
 _OUT_KIND = {"int8": _lib.OUT_INT8, "f32": _lib.OUT_F32, "int8+deq": _lib.OUT_INT8_DEQ}
 
 
+class GemmTimer:
+    """Records CUDA events around every GEMM kernel launch on the current stream.
+
+    Used by bench.py to measure the dominant kernel live inside the timed
+    region: ``ops`` is the algorithmic work 2*M*N*K per launch.
+    """
+
+    def __init__(self):
+        self.records: list[tuple[str, int, torch.cuda.Event, torch.cuda.Event]] = []
+
+    def __enter__(self):
+        global _TIMER
+        _TIMER = self
+        return self
+
+    def __exit__(self, *exc):
+        global _TIMER
+        _TIMER = None
+
+    def summary(self) -> dict:
+        torch.cuda.synchronize()
+        ms = sum(a.elapsed_time(b) for _, _, a, b in self.records)
+        ops = sum(o for _, o, _, _ in self.records)
+        return {"launches": len(self.records), "ms": ms, "ops": ops}
+
+
+_TIMER: GemmTimer | None = None
+
+
+def _timed(kind: str, ops: int, call):
+    if _TIMER is None:
+        return call()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    rc = call()
+    b.record()
+    _TIMER.records.append((kind, ops, a, b))
+    return rc
+
+
 def _outputs(m: int, n: int, device, out: str):
     yq = ys = yf = None
     if out in ("int8", "int8+deq"):
@@ -192,11 +232,11 @@ def block_mm_forward(xq: BlockQuantTensor, wq: BlockQuantTensor, cfg: TileConfig
         bias = bias if isinstance(bias, torch.Tensor) else torch.as_tensor(np.asarray(bias))
         bias = bias.to(device=xq.device, dtype=torch.float32).contiguous()
     yq, yf = _outputs(xq.rows, wq.rows, xq.device, out)
-    _lib.check(L.jf_gemm_fwd(
+    _lib.check(_timed("fwd", 2 * xq.rows * xq.cols * wq.rows, lambda: L.jf_gemm_fwd(
         xq.values.data_ptr(), xq.scales.data_ptr(), wq.values.data_ptr(), wq.scales.data_ptr(),
         _lib.ptr(bias), xq.rows, xq.cols, wq.rows, _rt.promotion_code(promotion), _OUT_KIND[out],
         _lib.ptr(yq and yq.values), _lib.ptr(yq and yq.scales), _lib.ptr(yf), _rt.err_ptr(),
-        _lib.stream_handle()), "gemm_fwd")
+        _lib.stream_handle())), "gemm_fwd")
     return _finish(yq, yf, mode, out)
 
 
@@ -220,17 +260,14 @@ def block_mm_grad_input(dyq: BlockQuantTensor, wq: BlockQuantTensor, cfg: TileCo
         _count_call(counters, dyq.rows, dyq.cols, wq.cols, cfg, mode, quantize)
     L = _lib.lib()
     n, d, c = dyq.rows, dyq.cols, wq.cols
-    scratch = None
-    if wt is None:
-        scratch = torch.empty(int(L.jf_gemm_scratch_bytes(1, n, d, c)), dtype=torch.uint8,
-                              device=dyq.device)
+    wt_codes = wt.values if wt is not None else transpose_codes(wq.values)
     yq, yf = _outputs(n, c, dyq.device, out)
-    _lib.check(L.jf_gemm_dgrad(
+    _lib.check(_timed("dgrad", 2 * n * d * c, lambda: L.jf_gemm_dgrad(
         dyq.values.data_ptr(), dyq.scales.data_ptr(), wq.values.data_ptr(), wq.scales.data_ptr(),
-        _lib.ptr(wt and wt.values), _lib.ptr(wt and wt.scales), n, d, c,
+        wt_codes.data_ptr(), None, n, d, c,
         _rt.promotion_code(promotion), _OUT_KIND[out], _lib.ptr(yq and yq.values),
-        _lib.ptr(yq and yq.scales), _lib.ptr(yf), _lib.ptr(scratch), _rt.err_ptr(),
-        _lib.stream_handle()), "gemm_dgrad")
+        _lib.ptr(yq and yq.scales), _lib.ptr(yf), None, _rt.err_ptr(),
+        _lib.stream_handle())), "gemm_dgrad")
     return _finish(yq, yf, mode, out)
 
 
@@ -250,15 +287,25 @@ def block_mm_grad_weight(dyq: BlockQuantTensor, xq: BlockQuantTensor, cfg: TileC
         _count_call(counters, dyq.cols, dyq.rows, xq.cols, cfg, mode, quantize)
     L = _lib.lib()
     n, d, c = dyq.rows, dyq.cols, xq.cols
-    scratch = torch.empty(int(L.jf_gemm_scratch_bytes(2, n, d, c)), dtype=torch.uint8,
-                          device=dyq.device)
+    dyt = transpose_codes(dyq.values)   # [d x n]: the K(=tokens)-major operands
+    xt = transpose_codes(xq.values)     # [c x n]
     yq, yf = _outputs(d, c, dyq.device, out)
-    _lib.check(L.jf_gemm_wgrad(
+    _lib.check(_timed("wgrad", 2 * n * d * c, lambda: L.jf_gemm_wgrad(
         dyq.values.data_ptr(), dyq.scales.data_ptr(), xq.values.data_ptr(), xq.scales.data_ptr(),
-        n, d, c, _rt.promotion_code(promotion), _OUT_KIND[out], _lib.ptr(yq and yq.values),
-        _lib.ptr(yq and yq.scales), _lib.ptr(yf), scratch.data_ptr(), _rt.err_ptr(),
-        _lib.stream_handle()), "gemm_wgrad")
+        dyt.data_ptr(), xt.data_ptr(), n, d, c, _rt.promotion_code(promotion), _OUT_KIND[out],
+        _lib.ptr(yq and yq.values), _lib.ptr(yq and yq.scales), _lib.ptr(yf), None, _rt.err_ptr(),
+        _lib.stream_handle())), "gemm_wgrad")
     return _finish(yq, yf, mode, out)
+
+
+def transpose_codes(values: torch.Tensor) -> torch.Tensor:
+    """Transposed int8 codes (libjetfire transpose kernel; scales are read transposed in place)."""
+    L = _lib.lib()
+    n, c = values.shape
+    out = torch.empty((c, n), dtype=torch.int8, device=values.device)
+    _lib.check(L.jf_transpose(values.data_ptr(), None, n, c, out.data_ptr(), None,
+                              _lib.stream_handle()), "transpose")
+    return out
 
 
 def block_partials(a: torch.Tensor, bt: torch.Tensor, kblk: int) -> torch.Tensor:

@@ -160,3 +160,16 @@ def test_layer_golden(golden):
     assert eq(q, g["lin_y_q"]) and eq(s, g["lin_y_s"])
     dq, ds, dw, db = O.linear_backward(g["lin_x_q"], g["lin_x_s"], g["lin_w"], g["lin_dy_q"], g["lin_dy_s"])
     assert eq(dq, g["lin_dx_q"]) and eq(ds, g["lin_dx_s"]) and eq(dw, g["lin_dw"]) and eq(db, g["lin_db"])
+
+
+def test_block_oracle_matches_reference_golden(golden):
+    g = golden("layers")
+    c, heads, hidden, batch, seq = (int(v) for v in g["blk_cfg"])
+    p = {k[6:]: g[k] for k in g.files if k.startswith("blk_p_")}
+    (oq, os_), saved = O.block_forward(p, g["blk_x_q"], g["blk_x_s"], batch, seq, heads)
+    # attention is FP32 numpy in both: identical op order -> bit-identical codes
+    assert eq(oq, g["blk_out_q"]) and eq(os_, g["blk_out_s"])
+    (dq, ds), grads = O.block_backward(p, saved, g["blk_dy_q"], g["blk_dy_s"])
+    assert eq(dq, g["blk_dx_q"]) and eq(ds, g["blk_dx_s"])
+    for k, v in grads.items():
+        np.testing.assert_allclose(v, g["blk_g_" + k], rtol=1e-5, atol=1e-6 * max(1.0, np.abs(v).max()))
