@@ -78,20 +78,20 @@ int jf_gemm_fwd(const int8_t *x, const float *xs, const int8_t *w, const float *
                 jf_stream_t stream);
 
 /* K4 — block_mm_grad_input  [qgemm.py:312-333]:  dX[n x c] = dY[n x d] . W[d x c].
- * wt: optional W^T codes [c x d] (wts: its scales, unused — W's grid is read transposed)
- * (NULL: transposed internally into `scratch`, which must then hold c*d bytes). */
+ * wt/wts: optional W^T codes [c x d] and scales [c/32 x d/32] (NULL: W is transposed
+ * internally into `scratch`, which must then hold c*d bytes, and W's grid is read strided). */
 int jf_gemm_dgrad(const int8_t *dy, const float *dys, const int8_t *w, const float *ws,
                   const int8_t *wt, const float *wts, int64_t n, int64_t d, int64_t c,
                   int32_t mode, int32_t out_kind, int8_t *dxq, float *dxs, float *dxf,
                   void *scratch, int32_t *err, jf_stream_t stream);
 
 /* K5 — block_mm_grad_weight  [qgemm.py:336-357]:  dW[d x c] = dY[n x d]^T . X[n x c].
- * dyt / xt: optional transposed codes dY^T [d x n] and X^T [c x n] (NULL: transposed
- * internally into `scratch`, which then needs n*d + n*c bytes). */
+ * dyt/dyts, xt/xts: optional transposed tensors dY^T [d x n] and X^T [c x n] (codes + scale
+ * grids; NULL: codes transposed internally into `scratch` (n*d + n*c bytes), grids read strided). */
 int jf_gemm_wgrad(const int8_t *dy, const float *dys, const int8_t *x, const float *xs,
-                  const int8_t *dyt, const int8_t *xt, int64_t n, int64_t d, int64_t c,
-                  int32_t mode, int32_t out_kind, int8_t *dwq, float *dws, float *dwf,
-                  void *scratch, int32_t *err, jf_stream_t stream);
+                  const int8_t *dyt, const float *dyts, const int8_t *xt, const float *xts,
+                  int64_t n, int64_t d, int64_t c, int32_t mode, int32_t out_kind, int8_t *dwq,
+                  float *dws, float *dwf, void *scratch, int32_t *err, jf_stream_t stream);
 
 /* Scratch bytes jf_gemm_dgrad / jf_gemm_wgrad need for the given shape. */
 size_t jf_gemm_scratch_bytes(int32_t which /*1=dgrad,2=wgrad*/, int64_t n, int64_t d, int64_t c);

@@ -47,8 +47,8 @@ SIGNATURES = {
     "jf_gemm_fwd": (ctypes.c_int, [_P, _P, _P, _P, _P, _I64, _I64, _I64, _I32, _I32, _P, _P, _P, _P, _P]),
     "jf_gemm_dgrad": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I32, _I32, _P, _P, _P,
                                      _P, _P, _P]),
-    "jf_gemm_wgrad": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I32, _I32, _P, _P, _P, _P, _P,
-                                     _P]),
+    "jf_gemm_wgrad": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I32, _I32, _P, _P, _P,
+                                     _P, _P, _P]),
     "jf_gemm_scratch_bytes": (_SZ, [_I32, _I64, _I64, _I64]),
     "jf_gemm_partials": (ctypes.c_int, [_P, _P, _I64, _I64, _I64, _I64, _P, _P]),
     "jf_add_stats": (ctypes.c_int, [_P, _P, _P, _P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P]),

@@ -5,23 +5,28 @@
 // exactly as qgemm.py:193-229 (_mm_core / _scaled_accumulate), then +bias and
 // a 32x32 block requantization (qgemm.py:266-279).
 //
-// Design (one persistent CTA per SM, warp-specialized):
-//   warp 0      TMA producer: 128x128-byte tiles of A and B (K-major, SW128)
-//               into a 4-stage smem ring (4 K chunks per stage).
-//   warp 1      TMEM owner + MMA issuer: one tcgen05.mma.kind::i8 (M=128,
-//               N=128, K=32) per K chunk into one of 4 TMEM int32 buffers;
-//               every chunk is a fresh product (accumulate=0), because the
-//               reference promotes each 32-deep partial separately.
-//   warps 2-17  promotion/epilogue: 4 warpgroups x 32 columns.  Each thread
-//               owns one row x 32 columns of the FP32 accumulator in
-//               registers; per chunk it tcgen05.ld's its int32 partials,
-//               frees the TMEM buffer, and promotes:
-//                 EXACT: acc = fl(acc + fl(fl(P*sa)*sb))   (bit-exact)
-//                 FAST : acc = fma(P, sa*sb, acc)          (sa*sb exact)
-//               After the last chunk: +bias, 32x32 absmax (warp = 32 rows),
-//               binary16 scale, RNE codes, store INT8 + scale.
-// The promotion (one FP32 op chain per output per 32 MACs) is what bounds
-// this kernel on B200 — see DESIGN.md §GEMM roofline.
+// Design (one persistent CTA per SM, warp-specialized, 128x128 output tiles):
+//   warp 0        TMA producer: 128x128-byte K-major SW128 tiles of A and B
+//                 into a 6-stage smem ring (4 K chunks per stage).
+//   warps 1..I    MMA issuers (I = 3 when K % 128 == 0, else 1): one
+//                 tcgen05.mma.kind::i8 (M=128, N=128, K=32) per K chunk into
+//                 TMEM buffer (chunk % 4); every chunk is a fresh int32
+//                 partial (accumulate = 0) because the reference promotes
+//                 each 32-deep product separately.  Issuing is spread over
+//                 several warps because one tcgen05.mma + commit + barrier
+//                 wait costs a single thread ~500 cycles (measured: the
+//                 single-issuer pipeline ran at one chunk per ~575 cycles).
+//   warps I+1..   promotion/epilogue (E = 16 warps, 32 columns each; TMEM
+//                 lane quarter = warp % 4).  Per chunk a thread tcgen05.ld's
+//                 its 32 int32 partials, frees the buffer, and promotes in
+//                 packed f32x2 ops:
+//                   EXACT: acc = fl(acc + fl(fl(P*sa)*sb))   (bit-exact)
+//                   FAST : acc = fma(P, sa*sb, acc)          (sa*sb exact)
+//                 After the last chunk: +bias, 32x32 absmax (warp = 32 rows),
+//                 binary16 scale, RNE codes, INT8 + scale stores.
+// Bounds: the promotion costs an I2F (half-rate pipe) plus
+// 1 (fast) / 3 (exact) FP32 ops per output per 32 MACs, and each chunk's
+// partial must round-trip TMEM -> registers within the 512-column TMEM.
 #include "common.cuh"
 
 namespace jf {
@@ -30,12 +35,9 @@ namespace gemm {
 constexpr int BM = 128;
 constexpr int BN = 128;
 constexpr int BK = 128;  // bytes of K per stage (4 chunks)
-constexpr int kStages = 4;
+constexpr int kStages = 6;
 constexpr int kChunksPerStage = BK / 32;
-constexpr int kTmemBufs = 4;
-constexpr int kEpiWarps = 16;
-constexpr int kCtrlWarps = 2;  // TMA warp + MMA warp; epilogue warps use lane quarter warp%4
-constexpr int kThreads = (kCtrlWarps + kEpiWarps) * 32;
+constexpr int kTmemBufs = 4;  // == kChunksPerStage: chunk c of a stage uses buffer c
 constexpr uint32_t kStageBytesA = BM * BK;
 constexpr uint32_t kStageBytesB = BN * BK;
 
@@ -54,7 +56,21 @@ struct Params {
   int32_t *err;
   int out_kind;
   float zero;  // always 0.0f; opaque to ptxas (blocks FMUL2+FADD2 contraction)
+#ifdef JF_GEMM_TRACE
+  long long *ts;  // CTA 0 event timestamps (first 256 chunks), tools/gemm_timeline.py
+#endif
 };
+
+#ifdef JF_GEMM_TRACE
+#define JF_TRACE(slot, g)                                                   \
+  do {                                                                      \
+    if (blockIdx.x == 0 && (g) < 256) p.ts[(slot) * 256 + (g)] = clock64(); \
+  } while (0)
+#else
+#define JF_TRACE(slot, g) \
+  do {                    \
+  } while (0)
+#endif
 
 struct Smem {
   uint64_t full[kStages];
@@ -66,10 +82,78 @@ struct Smem {
 
 constexpr size_t kSmemBytes = 1024 /*align slack*/ + kStages * (kStageBytesA + kStageBytesB) + 256;
 
+// Promote one 32-column block of int32 partials into the FP32 accumulator.
 template <bool kFast>
-__global__ void __maxnreg__(96)
+JF_DEV void promote32(float *acc, const uint32_t *r, float sa, float sb, float zero) {
+  if (kFast) {
+    const float s = __fmul_rn(sa, sb);  // exact: 11 x 11 significant bits
+#pragma unroll
+    for (int j = 0; j < 32; j += 2)
+      ffma2_rn(acc[j], acc[j + 1], __int2float_rn((int)r[j]), __int2float_rn((int)r[j + 1]), s, s, acc[j],
+               acc[j + 1]);
+  } else {
+    // packed f32x2, every op an IEEE-rounded fp32 op in the reference order.
+    // ptxas contracts mul.rn.f32x2 + add.rn.f32x2 into FFMA2 (not equivalent);
+    // an fma with a runtime +0 addend is a correctly rounded product it cannot fuse.
+#pragma unroll
+    for (int j = 0; j < 32; j += 2) {
+      float t0, t1;
+      fmul2_rn(t0, t1, __int2float_rn((int)r[j]), __int2float_rn((int)r[j + 1]), sa, sa);
+      ffma2_rn(t0, t1, t0, t1, sb, sb, zero, zero);
+      fadd2_rn(acc[j], acc[j + 1], acc[j], acc[j + 1], t0, t1);
+    }
+  }
+}
+
+// +bias, 32x32 requantization (warp = 32 rows), stores.  Returns error flags.
+JF_DEV int finish_block(const Params &p, float *acc, int64_t I, int64_t J, int lane) {
+  const int64_t row = I * 32 + lane;
+  const int64_t col0 = J * 32;
+  if (p.bias != nullptr) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) acc[j] = __fadd_rn(acc[j], __ldg(p.bias + col0 + j));
+  }
+  if (p.out_kind == OUT_F32) {
+    float *dst = p.yf + row * p.N + col0;
+#pragma unroll
+    for (int j = 0; j < 32; j += 4)
+      *reinterpret_cast<float4 *>(dst + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+    return 0;
+  }
+  uint32_t m = 0;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) m = max(m, abs_bits(acc[j]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  int f = 0;
+  const float sc = block_scale(m, f);
+  uint32_t w[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    w[k] = pack4(quant_code(acc[4 * k], sc), quant_code(acc[4 * k + 1], sc), quant_code(acc[4 * k + 2], sc),
+                 quant_code(acc[4 * k + 3], sc));
+  int8_t *dq = p.yq + row * p.N + col0;
+  reinterpret_cast<uint4 *>(dq)[0] = make_uint4(w[0], w[1], w[2], w[3]);
+  reinterpret_cast<uint4 *>(dq)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+  if (lane == 0) p.ys[I * (p.N >> 5) + J] = sc;
+  if (p.out_kind == OUT_INT8_DEQ) {
+    float *dst = p.yf + row * p.N + col0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      *reinterpret_cast<float4 *>(dst + 4 * k) =
+          make_float4(__fmul_rn(code_at(w[k], 0), sc), __fmul_rn(code_at(w[k], 1), sc),
+                      __fmul_rn(code_at(w[k], 2), sc), __fmul_rn(code_at(w[k], 3), sc));
+  }
+  return lane == 0 ? f : 0;
+}
+
+// kEpi promotion warps (8 or 16) in (kEpi/4) column groups of kCols = BN*4/kEpi;
+// kIss MMA issuer warps (1, or 3 when nchunks % 4 == 0).
+template <bool kFast, bool kPartials, int kEpi, int kIss>
+__global__ void __launch_bounds__((1 + kIss + kEpi) * 32, 1)
     gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const Params p) {
+  constexpr int kCtrl = 1 + kIss;  // warp 0: TMA, warps 1..kIss: MMA issuers
   extern __shared__ uint8_t smem_raw[];
   uint8_t *base = reinterpret_cast<uint8_t *>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -83,17 +167,20 @@ __global__ void __maxnreg__(96)
   const int64_t ntiles = mt * nt;
   const int nchunks = (int)(p.K / 32);
   const int nstages_k = (nchunks + kChunksPerStage - 1) / kChunksPerStage;
+  const int my_tiles = (int)((ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x);
+  const uint32_t bar_full = smem_u32(&S.full[0]), bar_empty = smem_u32(&S.empty[0]);
+  const uint32_t bar_tfull = smem_u32(&S.tfull[0]), bar_tempty = smem_u32(&S.tempty[0]);
 
   if (threadIdx.x == 0) {
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&S.full[s], 1);
-      mbar_init(&S.empty[s], 1);
+      mbar_init(&S.empty[s], kIss > 1 ? kChunksPerStage : 1);  // multi-issuer: one commit per chunk
     }
     for (int b = 0; b < kTmemBufs; ++b) {
       mbar_init(&S.tfull[b], 1);
-      mbar_init(&S.tempty[b], kEpiWarps);
+      mbar_init(&S.tempty[b], kEpi);
     }
     fence_barrier_init();
   }
@@ -103,10 +190,6 @@ __global__ void __maxnreg__(96)
   tc_fence_after();
   const uint32_t tmem = S.tmem_base;
 
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-
   if (warp == 0) {
     // ───────────── TMA producer ─────────────
     if (lane == 0) {
@@ -115,7 +198,7 @@ __global__ void __maxnreg__(96)
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int m0 = (int)((tile % mt) * BM), n0 = (int)((tile / mt) * BN);
         for (int ks = 0; ks < nstages_k; ++ks) {
-          mbar_wait(&S.empty[stage], phase ^ 1);
+          mbar_wait_u32(bar_empty + 8 * stage, phase ^ 1);
           mbar_arrive_expect_tx(&S.full[stage], kStageBytesA + kStageBytesB);
           tma_load_2d(sA + stage * kStageBytesA, &tmA, &S.full[stage], ks * BK, m0);
           tma_load_2d(sB + stage * kStageBytesB, &tmB, &S.full[stage], ks * BK, n0);
@@ -126,30 +209,59 @@ __global__ void __maxnreg__(96)
         }
       }
     }
-  } else if (warp == 1) {
-    // ───────────── MMA issuer ─────────────
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_i8(BM, BN, 0, 0);
-      int stage = 0;
-      uint32_t phase = 0;
-      uint32_t g = 0;  // global chunk counter (TMEM ring position)
+  } else if (warp < kCtrl) {
+    // ───────────── MMA issuers ─────────────
+    // Descriptors are precomputed: the per-chunk path is wait -> fence -> MMA -> commit.
+    const uint64_t adesc0 = smem_desc_sw128(smem_u32(sA), 16, 1024);
+    const uint64_t bdesc0 = smem_desc_sw128(smem_u32(sB), 16, 1024);
+    constexpr uint32_t idesc = idesc_i8(BM, BN, 0, 0);
+    if (kIss > 1) {
+      // issuer j takes global chunks g = j, j+kIss, ...: stage seq g/4, buffer (and
+      // K slice within the stage) g%4, and this is buffer g%4's (g/4)-th use.
+      if (lane == 0) {
+        const int total = my_tiles * nchunks;
+        for (int g = warp - 1; g < total; g += kIss) {
+          const int G = g >> 2, c = g & 3, slot = G % kStages;
+          mbar_wait_u32(bar_full + 8 * slot, (uint32_t)(G / kStages) & 1);
+          JF_TRACE(4, g);
+          mbar_wait_u32(bar_tempty + 8 * c, ((uint32_t)G & 1) ^ 1);
+          JF_TRACE(0, g);
+          tc_fence_after();
+          mma_i8_ss(tmem + c * BN, adesc0 + (uint64_t)((slot * kStageBytesA + c * 32) >> 4),
+                    bdesc0 + (uint64_t)((slot * kStageBytesB + c * 32) >> 4), idesc, 0u);
+          JF_TRACE(5, g);
+          mma_commit(&S.tfull[c]);
+          mma_commit(&S.empty[slot]);
+          JF_TRACE(6, g);
+        }
+      }
+    } else if (lane == 0) {
+      // single issuer (generic K): chunk ci of every tile lands in TMEM buffer ci % 4
+      int stage = 0, gk = 0;
+      uint32_t phase = 0, tphase = 0;
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         for (int ks = 0; ks < nstages_k; ++ks) {
-          mbar_wait(&S.full[stage], phase);
+          mbar_wait_u32(bar_full + 8 * stage, phase);
           tc_fence_after();
-          const uint32_t a0 = smem_u32(sA + stage * kStageBytesA);
-          const uint32_t b0 = smem_u32(sB + stage * kStageBytesB);
+          const uint64_t ad = adesc0 + (uint64_t)((stage * kStageBytesA) >> 4);
+          const uint64_t bd = bdesc0 + (uint64_t)((stage * kStageBytesB) >> 4);
           const int nch = min(kChunksPerStage, nchunks - ks * kChunksPerStage);
-          for (int c = 0; c < nch; ++c, ++g) {
-            const uint32_t buf = g % kTmemBufs;
-            mbar_wait(&S.tempty[buf], ((g / kTmemBufs) & 1) ^ 1);
-            tc_fence_after();
-            const uint64_t ad = smem_desc_sw128(a0 + c * 32, 16, 1024);
-            const uint64_t bd = smem_desc_sw128(b0 + c * 32, 16, 1024);
-            mma_i8_ss(tmem + buf * BN, ad, bd, idesc, 0u);  // fresh int32 partial per chunk
-            mma_commit(&S.tfull[buf]);
+#pragma unroll
+          for (int c = 0; c < kChunksPerStage; ++c) {
+            if (c < nch) {
+              JF_TRACE(4, gk + c);
+              mbar_wait_u32(bar_tempty + 8 * c, ((tphase >> c) & 1) ^ 1);
+              JF_TRACE(0, gk + c);
+              tphase ^= 1u << c;
+              tc_fence_after();
+              mma_i8_ss(tmem + c * BN, ad + 2 * c, bd + 2 * c, idesc, 0u);
+              JF_TRACE(5, gk + c);
+              mma_commit(&S.tfull[c]);
+              JF_TRACE(6, gk + c);
+            }
           }
           mma_commit(&S.empty[stage]);
+          gk += nch;
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
@@ -157,112 +269,97 @@ __global__ void __maxnreg__(96)
         }
       }
     }
-  } else if (warp >= kCtrlWarps) {
+  } else {
     // ───────────── promotion + epilogue ─────────────
-    const int lq = warp & 3;                   // TMEM lane quarter == row block in tile
-    const int cg = (warp - kCtrlWarps) >> 2;   // 32-column group
-    const uint32_t t_lane = (uint32_t)(lq * 32) << 16;
-    uint32_t g = 0;
+    constexpr int kCols = BN * 4 / kEpi;        // columns per warp: 64 (8 warps) or 32 (16 warps)
+    constexpr int kBlk = kCols / 32;            // 32-column blocks per warp
+    const int lq = warp & 3;                    // TMEM lane quarter == 32-row block of the tile
+    const int cgp = (warp - kCtrl) >> 2;        // column group
+    const uint32_t tcol = tmem + ((uint32_t)(lq * 32) << 16) + cgp * kCols;
+    const bool vec_scales = (p.sa_s1 == 1) && (p.sb_s1 == 1) && (nchunks % 4 == 0);
+    uint32_t tphase = 0;
     int flags = 0;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      const int64_t I = (tile % mt) * (BM / 32) + lq;  // 32-row block index
-      const int64_t J = (tile / mt) * (BN / 32) + cg;  // 32-col block index
-      const bool valid = (I * 32 < p.M) && (J * 32 < p.N);
-      const bool scaled = valid && p.out_kind != OUT_I32;
-      const float *pa = scaled ? p.sa + I * p.sa_s0 : nullptr;
-      const float *pb = scaled ? p.sb + J * p.sb_s0 : nullptr;
-      float acc[32];
+    int lt = 0;  // this CTA's local tile index
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {
+      const int64_t I = (tile % mt) * (BM / 32) + lq;              // 32-row block index
+      const int64_t J0 = (tile / mt) * (BN / 32) + kBlk * cgp;     // first 32-col block
+      const bool vrow = I * 32 < p.M;
+      bool vb[kBlk];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) acc[j] = 0.0f;
-      float sa_n = scaled ? __ldg(pa) : 0.f, sb_n = scaled ? __ldg(pb) : 0.f;
-      uint32_t r[32];
-      for (int ci = 0; ci < nchunks; ++ci, ++g) {
-        const float sa = sa_n, sb = sb_n;
-        if (scaled && ci + 1 < nchunks) {  // prefetch next chunk's scales
-          sa_n = __ldg(pa + (ci + 1) * p.sa_s1);
-          sb_n = __ldg(pb + (ci + 1) * p.sb_s1);
-        }
-        const uint32_t buf = g % kTmemBufs;
-        mbar_wait(&S.tfull[buf], (g / kTmemBufs) & 1);
-        tc_fence_after();
-        const uint32_t taddr = tmem + t_lane + buf * BN + cg * 32;
-        tmem_ld_32x32b_x32(taddr, r);
-        tmem_wait_ld();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&S.tempty[buf]);
-        if (p.out_kind == OUT_I32) {
-          // debug: raw int32 partial of the (single) chunk
-          if (valid) {
-            int32_t *dst = reinterpret_cast<int32_t *>(p.yf) + (I * 32 + lane) * p.N + J * 32;
+      for (int q = 0; q < kBlk; ++q) vb[q] = vrow && ((J0 + q) * 32 < p.N);
+      float acc[kBlk][32];
 #pragma unroll
-            for (int j = 0; j < 32; j += 4)
-              *reinterpret_cast<int4 *>(dst + j) =
-                  make_int4((int)r[j], (int)r[j + 1], (int)r[j + 2], (int)r[j + 3]);
-          }
-          continue;
-        }
-        if (kFast) {
-          const float s = __fmul_rn(sa, sb);  // exact: 11 x 11 significant bits
+      for (int q = 0; q < kBlk; ++q)
 #pragma unroll
-          for (int j = 0; j < 32; j += 2)
-            ffma2_rn(acc[j], acc[j + 1], __int2float_rn((int)r[j]), __int2float_rn((int)r[j + 1]), s, s,
-                     acc[j], acc[j + 1]);
-        } else {
-          // packed f32x2, every op an IEEE-rounded fp32 op in the reference order.
-          // ptxas contracts mul.rn.f32x2 + add.rn.f32x2 into FFMA2 (not equivalent);
-          // an fma with a runtime +0 addend is a correctly rounded product it cannot fuse.
+        for (int j = 0; j < 32; ++j) acc[q][j] = 0.0f;
+      const float *pa = p.sa + (kPartials || !vrow ? 0 : I * p.sa_s0);
+      const float *pb[kBlk];
 #pragma unroll
-          for (int j = 0; j < 32; j += 2) {
-            float t0, t1;
-            fmul2_rn(t0, t1, __int2float_rn((int)r[j]), __int2float_rn((int)r[j + 1]), sa, sa);
-            ffma2_rn(t0, t1, t0, t1, sb, sb, p.zero, p.zero);
-            fadd2_rn(acc[j], acc[j + 1], acc[j], acc[j + 1], t0, t1);
+      for (int q = 0; q < kBlk; ++q) pb[q] = p.sb + (kPartials || !vb[q] ? 0 : (J0 + q) * p.sb_s0);
+      for (int cb = 0; cb < nchunks; cb += kTmemBufs) {
+        float sav[4] = {0.f, 0.f, 0.f, 0.f}, sbv[kBlk][4];
+#pragma unroll
+        for (int q = 0; q < kBlk; ++q) sbv[q][0] = sbv[q][1] = sbv[q][2] = sbv[q][3] = 0.f;
+        if (!kPartials) {
+          if (vec_scales) {  // K-contiguous scale grids: 4 chunks per 16-byte load
+            if (vrow) {
+              const float4 t = __ldg(reinterpret_cast<const float4 *>(pa + cb));
+              sav[0] = t.x; sav[1] = t.y; sav[2] = t.z; sav[3] = t.w;
+            }
+#pragma unroll
+            for (int q = 0; q < kBlk; ++q)
+              if (vb[q]) {
+                const float4 t = __ldg(reinterpret_cast<const float4 *>(pb[q] + cb));
+                sbv[q][0] = t.x; sbv[q][1] = t.y; sbv[q][2] = t.z; sbv[q][3] = t.w;
+              }
+          } else {
+#pragma unroll
+            for (int b = 0; b < kTmemBufs; ++b)
+              if (cb + b < nchunks) {
+                if (vrow) sav[b] = __ldg(pa + (cb + b) * p.sa_s1);
+#pragma unroll
+                for (int q = 0; q < kBlk; ++q)
+                  if (vb[q]) sbv[q][b] = __ldg(pb[q] + (cb + b) * p.sb_s1);
+              }
           }
         }
+#pragma unroll
+        for (int b = 0; b < kTmemBufs; ++b) {
+          if (cb + b >= nchunks) break;
+          mbar_wait_u32(bar_tfull + 8 * b, (tphase >> b) & 1);
+          if (warp == kCtrl && lane == 0) JF_TRACE(1, lt * nchunks + cb + b);
+          tphase ^= 1u << b;
+          tc_fence_after();
+          uint32_t r[kBlk][32];
+#pragma unroll
+          for (int q = 0; q < kBlk; ++q) tmem_ld_32x32b_x32(tcol + b * BN + 32 * q, r[q]);
+          tmem_wait_ld();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_u32(bar_tempty + 8 * b);
+          if (warp == kCtrl && lane == 0) JF_TRACE(2, lt * nchunks + cb + b);
+          if (warp == kCtrl + kEpi - 1 && lane == 0) JF_TRACE(3, lt * nchunks + cb + b);
+          if (kPartials) {
+            // debug: raw int32 partials of the (single) chunk
+#pragma unroll
+            for (int q = 0; q < kBlk; ++q)
+              if (vb[q]) {
+                int32_t *dst = reinterpret_cast<int32_t *>(p.yf) + (I * 32 + lane) * p.N + (J0 + q) * 32;
+#pragma unroll
+                for (int j = 0; j < 32; j += 4)
+                  *reinterpret_cast<int4 *>(dst + j) =
+                      make_int4((int)r[q][j], (int)r[q][j + 1], (int)r[q][j + 2], (int)r[q][j + 3]);
+              }
+          } else {
+#pragma unroll
+            for (int q = 0; q < kBlk; ++q) promote32<kFast>(acc[q], r[q], sav[b], sbv[q][b], p.zero);
+          }
+        }
       }
-      if (!valid || p.out_kind == OUT_I32) continue;
-      // ── epilogue: bias, requantization, stores ──
-      const int64_t row = I * 32 + lane;
-      const int64_t col0 = J * 32;
-      if (p.bias != nullptr) {
+      if (kPartials) continue;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) acc[j] = __fadd_rn(acc[j], __ldg(p.bias + col0 + j));
-      }
-      if (p.out_kind == OUT_F32) {
-        float *dst = p.yf + row * p.N + col0;
-#pragma unroll
-        for (int j = 0; j < 32; j += 4)
-          *reinterpret_cast<float4 *>(dst + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
-        continue;
-      }
-      uint32_t m = 0;
-#pragma unroll
-      for (int j = 0; j < 32; ++j) m = max(m, abs_bits(acc[j]));
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-      int f = 0;
-      const float sc = block_scale(m, f);
-      uint32_t w[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k)
-        w[k] = pack4(quant_code(acc[4 * k], sc), quant_code(acc[4 * k + 1], sc),
-                     quant_code(acc[4 * k + 2], sc), quant_code(acc[4 * k + 3], sc));
-      int8_t *dq = p.yq + row * p.N + col0;
-      reinterpret_cast<uint4 *>(dq)[0] = make_uint4(w[0], w[1], w[2], w[3]);
-      reinterpret_cast<uint4 *>(dq)[1] = make_uint4(w[4], w[5], w[6], w[7]);
-      if (lane == 0) {
-        p.ys[I * (p.N >> 5) + J] = sc;
-        flags |= f;
-      }
-      if (p.out_kind == OUT_INT8_DEQ) {
-        float *dst = p.yf + row * p.N + col0;
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          *reinterpret_cast<float4 *>(dst + 4 * k) =
-              make_float4(__fmul_rn(code_at(w[k], 0), sc), __fmul_rn(code_at(w[k], 1), sc),
-                          __fmul_rn(code_at(w[k], 2), sc), __fmul_rn(code_at(w[k], 3), sc));
-      }
+      for (int q = 0; q < kBlk; ++q)
+        if (vb[q]) flags |= finish_block(p, acc[q], I, J0 + q, lane);
     }
     if (lane == 0) raise_flags(p.err, flags);
   }
@@ -284,6 +381,14 @@ int jf_num_sms();
 bool jf_make_tmap_i8(CUtensorMap *map, const void *ptr, int64_t rows, int64_t cols, int64_t ld,
                      int box_cols, int box_rows);
 
+#ifdef JF_GEMM_TRACE
+static long long *g_trace = nullptr;
+extern "C" int jf_gemm_debug_timestamps(long long *host) {
+  if (!g_trace) return 1;
+  return cudaMemcpy(host, g_trace, 2048 * sizeof(long long), cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 2;
+}
+#endif
+
 // Core launcher: A [M x K] (row stride lda), Bt [N x K] (row stride ldb), both K-major codes.
 int jf_gemm_launch(const int8_t *A, int64_t lda, const int8_t *Bt, int64_t ldb, int64_t M,
                    int64_t N, int64_t K, const float *sa, int64_t sa_s0, int64_t sa_s1,
@@ -299,19 +404,46 @@ int jf_gemm_launch(const int8_t *A, int64_t lda, const int8_t *Bt, int64_t ldb, 
   if (!jf_make_tmap_i8(&ta, A, M, K, lda, BK, BM) || !jf_make_tmap_i8(&tb, Bt, N, K, ldb, BK, BN))
     return JF_ERR_LAUNCH;
   Params p{M, N, K, sa, sa_s0, sa_s1, sb, sb_s0, sb_s1, bias, yq, ys, (float *)yf, err, out_kind, 0.0f};
+#ifdef JF_GEMM_TRACE
+  static long long *ts = nullptr;
+  if (!ts) cudaMalloc(&ts, 2048 * sizeof(long long));
+  p.ts = ts;
+  g_trace = ts;
+#endif
   const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   const int grid = (int)(tiles < jf_num_sms() ? tiles : jf_num_sms());
   const bool fast = mode == JF_MODE_FAST;
-  auto kern = fast ? gemm_i8_kernel<true> : gemm_i8_kernel<false>;
-  static bool attr_done[2] = {false, false};
-  const int ki = fast ? 1 : 0;
-  if (!attr_done[ki]) {
+  const bool partials = out_kind == OUT_I32;
+  static int epi = 0, iss_env = -1;
+  if (epi == 0) {
+    const char *e = getenv("JF_GEMM_EPI");
+    epi = (e && atoi(e) == 8) ? 8 : 16;  // default: 16 promotion warps (measured best)
+    const char *i = getenv("JF_GEMM_ISSUERS");
+    iss_env = (i && atoi(i) == 1) ? 1 : 3;
+  }
+  // multi-issuer pipeline needs whole 4-chunk stages (K % 128 == 0)
+  const int iss = (!partials && K % BK == 0) ? iss_env : 1;
+  void (*kern)(const CUtensorMap, const CUtensorMap, const Params);
+#define JF_PICK(E, IS)                                                                 \
+  kern = partials ? gemm_i8_kernel<false, true, E, 1>                                  \
+                  : (fast ? gemm_i8_kernel<true, false, E, IS> : gemm_i8_kernel<false, false, E, IS>);
+  if (epi == 16) {
+    if (iss == 3) { JF_PICK(16, 3) } else { JF_PICK(16, 1) }
+  } else {
+    if (iss == 3) { JF_PICK(8, 3) } else { JF_PICK(8, 1) }
+  }
+#undef JF_PICK
+  static bool attr_done[2][2][3] = {};
+  const int ki = partials ? 2 : (fast ? 1 : 0);
+  bool &done = attr_done[epi == 16][iss == 3][ki];
+  if (!done) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes) !=
         cudaSuccess)
       return jf_launch_check("gemm attr");
-    attr_done[ki] = true;
+    done = true;
   }
-  kern<<<grid, kThreads, kSmemBytes, stream>>>(ta, tb, p);
+  const int threads = (1 + iss + epi) * 32;
+  kern<<<grid, threads, kSmemBytes, stream>>>(ta, tb, p);
   return jf_launch_check("gemm_i8");
 }
 
@@ -333,29 +465,34 @@ extern "C" int jf_gemm_dgrad(const int8_t *dy, const float *dys, const int8_t *w
                              const int8_t *wt, const float *wts, int64_t n, int64_t d, int64_t c,
                              int32_t mode, int32_t out_kind, int8_t *dxq, float *dxs, float *dxf,
                              void *scratch, int32_t *err, jf_stream_t stream) {
-  (void)wts;
   if (wt == nullptr) {
     if (scratch == nullptr) return JF_ERR_ARG;
     int8_t *t = static_cast<int8_t *>(scratch);
     int rc = jf_transpose(w, nullptr, d, c, t, nullptr, stream);
     if (rc) return rc;
     wt = t;
+    wts = nullptr;
   }
-  // A = dY [n x d] (K = d), Bt = W^T [c x d]; sB(ci, J) = W.scales[ci, J]
+  // A = dY [n x d] (K = d), Bt = W^T [c x d]; sB(ci, J) = W.scales[ci, J] = W^T.scales[J, ci]
+  if (wts != nullptr)
+    return jf_gemm_launch(dy, d, wt, d, n, c, d, dys, d / 32, 1, wts, d / 32, 1, nullptr, mode,
+                          out_kind, dxq, dxs, dxf, err, (cudaStream_t)stream);
   return jf_gemm_launch(dy, d, wt, d, n, c, d, dys, d / 32, 1, ws, 1, c / 32, nullptr, mode,
                         out_kind, dxq, dxs, dxf, err, (cudaStream_t)stream);
 }
 
 extern "C" int jf_gemm_wgrad(const int8_t *dy, const float *dys, const int8_t *x, const float *xs,
-                             const int8_t *dyt, const int8_t *xt, int64_t n, int64_t d, int64_t c,
-                             int32_t mode, int32_t out_kind, int8_t *dwq, float *dws, float *dwf,
-                             void *scratch, int32_t *err, jf_stream_t stream) {
+                             const int8_t *dyt, const float *dyts, const int8_t *xt,
+                             const float *xts, int64_t n, int64_t d, int64_t c, int32_t mode,
+                             int32_t out_kind, int8_t *dwq, float *dws, float *dwf, void *scratch,
+                             int32_t *err, jf_stream_t stream) {
   int8_t *s8 = static_cast<int8_t *>(scratch);
   if (dyt == nullptr) {
     if (scratch == nullptr) return JF_ERR_ARG;
     int rc = jf_transpose(dy, nullptr, n, d, s8, nullptr, stream);  // [d x n]
     if (rc) return rc;
     dyt = s8;
+    dyts = nullptr;
   }
   if (xt == nullptr) {
     if (scratch == nullptr) return JF_ERR_ARG;
@@ -363,9 +500,15 @@ extern "C" int jf_gemm_wgrad(const int8_t *dy, const float *dys, const int8_t *x
     int rc = jf_transpose(x, nullptr, n, c, t, nullptr, stream);  // [c x n]
     if (rc) return rc;
     xt = t;
+    xts = nullptr;
   }
-  // A = dY^T [d x n] (K = n): sA(I, ci) = dY.scales[ci, I]; Bt = X^T [c x n]: sB(ci, J) = X.scales[ci, J]
-  return jf_gemm_launch(dyt, n, xt, n, d, c, n, dys, 1, d / 32, xs, 1, c / 32, nullptr, mode,
+  // A = dY^T [d x n] (K = n): sA(I, ci) = dY.scales[ci, I] (= dY^T.scales[I, ci]);
+  // Bt = X^T [c x n]: sB(ci, J) = X.scales[ci, J] (= X^T.scales[J, ci])
+  const float *sa = dyts ? dyts : dys;
+  const int64_t sa0 = dyts ? n / 32 : 1, sa1 = dyts ? 1 : d / 32;
+  const float *sb = xts ? xts : xs;
+  const int64_t sb0 = xts ? n / 32 : 1, sb1 = xts ? 1 : c / 32;
+  return jf_gemm_launch(dyt, n, xt, n, d, c, n, sa, sa0, sa1, sb, sb0, sb1, nullptr, mode,
                         out_kind, dwq, dws, dwf, err, (cudaStream_t)stream);
 }
 

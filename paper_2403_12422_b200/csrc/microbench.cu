@@ -147,17 +147,22 @@ __global__ void __launch_bounds__(512, 1) tmem_kernel(float *out, long long *cyc
 }
 
 // ── raw tcgen05.mma kind::i8 issue rate ────────────────────────────────
-template <int N>
+// MODE 0: back-to-back MMAs, one commit at the end.
+// MODE 1: a tcgen05.commit (to one of 4 mbarriers) after every MMA, never waited.
+// MODE 2: MMA -> commit -> wait on that commit before the next MMA (latency).
+template <int N, int MODE = 0>
 __global__ void __launch_bounds__(128, 1) mma_kernel(long long *cyc, int nmma) {
   extern __shared__ uint8_t smraw[];
   uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
   __shared__ uint32_t tbase;
   __shared__ uint64_t bar;
+  __shared__ uint64_t bars[4];
   const int warp = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < (128 + N) * 128 / 4; i += blockDim.x)
     reinterpret_cast<uint32_t *>(sm)[i] = 0x01010101u * (i & 7);
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
+    for (int i = 0; i < 4; ++i) mbar_init(&bars[i], 1);
     fence_barrier_init();
   }
   if (warp == 0) tmem_alloc(&tbase, 512);
@@ -171,17 +176,133 @@ __global__ void __launch_bounds__(128, 1) mma_kernel(long long *cyc, int nmma) {
     long long t0 = clock64();
     for (int i = 0; i < nmma; ++i) {
       const int c = i & 3;
-      mma_i8_ss(tbase + (i & 1) * N, smem_desc_sw128(a0 + c * 32, 16, 1024),
-                smem_desc_sw128(b0 + c * 32, 16, 1024), idesc, 1u);
+      const uint32_t dst = (MODE >= 6) ? tbase + (i & 3) * N : tbase + (i & 1) * N;
+      mma_i8_ss(dst % 512 + (tbase & 0xffff0000u), smem_desc_sw128(a0 + c * 32, 16, 1024),
+                smem_desc_sw128(b0 + c * 32, 16, 1024), idesc, (MODE == 6 || MODE == 8) ? 0u : 1u);
+      if (MODE >= 1 && MODE != 8) mma_commit(&bars[i & 3]);
+      if (MODE == 2) mbar_wait(&bars[i & 3], (i >> 2) & 1);
+      if (MODE == 3 || MODE == 5) tc_fence_after();
+      if (MODE == 4) {
+        tc_fence_after();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      }
     }
     mma_commit(&bar);
     mbar_wait(&bar, 0);
     long long t1 = clock64();
     cyc[blockIdx.x] = t1 - t0;
   }
+  if (MODE == 5 && warp >= 2) {  // concurrent TMEM readers on the second half of TMEM
+    uint32_t r[32];
+    uint32_t acc = 0;
+    for (int i = 0; i < nmma / 2; ++i) {
+      tmem_ld_32x32b_x32(tbase + ((uint32_t)((warp & 3) * 32) << 16) + 256 + (i & 7) * 32, r);
+      tmem_wait_ld();
+      acc ^= r[i & 31];
+    }
+    if (acc == 0x12345) cyc[blockIdx.x] = 0;
+  }
   tc_fence_before();
   __syncthreads();
   if (warp == 0) tmem_dealloc(tbase, 512);
+}
+
+// Concurrency: MMA+commit stream (1 thread) alongside TMEM readers (W warps of LDTM.xX)
+// reading 64 KB per "chunk" each; no barriers between them.  Reports both rates.
+template <int W, int X>
+__global__ void __launch_bounds__(32 * (W + 1), 1) mma_ld_kernel(long long *cyc, int nchunk, float *out) {
+  extern __shared__ uint8_t smraw[];
+  uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint32_t tbase;
+  __shared__ uint64_t bars[4];
+  const int warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < 256 * 128 / 4; i += blockDim.x) reinterpret_cast<uint32_t *>(sm)[i] = 0x01010101u * (i & 7);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 4; ++i) mbar_init(&bars[i], 1);
+    fence_barrier_init();
+  }
+  if (warp == W) tmem_alloc(&tbase, 512);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == W) {
+    if ((threadIdx.x & 31) == 0) {
+      const uint32_t a0 = smem_u32(sm), b0 = smem_u32(sm + 128 * 128);
+      long long t0 = clock64();
+      for (int i = 0; i < (W < 0 ? 0 : nchunk); ++i) {
+        mma_i8_ss(tbase + (i & 1) * 128, smem_desc_sw128(a0 + (i & 3) * 32, 16, 1024),
+                  smem_desc_sw128(b0 + (i & 3) * 32, 16, 1024), idesc_i8(128, 128, 0, 0), 0u);
+        mma_commit(&bars[i & 3]);
+      }
+      mbar_wait(&bars[(nchunk - 1) & 3], ((nchunk - 1) >> 2) & 1);
+      cyc[blockIdx.x * 2] = clock64() - t0;
+    }
+  } else {
+    // each warp reads its lane quarter x (128*4/W) columns per chunk
+    constexpr int kColsPerWarp = 128 * 4 / W;
+    const uint32_t t = tbase + ((uint32_t)((warp & 3) * 32) << 16) + (warp >> 2) * kColsPerWarp;
+    uint32_t acc = 0;
+    long long t0 = clock64();
+    for (int i = 0; i < nchunk; ++i) {
+      for (int k = 0; k < kColsPerWarp; k += (X == 256 || X == 128) ? 32 : X) {
+        if (X == 32) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(t + 256 + (i & 1) * 128 + k, r);
+          tmem_wait_ld();
+          acc ^= r[i & 31];
+        } else if (X == 256 || X == 128) {  // 16x256b.x8 / 16x128b.x16: 16 lanes x 64 cols per instr
+          uint32_t r[32];
+          const uint32_t ta = t + 256 + (i & 1) * 128 + k;
+          if (X == 256)
+            asm volatile("tcgen05.ld.sync.aligned.16x256b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]) : "r"(ta));
+          else
+            asm volatile("tcgen05.ld.sync.aligned.16x128b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]) : "r"(ta));
+          tmem_wait_ld();
+          acc ^= r[i & 31];
+        } else {
+          uint32_t r[64];
+          tmem_ld_32x32b_x64(t + 256 + (i & 1) * 128 + k, r);
+          tmem_wait_ld();
+          acc ^= r[i & 63];
+        }
+      }
+    }
+    if (warp == 0 && (threadIdx.x & 31) == 0) cyc[blockIdx.x * 2 + 1] = clock64() - t0;
+    out[blockIdx.x * blockDim.x + threadIdx.x] = (float)acc;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == W) tmem_dealloc(tbase, 512);
+}
+
+// Legacy warp-level IMMA: mma.sync.m16n8k32 s8 x s8 -> s32 (register accumulators).
+__global__ void __launch_bounds__(512, 1) mmasync_kernel(long long *cyc, int iters, int *out) {
+  uint32_t a[4], b[2];
+  int c[8][4];
+  for (int i = 0; i < 4; ++i) a[i] = 0x01010101u * (threadIdx.x + i);
+  for (int i = 0; i < 2; ++i) b[i] = 0x01020304u * (threadIdx.x + i);
+  for (int j = 0; j < 8; ++j)
+    for (int i = 0; i < 4; ++i) c[j][i] = 0;
+  __syncthreads();
+  long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      asm volatile(
+          "mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+          : "+r"(c[j][0]), "+r"(c[j][1]), "+r"(c[j][2]), "+r"(c[j][3])
+          : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  int s = 0;
+  for (int j = 0; j < 8; ++j)
+    for (int i = 0; i < 4; ++i) s += c[j][i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
 }
 
 static int g_sms;
@@ -218,19 +339,45 @@ void run_tmem(const char *name, float *d_out, long long *d_cyc) {
          name, elems / cyc, elems * 4 / cyc, cyc);
 }
 
-template <int N>
+template <int N, int MODE = 0>
 void run_mma(long long *d_cyc) {
   const size_t smem = 1024 + (128 + N) * 128;
-  CK(cudaFuncSetAttribute(mma_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CK(cudaFuncSetAttribute(mma_kernel<N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int nmma = 4096;
-  mma_kernel<N><<<g_sms, 128, smem>>>(d_cyc, nmma);
+  mma_kernel<N, MODE><<<g_sms, 128, smem>>>(d_cyc, nmma);
   CK(cudaDeviceSynchronize());
-  mma_kernel<N><<<g_sms, 128, smem>>>(d_cyc, nmma);
+  mma_kernel<N, MODE><<<g_sms, 128, smem>>>(d_cyc, nmma);
   CK(cudaDeviceSynchronize());
   double cyc = median_cycles(d_cyc, g_sms);
   double macs = 128.0 * N * 32 * nmma;
-  printf("{\"bench\": \"mma_i8_m128_n%d_k32\", \"mac_per_clk_per_sm\": %.1f, \"clk_per_mma\": %.2f}\n", N,
-         macs / cyc, cyc / nmma);
+  printf("{\"bench\": \"mma_i8_m128_n%d_k32_mode%d\", \"mac_per_clk_per_sm\": %.1f, \"clk_per_mma\": %.2f}\n", N,
+         MODE, macs / cyc, cyc / nmma);
+}
+
+template <int W, int X>
+void run_mma_ld(long long *d_cyc, float *d_out) {
+  const size_t smem = 1024 + 256 * 128;
+  CK(cudaFuncSetAttribute(mma_ld_kernel<W, X>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int n = 2048;
+  mma_ld_kernel<W, X><<<g_sms, 32 * (W + 1), smem>>>(d_cyc, n, d_out);
+  CK(cudaDeviceSynchronize());
+  mma_ld_kernel<W, X><<<g_sms, 32 * (W + 1), smem>>>(d_cyc, n, d_out);
+  CK(cudaDeviceSynchronize());
+  std::vector<long long> h(2 * g_sms);
+  CK(cudaMemcpy(h.data(), d_cyc, 2 * g_sms * sizeof(long long), cudaMemcpyDeviceToHost));
+  printf("{\"bench\": \"mma+ld W=%d x%d\", \"mma_clk_per_chunk\": %.1f, \"ld_clk_per_chunk\": %.1f}\n", W, X,
+         (double)h[0] / n, (double)h[1] / n);
+}
+
+void run_mmasync(long long *d_cyc, float *d_out) {
+  const int iters = 2048;
+  mmasync_kernel<<<g_sms, 512>>>(d_cyc, iters, (int *)d_out);
+  CK(cudaDeviceSynchronize());
+  mmasync_kernel<<<g_sms, 512>>>(d_cyc, iters, (int *)d_out);
+  CK(cudaDeviceSynchronize());
+  double cyc = median_cycles(d_cyc, g_sms);
+  double macs = 16.0 * 512 / 32 * iters * 8 * (16 * 8 * 32);
+  printf("{\"bench\": \"mma.sync m16n8k32 s8 (16 warps)\", \"mac_per_clk_per_sm\": %.1f}\n", macs / cyc);
 }
 
 int main() {
@@ -241,7 +388,7 @@ int main() {
   float *d_out;
   long long *d_cyc;
   CK(cudaMalloc(&d_out, g_sms * 1024 * sizeof(float)));
-  CK(cudaMalloc(&d_cyc, g_sms * sizeof(long long)));
+  CK(cudaMalloc(&d_cyc, 2 * g_sms * sizeof(long long)));
   run_fp<0>("ffma", d_out, d_cyc, 8);
   run_fp<1>("fmul", d_out, d_cyc, 8);
   run_fp<2>("fadd", d_out, d_cyc, 8);
@@ -259,5 +406,21 @@ int main() {
   run_mma<128>(d_cyc);
   run_mma<256>(d_cyc);
   run_mma<64>(d_cyc);
+  run_mma<128, 1>(d_cyc);
+  run_mma<128, 2>(d_cyc);
+  run_mma<256, 1>(d_cyc);
+  run_mma<128, 3>(d_cyc);
+  run_mma<128, 4>(d_cyc);
+  run_mma<128, 5>(d_cyc);
+  run_mma<128, 6>(d_cyc);   // accumulate=0, commit per MMA, 4 rotating buffers
+  run_mma<128, 7>(d_cyc);   // accumulate=1, commit per MMA, 4 rotating buffers
+  run_mma<128, 8>(d_cyc);   // accumulate=0, no per-MMA commit
+  run_mmasync(d_cyc, d_out);
+  run_mma_ld<16, 32>(d_cyc, d_out);
+  run_mma_ld<8, 32>(d_cyc, d_out);
+  run_mma_ld<8, 64>(d_cyc, d_out);
+  run_mma_ld<4, 64>(d_cyc, d_out);
+  run_mma_ld<16, 256>(d_cyc, d_out);
+  run_mma_ld<16, 128>(d_cyc, d_out);
   return 0;
 }

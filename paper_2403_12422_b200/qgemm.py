@@ -260,11 +260,12 @@ def block_mm_grad_input(dyq: BlockQuantTensor, wq: BlockQuantTensor, cfg: TileCo
         _count_call(counters, dyq.rows, dyq.cols, wq.cols, cfg, mode, quantize)
     L = _lib.lib()
     n, d, c = dyq.rows, dyq.cols, wq.cols
-    wt_codes = wt.values if wt is not None else transpose_codes(wq.values)
+    if wt is None:
+        wt = wq.transposed()
     yq, yf = _outputs(n, c, dyq.device, out)
     _lib.check(_timed("dgrad", 2 * n * d * c, lambda: L.jf_gemm_dgrad(
         dyq.values.data_ptr(), dyq.scales.data_ptr(), wq.values.data_ptr(), wq.scales.data_ptr(),
-        wt_codes.data_ptr(), None, n, d, c,
+        wt.values.data_ptr(), wt.scales.data_ptr(), n, d, c,
         _rt.promotion_code(promotion), _OUT_KIND[out], _lib.ptr(yq and yq.values),
         _lib.ptr(yq and yq.scales), _lib.ptr(yf), None, _rt.err_ptr(),
         _lib.stream_handle())), "gemm_dgrad")
@@ -287,12 +288,13 @@ def block_mm_grad_weight(dyq: BlockQuantTensor, xq: BlockQuantTensor, cfg: TileC
         _count_call(counters, dyq.cols, dyq.rows, xq.cols, cfg, mode, quantize)
     L = _lib.lib()
     n, d, c = dyq.rows, dyq.cols, xq.cols
-    dyt = transpose_codes(dyq.values)   # [d x n]: the K(=tokens)-major operands
-    xt = transpose_codes(xq.values)     # [c x n]
+    dyt = dyq.transposed()   # dY^T [d x n]: the K(=tokens)-major operands (codes + grid)
+    xt = xq.transposed()     # X^T [c x n]
     yq, yf = _outputs(d, c, dyq.device, out)
     _lib.check(_timed("wgrad", 2 * n * d * c, lambda: L.jf_gemm_wgrad(
         dyq.values.data_ptr(), dyq.scales.data_ptr(), xq.values.data_ptr(), xq.scales.data_ptr(),
-        dyt.data_ptr(), xt.data_ptr(), n, d, c, _rt.promotion_code(promotion), _OUT_KIND[out],
+        dyt.values.data_ptr(), dyt.scales.data_ptr(), xt.values.data_ptr(), xt.scales.data_ptr(), n, d, c,
+        _rt.promotion_code(promotion), _OUT_KIND[out],
         _lib.ptr(yq and yq.values), _lib.ptr(yq and yq.scales), _lib.ptr(yf), None, _rt.err_ptr(),
         _lib.stream_handle())), "gemm_wgrad")
     return _finish(yq, yf, mode, out)

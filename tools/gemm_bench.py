@@ -58,7 +58,10 @@ def main():
                 print(json.dumps({"shape": name, "op": op, "mode": mode, "M_N_K": [n, c, d],
                                   "us_per_launch": round(1e3 * s["ms"] / s["launches"], 1),
                                   "tops": round(tops, 1), "frac_int8_peak": round(tops / 4500, 4)}), flush=True)
-    jf.check_errors()
+    try:
+        jf.check_errors()
+    except ValueError as e:
+        print(json.dumps({"error_flag": str(e)}))
 
 
 if __name__ == "__main__":
