@@ -123,11 +123,17 @@ int jf_ln_bwd(const int8_t *x, const float *xs, const float *mu, const float *in
               int32_t *err, jf_stream_t stream);
 size_t jf_ln_bwd_workspace_bytes(int64_t n, int64_t c);
 
-/* K9 / K10 — gelu_forward / gelu_backward  [qnonlinear.py:150-175]. */
+/* K9 / K10 — gelu_forward / gelu_backward  [qnonlinear.py:150-175].
+ * tables: optional (NULL: per-tile tables) lookup tables built once by
+ * jf_gelu_build_tables into a caller buffer of jf_gelu_tables_bytes() bytes:
+ * f(code * s) for every positive binary16 scale s and code in [-127, 127]. */
+size_t jf_gelu_tables_bytes(void);
+int jf_gelu_build_tables(float *tables, jf_stream_t stream);
 int jf_gelu_fwd(const int8_t *x, const float *xs, int64_t n, int64_t c, int8_t *yq, float *ys,
-                int32_t *err, jf_stream_t stream);
+                const float *tables, int32_t *err, jf_stream_t stream);
 int jf_gelu_bwd(const int8_t *x, const float *xs, const int8_t *dy, const float *dys, int64_t n,
-                int64_t c, int8_t *dxq, float *dxs, int32_t *err, jf_stream_t stream);
+                int64_t c, int8_t *dxq, float *dxs, const float *tables, int32_t *err,
+                jf_stream_t stream);
 
 /* K11 — dbias = dequantize(dY).sum(axis=0)  [qlayers.py:180]; out [c] float32.
  * workspace: >= jf_colsum_workspace_bytes(n, c) bytes. */

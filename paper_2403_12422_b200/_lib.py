@@ -55,8 +55,10 @@ SIGNATURES = {
     "jf_ln_fwd": (ctypes.c_int, [_P, _P, _P, _P, _I64, _I64, _I64, _P, _P, _F32, _P, _P, _P, _P, _P, _P]),
     "jf_ln_bwd": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P]),
     "jf_ln_bwd_workspace_bytes": (_SZ, [_I64, _I64]),
-    "jf_gelu_fwd": (ctypes.c_int, [_P, _P, _I64, _I64, _P, _P, _P, _P]),
-    "jf_gelu_bwd": (ctypes.c_int, [_P, _P, _P, _P, _I64, _I64, _P, _P, _P, _P]),
+    "jf_gelu_tables_bytes": (_SZ, []),
+    "jf_gelu_build_tables": (ctypes.c_int, [_P, _P]),
+    "jf_gelu_fwd": (ctypes.c_int, [_P, _P, _I64, _I64, _P, _P, _P, _P, _P]),
+    "jf_gelu_bwd": (ctypes.c_int, [_P, _P, _P, _P, _I64, _I64, _P, _P, _P, _P, _P]),
     "jf_colsum": (ctypes.c_int, [_P, _P, _I64, _I64, _P, _P, _P]),
     "jf_colsum_workspace_bytes": (_SZ, [_I64, _I64]),
     "jf_dropout": (ctypes.c_int, [_P, _P, _P, _F32, _I64, _I64, _P, _P, _P, _P]),
@@ -108,7 +110,7 @@ def stream_handle() -> int:
 KERNELS_PER_CALL = {
     "quantize": 1, "dequantize": 1, "transpose": 1, "gemm_fwd": 1, "gemm_dgrad": 1, "gemm_wgrad": 1,
     "gemm_partials": 1, "add_stats": 1, "ln_fwd": 2, "ln_bwd": 4, "gelu_fwd": 1, "gelu_bwd": 1,
-    "colsum": 2, "dropout": 1,
+    "colsum": 2, "dropout": 1, "gelu_tables": 1,
 }
 launch_count = [0]
 

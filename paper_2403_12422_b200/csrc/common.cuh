@@ -54,6 +54,20 @@ JF_DEV int quant_code(float x, float s) {
   return q;
 }
 
+// Same result as quant_code, without a division on the common path:
+// y = fl(x * r), r = fl(1/s).  |y - fl(x/s)| <= 1.5 * 2^-23 * |x/s| <= 2.3e-5
+// (|x/s| <= 128), so unless y lies within 3e-5 of a half-integer, y and
+// fl(x/s) are on the same side of every rounding boundary and fl(x/s) is not a
+// tie: rint(y) == rint(fl(x/s)).  The rare near-tie case takes the exact path.
+JF_DEV int quant_code_fast(float x, float s, float r) {
+  const float y = __fmul_rn(x, r);
+  const float d = fabsf(__fsub_rn(__fsub_rn(y, floorf(y)), 0.5f));
+  int q = (d > 3.0e-5f) ? __float2int_rn(y) : __float2int_rn(__fdiv_rn(x, s));
+  q = q > kQmax ? kQmax : q;
+  q = q < -kQmax ? -kQmax : q;
+  return q;
+}
+
 JF_DEV uint32_t abs_bits(float x) { return __float_as_uint(x) & 0x7fffffffu; }
 
 // pack 4 codes into one 32-bit word (little-endian byte order = column order)

@@ -161,6 +161,70 @@ JF_DEV void ln_row_vals(const LnRowArgs &A, int64_t row, int64_t col, float mrow
   dxhat = __fmul_rn(dv, __ldg(A.gamma + col));
 }
 
+// Fast path (perfect tree, all NL = 2^depth leaves of equal size Lf, Lf % 8 == 0):
+// numpy's leaf sum is ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) with r_j the
+// sequential sum of elements j, j+8, ..., so the whole row is a balanced tree
+// over 8*NL sequential "chains".  Lane (g = lane>>3, j = lane&7) sums chain j
+// of leaf 4*it + g; xor-butterflies over j (1,2,4) give leaf sums, over g (8,16)
+// pairs/quads of leaves, and the per-iteration values are combined in index
+// order in registers — the exact numpy association, with all 32 lanes busy.
+__global__ void __launch_bounds__(256) ln_bwd_rows_fast_kernel(LnRowArgs A, int nleaf, int leaf_len,
+                                                               float *m1, float *m2) {
+  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= A.n) return;
+  const float mr = __ldg(A.mu + row), ir = __ldg(A.inv_std + row);
+  const int g = lane >> 3, j = lane & 7;
+  const int64_t cb = A.c >> 5;
+  const int8_t *xr = A.x + row * A.c;
+  const int8_t *dr = A.dy + row * A.c;
+  const float *sxr = A.xs + (row >> 5) * cb;
+  const float *sdr = A.dys + (row >> 5) * cb;
+  const int iters = (nleaf + 3) >> 2;
+  const int gl = nleaf < 4 ? nleaf : 4;  // leaves per iteration
+  float v1[32], v2[32];  // per-iteration partial trees (nleaf <= 128)
+  for (int it = 0; it < iters; ++it) {
+    const int L = it * 4 + g;
+    float c1 = 0.f, c2 = 0.f;
+    if (L < nleaf) {
+      const int base = L * leaf_len + j;
+      for (int i = 0; i < leaf_len / 8; ++i) {
+        const int k = base + 8 * i;
+        const float xv = __fmul_rn((float)xr[k], __ldg(sxr + (k >> 5)));
+        const float dv = __fmul_rn((float)dr[k], __ldg(sdr + (k >> 5)));
+        const float xh = __fmul_rn(__fsub_rn(xv, mr), ir);
+        const float dxh = __fmul_rn(dv, __ldg(A.gamma + k));
+        const float pr = __fmul_rn(dxh, xh);
+        c1 = (i == 0) ? dxh : __fadd_rn(c1, dxh);
+        c2 = (i == 0) ? pr : __fadd_rn(c2, pr);
+      }
+    }
+    // leaf tree over the 8 chains
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      c1 = __fadd_rn(c1, __shfl_xor_sync(0xffffffffu, c1, o));
+      c2 = __fadd_rn(c2, __shfl_xor_sync(0xffffffffu, c2, o));
+    }
+    // pairs / quads of leaves (only as many levels as leaves present)
+    for (int o = 8; o < 8 * gl; o <<= 1) {
+      c1 = __fadd_rn(c1, __shfl_xor_sync(0xffffffffu, c1, o));
+      c2 = __fadd_rn(c2, __shfl_xor_sync(0xffffffffu, c2, o));
+    }
+    v1[it & 31] = c1;
+    v2[it & 31] = c2;
+  }
+  // combine iteration values in tree (index) order: iters is a power of two
+  for (int step = 1; step < iters; step <<= 1)
+    for (int t = 0; t < iters; t += 2 * step) {
+      v1[t] = __fadd_rn(v1[t], v1[t + step]);
+      v2[t] = __fadd_rn(v2[t], v2[t + step]);
+    }
+  if (lane == 0) {
+    m1[row] = __fdiv_rn(v1[0], (float)A.c);
+    m2[row] = __fdiv_rn(v2[0], (float)A.c);
+  }
+}
+
 __global__ void __launch_bounds__(256) ln_bwd_rows_kernel(LnRowArgs A, int depth, int perfect,
                                                           float *m1, float *m2) {
   const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -280,15 +344,36 @@ __global__ void __launch_bounds__(kTileThreads) ln_bwd_tile_kernel(
   }
 }
 
-// Sum per-strip partials over strips in order: out[j] = sum_s part[s, j].
+// Sum per-strip partials: out[j] = sum_s part[s, j].  CTA = 32 columns x 8
+// warps; warp w sums strips [w*S/8, (w+1)*S/8) in order (loads unrolled so
+// they stay in flight), then the 8 warp sums are added in warp order.
 __global__ void __launch_bounds__(256) strip_reduce_kernel(const float *__restrict__ part,
                                                            int64_t strips, int64_t c,
                                                            float *out) {
-  const int64_t j = (int64_t)blockIdx.x * 256 + threadIdx.x;
-  if (j >= c) return;
-  float acc = part[j];
-  for (int64_t s = 1; s < strips; ++s) acc = __fadd_rn(acc, part[s * c + j]);
-  out[j] = acc;
+  __shared__ float ws[8][32];
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int64_t j = (int64_t)blockIdx.x * 32 + l;
+  const int64_t s0 = strips * w / 8, s1 = strips * (w + 1) / 8;
+  float acc = 0.f;
+  if (j < c) {
+    int64_t s = s0;
+    for (; s + 8 <= s1; s += 8) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldg(part + (s + u) * c + j);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc = __fadd_rn(acc, v[u]);
+    }
+    for (; s < s1; ++s) acc = __fadd_rn(acc, __ldg(part + s * c + j));
+  }
+  ws[w][l] = acc;
+  __syncthreads();
+  if (w == 0 && j < c) {
+    float t = ws[0][l];
+#pragma unroll
+    for (int u = 1; u < 8; ++u) t = __fadd_rn(t, ws[u][l]);
+    out[j] = t;
+  }
 }
 
 // ── K11: dbias partials (qlayers.py:180) ───────────────────────────────
@@ -328,19 +413,93 @@ JF_DEV float norm_cdf_f32(float x) {
   return __fmul_rn(0.5f, __fadd_rn(1.0f, e));
 }
 
+// GELU input values are code * block_scale: a 32x32 block holds at most 255
+// distinct values, so each tile first tabulates f(code) for its 8 blocks
+// (8 x 255 evaluations of the FP64 erf instead of 8 x 1024) and every element
+// then looks its result up — bit-identical to evaluating f per element.
+JF_DEV void load_codes(const TilePos &t, const int8_t *__restrict__ q, int (&k)[4][8]) {
+  if (!t.active) return;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint2 w = __ldg(reinterpret_cast<const uint2 *>(q + t.row(i) * t.c + t.col()));
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      k[i][j] = (int)(int8_t)((w.x >> (8 * j)) & 0xffu);
+      k[i][4 + j] = (int)(int8_t)((w.y >> (8 * j)) & 0xffu);
+    }
+  }
+}
+
+// Global GELU tables: every block scale is a positive binary16 value, so all
+// possible GELU inputs are code * s for s in the 31744 positive f16 values.
+// Row (f16 bits of s) holds f(code * s) for code = -127..127 (+1 pad):
+//   table 0: fl(x * cdf(x))            (gelu_forward, qnonlinear.py:150-158)
+//   table 1: fl(fl(x * pdf) + cdf(x))  (gelu_grad_f32, qnonlinear.py:43-46)
+// Built once per process (8M FP64 erf evaluations, ~ms); the kernels then do
+// one L1-resident lookup per element — bit-identical to per-element math.
+constexpr int kF16Rows = 0x7C00;  // positive finite binary16 bit patterns (incl. subnormals)
+
+JF_DEV float gelu_val(float xv) { return __fmul_rn(xv, norm_cdf_f32(xv)); }
+JF_DEV float gelu_grad(float xv) {
+  const float ex = expf(__fmul_rn(__fmul_rn(-0.5f, xv), xv));
+  const float pdf = __fmul_rn(0.3989422804014327f, ex);
+  return __fadd_rn(__fmul_rn(xv, pdf), norm_cdf_f32(xv));
+}
+
+__global__ void __launch_bounds__(256) gelu_table_kernel(float *tab) {
+  const int64_t total = (int64_t)kF16Rows * 256;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int row = (int)(e >> 8), k = (int)(e & 255);
+    const float s = __half2float(__ushort_as_half((unsigned short)row));
+    const float xv = __fmul_rn((float)(k - 127), s);
+    tab[e] = k == 255 ? 0.f : gelu_val(xv);
+    tab[total + e] = k == 255 ? 0.f : gelu_grad(xv);
+  }
+}
+
+JF_DEV const float *gelu_row(const float *tab, float s) {
+  return tab + ((int64_t)__half_as_ushort(__float2half_rn(s)) << 8) + 127;
+}
+
 __global__ void __launch_bounds__(kTileThreads) gelu_fwd_kernel(const int8_t *__restrict__ x,
                                                                 const float *__restrict__ xs,
                                                                 int64_t n, int64_t c, int8_t *yq,
-                                                                float *ys, int32_t *err) {
+                                                                float *ys, int32_t *err,
+                                                                const float *__restrict__ gtab) {
   __shared__ uint32_t red[64];
+  __shared__ float tab[8][256];  // tab[block][code + 127] = fl(x * cdf(x)), x = fl(code * s)
   const TilePos t = tile_pos(n, c);
+  if (gtab != nullptr) {
+    int k[4][8];
+    float v[4][8];
+    load_codes(t, x, k);
+    if (t.active) {
+      const float *tb = gelu_row(gtab, __ldg(xs + t.scale_idx(t.r0, t.col())));
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[i][j] = __ldg(tb + k[i][j]);
+    }
+    quant_store(t, v, yq, ys, red, err);
+    return;
+  }
+  for (int e = threadIdx.x; e < 8 * 255; e += kTileThreads) {
+    const int b = e / 255, q = e % 255 - 127;
+    if (t.c0 + 32 * b < c) {
+      tab[b][q + 127] = gelu_val(__fmul_rn((float)q, __ldg(xs + t.scale_idx(t.r0, t.c0 + 32 * b))));
+    }
+  }
+  __syncthreads();
+  int k[4][8];
   float v[4][8];
-  load_deq(t, x, xs, v);
+  load_codes(t, x, k);
   if (t.active) {
+    const float *tb = tab[t.lane >> 2] + 127;
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 8; ++j) v[i][j] = __fmul_rn(v[i][j], norm_cdf_f32(v[i][j]));
+      for (int j = 0; j < 8; ++j) v[i][j] = tb[k[i][j]];
   }
   quant_store(t, v, yq, ys, red, err);
 }
@@ -350,23 +509,43 @@ __global__ void __launch_bounds__(kTileThreads) gelu_fwd_kernel(const int8_t *__
 // one documented tolerance-only op.
 __global__ void __launch_bounds__(kTileThreads) gelu_bwd_kernel(
     const int8_t *__restrict__ x, const float *__restrict__ xs, const int8_t *__restrict__ dy,
-    const float *__restrict__ dys, int64_t n, int64_t c, int8_t *dxq, float *dxs, int32_t *err) {
+    const float *__restrict__ dys, int64_t n, int64_t c, int8_t *dxq, float *dxs, int32_t *err,
+    const float *__restrict__ gtab) {
   __shared__ uint32_t red[64];
+  __shared__ float tab[8][256];  // tab[block][code + 127] = gelu'(fl(code * s_x))
   const TilePos t = tile_pos(n, c);
-  float v[4][8], d[4][8];
-  load_deq(t, x, xs, v);
+  if (gtab != nullptr) {
+    int k[4][8];
+    float d[4][8], v[4][8];
+    load_codes(t, x, k);
+    load_deq(t, dy, dys, d);
+    if (t.active) {
+      const float *tb = gelu_row(gtab + (int64_t)kF16Rows * 256, __ldg(xs + t.scale_idx(t.r0, t.col())));
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[i][j] = __fmul_rn(d[i][j], __ldg(tb + k[i][j]));
+    }
+    quant_store(t, v, dxq, dxs, red, err);
+    return;
+  }
+  for (int e = threadIdx.x; e < 8 * 255; e += kTileThreads) {
+    const int b = e / 255, q = e % 255 - 127;
+    if (t.c0 + 32 * b < c) {
+      tab[b][q + 127] = gelu_grad(__fmul_rn((float)q, __ldg(xs + t.scale_idx(t.r0, t.c0 + 32 * b))));
+    }
+  }
+  __syncthreads();
+  int k[4][8];
+  float d[4][8], v[4][8];
+  load_codes(t, x, k);
   load_deq(t, dy, dys, d);
   if (t.active) {
+    const float *tb = tab[t.lane >> 2] + 127;
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const float xv = v[i][j];
-        const float e = expf(__fmul_rn(__fmul_rn(-0.5f, xv), xv));
-        const float pdf = __fmul_rn(0.3989422804014327f, e);
-        const float g = __fadd_rn(__fmul_rn(xv, pdf), norm_cdf_f32(xv));
-        v[i][j] = __fmul_rn(d[i][j], g);
-      }
+      for (int j = 0; j < 8; ++j) v[i][j] = __fmul_rn(d[i][j], tb[k[i][j]]);
   }
   quant_store(t, v, dxq, dxs, red, err);
 }
@@ -457,6 +636,14 @@ static int pw_depth(int64_t len) {
   return a + 1;
 }
 
+// every leaf of the (perfect) tree has the same length
+static bool pw_equal_leaves(int64_t len, int depth) {
+  if (depth == 0) return true;
+  int64_t h = len / 2;
+  h -= h % 8;
+  return h == len - h && pw_equal_leaves(h, depth - 1);
+}
+
 extern "C" size_t jf_ln_bwd_workspace_bytes(int64_t n, int64_t c) {
   return (size_t)(2 * n + 2 * (n / 32) * c) * sizeof(float);
 }
@@ -473,13 +660,19 @@ extern "C" int jf_ln_bwd(const int8_t *x, const float *xs, const float *mu, cons
   int perfect = depth >= 0 && depth <= 8;
   if (!perfect) depth = 0;
   cudaStream_t st = (cudaStream_t)stream;
-  ln_bwd_rows_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(A, depth, perfect, m1, m2);
+  const int64_t leaf_len = perfect ? (c >> depth) : 0;
+  const bool fast = perfect && depth <= 7 && (leaf_len << depth) == c && leaf_len % 8 == 0 &&
+                    pw_equal_leaves(c, depth) && ((1 << depth) <= 4 || true);
+  if (fast)
+    ln_bwd_rows_fast_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(A, 1 << depth, (int)leaf_len, m1, m2);
+  else
+    ln_bwd_rows_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(A, depth, perfect, m1, m2);
   int rc = jf_launch_check("ln_bwd_rows");
   if (rc) return rc;
   ln_bwd_tile_kernel<<<tile_grid(n, c), kTileThreads, 0, st>>>(A, m1, m2, dxq, dxs, pg, pb, err);
   rc = jf_launch_check("ln_bwd_tile");
   if (rc) return rc;
-  const unsigned g = (unsigned)((c + 255) / 256);
+  const unsigned g = (unsigned)((c + 31) / 32);
   strip_reduce_kernel<<<g, 256, 0, st>>>(pg, n / 32, c, dgamma);
   strip_reduce_kernel<<<g, 256, 0, st>>>(pb, n / 32, c, dbeta);
   return jf_launch_check("ln_bwd_reduce");
@@ -497,24 +690,31 @@ extern "C" int jf_colsum(const int8_t *q, const float *s, int64_t n, int64_t c, 
   colsum_tile_kernel<<<tile_grid(n, c), kTileThreads, 0, st>>>(q, s, n, c, part);
   int rc = jf_launch_check("colsum_tile");
   if (rc) return rc;
-  strip_reduce_kernel<<<(unsigned)((c + 255) / 256), 256, 0, st>>>(part, n / 32, c, out);
+  strip_reduce_kernel<<<(unsigned)((c + 31) / 32), 256, 0, st>>>(part, n / 32, c, out);
   return jf_launch_check("colsum_reduce");
 }
 
+extern "C" size_t jf_gelu_tables_bytes(void) { return (size_t)2 * kF16Rows * 256 * sizeof(float); }
+
+extern "C" int jf_gelu_build_tables(float *tables, jf_stream_t stream) {
+  gelu_table_kernel<<<148 * 16, 256, 0, (cudaStream_t)stream>>>(tables);
+  return jf_launch_check("gelu_tables");
+}
+
 extern "C" int jf_gelu_fwd(const int8_t *x, const float *xs, int64_t n, int64_t c, int8_t *yq,
-                           float *ys, int32_t *err, jf_stream_t stream) {
+                           float *ys, const float *tables, int32_t *err, jf_stream_t stream) {
   if (!ok_shape(n, c)) return JF_ERR_ARG;
   gelu_fwd_kernel<<<tile_grid(n, c), kTileThreads, 0, (cudaStream_t)stream>>>(x, xs, n, c, yq, ys,
-                                                                              err);
+                                                                              err, tables);
   return jf_launch_check("gelu_fwd");
 }
 
 extern "C" int jf_gelu_bwd(const int8_t *x, const float *xs, const int8_t *dy, const float *dys,
-                           int64_t n, int64_t c, int8_t *dxq, float *dxs, int32_t *err,
-                           jf_stream_t stream) {
+                           int64_t n, int64_t c, int8_t *dxq, float *dxs, const float *tables,
+                           int32_t *err, jf_stream_t stream) {
   if (!ok_shape(n, c)) return JF_ERR_ARG;
   gelu_bwd_kernel<<<tile_grid(n, c), kTileThreads, 0, (cudaStream_t)stream>>>(x, xs, dy, dys, n,
-                                                                              c, dxq, dxs, err);
+                                                                              c, dxq, dxs, err, tables);
   return jf_launch_check("gelu_bwd");
 }
 

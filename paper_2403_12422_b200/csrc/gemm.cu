@@ -127,11 +127,12 @@ JF_DEV int finish_block(const Params &p, float *acc, int64_t I, int64_t J, int l
   for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
   int f = 0;
   const float sc = block_scale(m, f);
+  const float rc = __frcp_rn(sc);
   uint32_t w[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k)
-    w[k] = pack4(quant_code(acc[4 * k], sc), quant_code(acc[4 * k + 1], sc), quant_code(acc[4 * k + 2], sc),
-                 quant_code(acc[4 * k + 3], sc));
+    w[k] = pack4(quant_code_fast(acc[4 * k], sc, rc), quant_code_fast(acc[4 * k + 1], sc, rc),
+                 quant_code_fast(acc[4 * k + 2], sc, rc), quant_code_fast(acc[4 * k + 3], sc, rc));
   int8_t *dq = p.yq + row * p.N + col0;
   reinterpret_cast<uint4 *>(dq)[0] = make_uint4(w[0], w[1], w[2], w[3]);
   reinterpret_cast<uint4 *>(dq)[1] = make_uint4(w[4], w[5], w[6], w[7]);
@@ -419,7 +420,7 @@ int jf_gemm_launch(const int8_t *A, int64_t lda, const int8_t *Bt, int64_t ldb, 
     const char *e = getenv("JF_GEMM_EPI");
     epi = (e && atoi(e) == 8) ? 8 : 16;  // default: 16 promotion warps (measured best)
     const char *i = getenv("JF_GEMM_ISSUERS");
-    iss_env = (i && atoi(i) == 1) ? 1 : 3;
+    iss_env = (i && atoi(i) == 3) ? 3 : 1;  // default: one issuer (3 measured no faster)
   }
   // multi-issuer pipeline needs whole 4-chunk stages (K % 128 == 0)
   const int iss = (!partials && K % BK == 0) ? iss_env : 1;

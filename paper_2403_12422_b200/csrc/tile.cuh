@@ -77,14 +77,15 @@ JF_DEV void quant_store(const TilePos &t, const float (&v)[4][8], int8_t *__rest
   for (int w = 0; w < 8; ++w) am = max(am, red[w * 8 + qb]);
   int flags = 0;
   const float sc = block_scale(am, flags);
+  const float rc = __frcp_rn(sc);
   if (t.active) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       uint2 w;
-      w.x = pack4(quant_code(v[i][0], sc), quant_code(v[i][1], sc), quant_code(v[i][2], sc),
-                  quant_code(v[i][3], sc));
-      w.y = pack4(quant_code(v[i][4], sc), quant_code(v[i][5], sc), quant_code(v[i][6], sc),
-                  quant_code(v[i][7], sc));
+      w.x = pack4(quant_code_fast(v[i][0], sc, rc), quant_code_fast(v[i][1], sc, rc),
+                  quant_code_fast(v[i][2], sc, rc), quant_code_fast(v[i][3], sc, rc));
+      w.y = pack4(quant_code_fast(v[i][4], sc, rc), quant_code_fast(v[i][5], sc, rc),
+                  quant_code_fast(v[i][6], sc, rc), quant_code_fast(v[i][7], sc, rc));
       *reinterpret_cast<uint2 *>(q + t.row(i) * t.c + t.col()) = w;
     }
     if (t.warp == 0 && (t.lane & 3) == 0) {

@@ -86,6 +86,21 @@ class LayerNormContext:
 
 # ── GELU ────────────────────────────────────────────────────────────────
 
+_GELU_TABLES: dict[int, torch.Tensor] = {}
+
+
+def gelu_tables(device=None) -> torch.Tensor:
+    """Per-device lookup tables f(code * s) for all binary16 scales (built once, 64 MB)."""
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    tab = _GELU_TABLES.get(dev.index)
+    if tab is None:
+        L = _lib.lib()
+        tab = torch.empty(int(L.jf_gelu_tables_bytes()) // 4, dtype=torch.float32, device=dev)
+        _lib.check(L.jf_gelu_build_tables(tab.data_ptr(), _lib.stream_handle()), "gelu_tables")
+        _GELU_TABLES[dev.index] = tab
+    return tab
+
+
 
 def gelu_forward(xq: BlockQuantTensor, counters: AccessCounters | None = None) -> BlockQuantTensor:
     """y = x * CDF(x), requantized per block — kernel K9 (qnonlinear.py:150-158)."""
@@ -94,8 +109,8 @@ def gelu_forward(xq: BlockQuantTensor, counters: AccessCounters | None = None) -
     L = _lib.lib()
     y = empty_like_shape(xq.rows, xq.cols, xq.device)
     _lib.check(L.jf_gelu_fwd(xq.values.data_ptr(), xq.scales.data_ptr(), xq.rows, xq.cols,
-                             y.values.data_ptr(), y.scales.data_ptr(), _rt.err_ptr(),
-                             _lib.stream_handle()), "gelu_fwd")
+                             y.values.data_ptr(), y.scales.data_ptr(), gelu_tables(xq.device.index).data_ptr(),
+                             _rt.err_ptr(), _lib.stream_handle()), "gelu_fwd")
     _rt.maybe_check()
     return y
 
@@ -112,7 +127,8 @@ def gelu_backward(xq: BlockQuantTensor, dyq: BlockQuantTensor,
     y = empty_like_shape(xq.rows, xq.cols, xq.device)
     _lib.check(L.jf_gelu_bwd(xq.values.data_ptr(), xq.scales.data_ptr(), dyq.values.data_ptr(),
                              dyq.scales.data_ptr(), xq.rows, xq.cols, y.values.data_ptr(),
-                             y.scales.data_ptr(), _rt.err_ptr(), _lib.stream_handle()), "gelu_bwd")
+                             y.scales.data_ptr(), gelu_tables(xq.device.index).data_ptr(), _rt.err_ptr(),
+                             _lib.stream_handle()), "gelu_bwd")
     _rt.maybe_check()
     return y
 
