@@ -51,9 +51,9 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 // 2-D int8 tensor map: rows x cols (cols contiguous, row stride ld bytes),
-// box box_rows x box_cols, 128-byte swizzle (box_cols must be 128).
+// box box_rows x box_cols; 128-byte swizzle (box_cols must then be 128) or none.
 bool jf_make_tmap_i8(CUtensorMap *map, const void *ptr, int64_t rows, int64_t cols, int64_t ld,
-                     int box_cols, int box_rows) {
+                     int box_cols, int box_rows, bool swizzle128) {
   auto enc = get_encode();
   if (!enc) {
     jf_set_error("cuTensorMapEncodeTiled unavailable");
@@ -64,7 +64,8 @@ bool jf_make_tmap_i8(CUtensorMap *map, const void *ptr, int64_t rows, int64_t co
   cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(ptr), dims, strides,
-                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     snprintf(g_err, sizeof(g_err), "cuTensorMapEncodeTiled failed (%d) rows=%lld cols=%lld ld=%lld",

@@ -24,6 +24,8 @@
 // FP32 ops; at 128 FP32 ops/clk/SM the exact mode cannot exceed 384 clk per
 // 128x128x32 chunk (16.7% of the 64-clk tensor rate), fast mode is held to
 // 256 clk by the I2F rate.
+#include <string.h>
+
 #include "common.cuh"
 
 namespace jf {
@@ -55,6 +57,7 @@ struct Params {
   int32_t *err;
   int out_kind;
   float zero;  // always 0.0f; opaque to ptxas (blocks FMUL2+FADD2 contraction)
+  long long *trace;  // JF_GEMM_TRACE builds only: CTA 0 event clocks [8][512]
 };
 
 struct Smem {
@@ -84,6 +87,25 @@ JF_DEV void promote32(float *acc, const uint32_t *r, float sa, float sb, float z
     for (int j = 0; j < 32; j += 2) {
       float t0, t1;
       fmul2_rn(t0, t1, __int2float_rn((int)r[j]), __int2float_rn((int)r[j + 1]), sa, sa);
+      ffma2_rn(t0, t1, t0, t1, sb, sb, zero, zero);
+      fadd2_rn(acc[j], acc[j + 1], acc[j], acc[j + 1], t0, t1);
+    }
+  }
+}
+
+// Same, for f32 partials that hold exact integers (kind::f16 path: no I2F).
+template <bool kFast>
+JF_DEV void promote32f(float *acc, const uint32_t *r, float sa, float sb, float zero) {
+  if (kFast) {
+    const float s = __fmul_rn(sa, sb);
+#pragma unroll
+    for (int j = 0; j < 32; j += 2)
+      ffma2_rn(acc[j], acc[j + 1], __uint_as_float(r[j]), __uint_as_float(r[j + 1]), s, s, acc[j], acc[j + 1]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; j += 2) {
+      float t0, t1;
+      fmul2_rn(t0, t1, __uint_as_float(r[j]), __uint_as_float(r[j + 1]), sa, sa);
       ffma2_rn(t0, t1, t0, t1, sb, sb, zero, zero);
       fadd2_rn(acc[j], acc[j + 1], acc[j], acc[j + 1], t0, t1);
     }
@@ -336,6 +358,272 @@ __global__ void __launch_bounds__((2 + kEpiWarps) * 32, 1)
   if (warp == 1) tmem_dealloc(tmem, kTmemCols);
 }
 
+
+// ─────────────── kind::f16 variant: int8 codes in HBM, f16 tiles in smem ───────────────
+// The tensor core's int32 output forces one I2F per output element per chunk
+// (ALU pipe, half rate): on B200 that, not the MMA, bounds the kind::i8
+// kernel (ncu: ALU 65% / issue 68% busy in fast mode, tensor 12%).  Here the
+// int8 codes are widened to f16 in shared memory (every code is exact in
+// binary16) and tcgen05.mma.kind::f16 accumulates in f32: each 32-deep chunk's
+// partial is an integer of magnitude <= 32*127^2 < 2^24, so the f32 partial
+// IS the int32 partial, exactly, and the promotion reads it without any
+// conversion.  The widening costs ~1.5 instructions per OPERAND element
+// (8192 per 128x128x32 chunk) instead of one I2F per OUTPUT element (16384).
+//   warps 0..15  promotion/epilogue (as in gemm_i8_kernel); warp 0 lane 0
+//                also issues the MMAs right after its TMEM slot is released
+//   warps 16..19 converters; warp 16 lane 0 is also the TMA producer
+#ifdef JF_GEMM_TRACE
+#define JF_TR(ev, i)                                                                        \
+  do {                                                                                      \
+    if (blockIdx.x == 0 && (i) < 512 && p.trace) p.trace[(ev) * 512 + (i)] = clock64();     \
+  } while (0)
+#else
+#define JF_TR(ev, i) \
+  do {               \
+  } while (0)
+#endif
+
+namespace h16 {
+constexpr int BKH = 64;                       // K per stage (2 chunks)
+constexpr int kHStages = 3;                   // f16 ring depth (tensor-core operands)
+constexpr int kQStages = 8;                   // int8 ring depth (TMA lookahead)
+constexpr int kConvWarps = 4;
+constexpr int kWarps = kConvWarps + kEpiWarps;
+constexpr uint32_t kI8Bytes = BM * BKH;       // per operand per stage: 8 KB
+constexpr uint32_t kF16Bytes = BM * BKH * 2;  // 16 KB (128 rows x 128 B, SW128)
+struct Bars {
+  uint64_t full8[kQStages], empty8[kQStages], hfull[kHStages], hempty[kHStages];
+  uint64_t tfull[kPairSlots], tempty[kPairSlots];
+  uint32_t tmem_base;
+};
+constexpr size_t kSmemBytes = 1024 + kHStages * 2 * kF16Bytes + kQStages * 2 * kI8Bytes + 256;
+}  // namespace h16
+
+template <bool kFast, int kProbe = 0>  // diagnostics: kProbe 1 = converters skip the widening, 2 = no TMEM loads
+__global__ void __launch_bounds__(h16::kWarps * 32, 1)
+    gemm_h16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const Params p) {
+  using namespace h16;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *base = reinterpret_cast<uint8_t *>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *hA = base;                              // f16 ring (1024-aligned for SW128)
+  uint8_t *hB = hA + kHStages * kF16Bytes;
+  uint8_t *qA = hB + kHStages * kF16Bytes;          // int8 ring (TMA, no swizzle)
+  uint8_t *qB = qA + kQStages * kI8Bytes;
+  Bars &S = *reinterpret_cast<Bars *>(qB + kQStages * kI8Bytes);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t mt = (p.M + BM - 1) / BM, nt = (p.N + BN - 1) / BN;
+  const int64_t ntiles = mt * nt;
+  const int nchunks = (int)(p.K / 32);
+  const int nh = (nchunks + 1) / 2;  // stages (chunk pairs) per tile
+  const int my_tiles = (int)((ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x);
+  const int total = my_tiles * nh;   // stages this CTA streams
+  const uint32_t bar_full8 = smem_u32(&S.full8[0]), bar_empty8 = smem_u32(&S.empty8[0]);
+  const uint32_t bar_hfull = smem_u32(&S.hfull[0]), bar_hempty = smem_u32(&S.hempty[0]);
+  const uint32_t bar_tfull = smem_u32(&S.tfull[0]), bar_tempty = smem_u32(&S.tempty[0]);
+
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+    for (int s = 0; s < kQStages; ++s) {
+      mbar_init(&S.full8[s], 1);
+      mbar_init(&S.empty8[s], kConvWarps);
+    }
+    for (int s = 0; s < kHStages; ++s) {
+      mbar_init(&S.hfull[s], kConvWarps);
+      mbar_init(&S.hempty[s], 1);
+    }
+    for (int b = 0; b < kPairSlots; ++b) {
+      mbar_init(&S.tfull[b], 1);
+      mbar_init(&S.tempty[b], kEpiWarps);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc(&S.tmem_base, kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = S.tmem_base;
+
+  // Converters take the HIGHEST warp ids: the SMSP arbiter favours high warp
+  // ids, and the converters (plus the TMA producer among them) are the
+  // latency-critical producers; with low ids they starved behind the
+  // promotion warps (trace: 2.6k clk per stage vs ~0.3k of work).
+  const int cw = warp - kEpiWarps;  // converter index, valid when >= 0
+  if (cw >= 0) {
+    // ───────────── converters (converter 0 lane 0 is also the TMA producer) ─────────────
+    auto issue_tma = [&](int g) {
+      const int s = g % kQStages;
+      mbar_wait_u32(bar_empty8 + 8 * s, ((g / kQStages) & 1) ^ 1);
+      const int lt = g / nh, kh = g - lt * nh;
+      const int64_t tile = blockIdx.x + (int64_t)lt * gridDim.x;
+      const int m0 = (int)((tile % mt) * BM), n0 = (int)((tile / mt) * BN), k0 = kh * BKH;
+      mbar_arrive_expect_tx(&S.full8[s], 2 * kI8Bytes);
+      tma_load_2d(qA + s * kI8Bytes, &tmA, &S.full8[s], k0, m0);
+      tma_load_2d(qB + s * kI8Bytes, &tmB, &S.full8[s], k0, n0);
+    };
+    if (cw == 0 && lane == 0)
+      for (int g = 0; g < min(kQStages - 1, total); ++g) issue_tma(g);
+    __syncwarp();
+    const uint32_t q_base = smem_u32(qA), h_base = smem_u32(hA);
+    // item = (row of the 256 A|B rows, 16-byte source chunk c4 of its 64 bytes);
+    // thread handles rows 8*j + lane/4 of this warp's 64, chunk c4 = lane % 4
+    const int c4 = lane & 3;
+    for (int g = 0; g < total; ++g) {
+      const int s = g % kHStages, s8 = g % kQStages;
+      if (cw == 0 && lane == 0) JF_TR(0, g);
+      if (cw == 0 && lane == 0 && g + kQStages - 1 < total) issue_tma(g + kQStages - 1);
+      mbar_wait_u32(bar_full8 + 8 * s8, (g / kQStages) & 1);
+      if (cw == 0 && lane == 0) JF_TR(1, g);
+      mbar_wait_u32(bar_hempty + 8 * s, ((g / kHStages) & 1) ^ 1);
+      if (cw == 0 && lane == 0) JF_TR(2, g);
+      if (kProbe != 1) {
+        uint4 v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int rl = cw * 64 + j * 8 + (lane >> 2);  // 0..255
+          const int isB = rl >> 7, r = rl & 127;
+          v[j] = lds128(q_base + (uint32_t)(isB * kQStages + s8) * kI8Bytes + r * BKH + c4 * 16);
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int rl = cw * 64 + j * 8 + (lane >> 2);
+          const int isB = rl >> 7, r = rl & 127;
+          const uint32_t row = h_base + (uint32_t)(isB * kHStages + s) * kF16Bytes + r * 128;
+          uint32_t h[8];
+          i8x4_to_f16x4(v[j].x, h[0], h[1]);
+          i8x4_to_f16x4(v[j].y, h[2], h[3]);
+          i8x4_to_f16x4(v[j].z, h[4], h[5]);
+          i8x4_to_f16x4(v[j].w, h[6], h[7]);
+          // f16 chunks 2*c4, 2*c4+1 of the row, 128-byte swizzle (chunk ^ row % 8)
+          sts128(row + (((2 * c4) ^ (r & 7)) << 4), h[0], h[1], h[2], h[3]);
+          sts128(row + (((2 * c4 + 1) ^ (r & 7)) << 4), h[4], h[5], h[6], h[7]);
+        }
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive_u32(bar_hfull + 8 * s);
+        mbar_arrive_u32(bar_empty8 + 8 * s8);
+      }
+      if (cw == 0 && lane == 0) JF_TR(3, g);
+    }
+  } else {
+    // ───────────── promotion + epilogue (warp 0 lane 0 also issues the MMAs) ─────────────
+    const int ew = warp;
+    const int lq = warp & 3;
+    const int cg = ew >> 2;
+    const uint32_t tcol = tmem + ((uint32_t)(lq * 32) << 16) + cg * 32;
+    const bool vec_scales = (p.sa_s1 == 1) && (p.sb_s1 == 1) && (nchunks % 4 == 0);
+    const bool issuer = (ew == 0) && (lane == 0);
+    const uint64_t adesc0 = smem_desc_sw128(smem_u32(hA), 16, 1024);
+    const uint64_t bdesc0 = smem_desc_sw128(smem_u32(hB), 16, 1024);
+    constexpr uint32_t idesc = idesc_f16_f32(BM, BN);
+    // MMAs of stage g (a chunk pair) into TMEM slot g % 2; slot must be free
+    auto issue_mma = [&](int g) {
+      const int s = g % kHStages;
+      const uint32_t slot = g & 1;
+      const bool two = 2 * (g % nh) + 1 < nchunks;
+      JF_TR(4, g);
+      mbar_wait_u32(bar_hfull + 8 * s, (g / kHStages) & 1);
+      JF_TR(5, g);
+      mbar_wait_u32(bar_tempty + 8 * slot, ((g >> 1) & 1) ^ 1);
+      JF_TR(6, g);
+      tc_fence_after();
+      const uint64_t ad = adesc0 + (uint64_t)((s * kF16Bytes) >> 4);
+      const uint64_t bd = bdesc0 + (uint64_t)((s * kF16Bytes) >> 4);
+      const uint32_t d0 = tmem + slot * (2 * BN);
+      // chunk 0: K 0..31 = row bytes 0..63 (two K=16 MMAs, +32 B each); chunk 1: bytes 64..127
+      mma_f16_ss(d0, ad, bd, idesc, 0u);
+      mma_f16_ss(d0, ad + 2, bd + 2, idesc, 1u);
+      if (two) {
+        mma_f16_ss(d0 + BN, ad + 4, bd + 4, idesc, 0u);
+        mma_f16_ss(d0 + BN, ad + 6, bd + 6, idesc, 1u);
+      }
+      mma_commit(&S.tfull[slot]);
+      mma_commit(&S.hempty[s]);
+    };
+    if (issuer)
+      for (int g = 0; g < min(kPairSlots, total); ++g) issue_mma(g);
+    __syncwarp();
+    uint32_t q = 0;
+    int flags = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const int64_t I = (tile % mt) * (BM / 32) + lq;
+      const int64_t J = (tile / mt) * (BN / 32) + cg;
+      const bool valid = (I * 32 < p.M) && (J * 32 < p.N);
+      float acc[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) acc[j] = 0.0f;
+      const float *pa = p.sa + (valid ? I * p.sa_s0 : 0);
+      const float *pb = p.sb + (valid ? J * p.sb_s0 : 0);
+      float4 nsa = make_float4(0.f, 0.f, 0.f, 0.f), nsb = nsa;
+      auto load_scales = [&](int cb, float4 &a4, float4 &b4) {
+        if (!valid || cb >= nchunks) return;
+        if (vec_scales) {
+          a4 = __ldg(reinterpret_cast<const float4 *>(pa + cb));
+          b4 = __ldg(reinterpret_cast<const float4 *>(pb + cb));
+        } else {
+          float t[4], u[4];
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            t[b] = cb + b < nchunks ? __ldg(pa + (cb + b) * p.sa_s1) : 0.f;
+            u[b] = cb + b < nchunks ? __ldg(pb + (cb + b) * p.sb_s1) : 0.f;
+          }
+          a4 = make_float4(t[0], t[1], t[2], t[3]);
+          b4 = make_float4(u[0], u[1], u[2], u[3]);
+        }
+      };
+      load_scales(0, nsa, nsb);
+      for (int cb = 0; cb < nchunks; cb += 4) {
+        const float sav[4] = {nsa.x, nsa.y, nsa.z, nsa.w};
+        const float sbv[4] = {nsb.x, nsb.y, nsb.z, nsb.w};
+        load_scales(cb + 4, nsa, nsb);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c0 = cb + 2 * h;
+          if (c0 >= nchunks) break;
+          const bool two = c0 + 1 < nchunks;
+          const uint32_t slot = q & 1;
+          mbar_wait_u32(bar_tfull + 8 * slot, (q >> 1) & 1);
+          if (issuer) JF_TR(7, (int)q);
+          tc_fence_after();
+          uint32_t r[32];
+          const uint32_t t0 = tcol + slot * (2 * BN);
+          if (kProbe != 2) {
+            tmem_ld_32x32b_x32(t0, r);
+            tmem_wait_ld();
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) r[j] = __float_as_uint((float)(j + lane));
+          }
+          promote32f<kFast>(acc, r, sav[2 * h], sbv[2 * h], p.zero);
+          if (two && kProbe != 2) {
+            tmem_ld_32x32b_x32(t0 + BN, r);
+            tmem_wait_ld();
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_u32(bar_tempty + 8 * slot);
+          if (issuer && (int)q + kPairSlots < total) issue_mma((int)q + kPairSlots);
+          __syncwarp();
+          ++q;
+          if (two) promote32f<kFast>(acc, r, sav[2 * h + 1], sbv[2 * h + 1], p.zero);
+        }
+      }
+      if (valid) flags |= finish_block(p, acc, I, J, lane);
+    }
+    if (lane == 0) raise_flags(p.err, flags);
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, kTmemCols);
+}
+
 }  // namespace gemm
 }  // namespace jf
 
@@ -346,7 +634,15 @@ int jf_launch_check(const char *what);
 void jf_set_error(const char *msg);
 int jf_num_sms();
 bool jf_make_tmap_i8(CUtensorMap *map, const void *ptr, int64_t rows, int64_t cols, int64_t ld,
-                     int box_cols, int box_rows);
+                     int box_cols, int box_rows, bool swizzle128);
+
+#ifdef JF_GEMM_TRACE
+static long long *g_trace = nullptr;
+extern "C" int jf_gemm_trace_read(long long *host) {
+  if (!g_trace) return 1;
+  return cudaMemcpy(host, g_trace, 8 * 512 * sizeof(long long), cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 2;
+}
+#endif
 
 // Core launcher: A [M x K] (row stride lda), Bt [N x K] (row stride ldb), both K-major codes.
 int jf_gemm_launch(const int8_t *A, int64_t lda, const int8_t *Bt, int64_t ldb, int64_t M,
@@ -359,14 +655,53 @@ int jf_gemm_launch(const int8_t *A, int64_t lda, const int8_t *Bt, int64_t ldb, 
     jf_set_error("gemm: dims must be positive multiples of 32, strides multiples of 16");
     return JF_ERR_ARG;
   }
+  static int impl = -1;  // 0: kind::i8 path (default), 1: kind::f16 path (JF_GEMM_IMPL=h16)
+  if (impl < 0) {
+    const char *e = getenv("JF_GEMM_IMPL");
+    impl = (e && strcmp(e, "h16") == 0) ? 1 : 0;
+  }
+  const bool h16p = impl == 1 && out_kind != OUT_I32;
   CUtensorMap ta, tb;
-  if (!jf_make_tmap_i8(&ta, A, M, K, lda, BK, BM) || !jf_make_tmap_i8(&tb, Bt, N, K, ldb, BK, BN))
+  if (h16p) {
+    if (!jf_make_tmap_i8(&ta, A, M, K, lda, h16::BKH, BM, false) ||
+        !jf_make_tmap_i8(&tb, Bt, N, K, ldb, h16::BKH, BN, false))
+      return JF_ERR_LAUNCH;
+  } else if (!jf_make_tmap_i8(&ta, A, M, K, lda, BK, BM, true) ||
+             !jf_make_tmap_i8(&tb, Bt, N, K, ldb, BK, BN, true)) {
     return JF_ERR_LAUNCH;
-  Params p{M, N, K, sa, sa_s0, sa_s1, sb, sb_s0, sb_s1, bias, yq, ys, (float *)yf, err, out_kind, 0.0f};
+  }
+  Params p{M, N, K, sa, sa_s0, sa_s1, sb, sb_s0, sb_s1, bias, yq, ys, (float *)yf, err, out_kind, 0.0f, nullptr};
+#ifdef JF_GEMM_TRACE
+  if (!g_trace) {
+    cudaMalloc(&g_trace, 8 * 512 * sizeof(long long));
+  }
+  cudaMemsetAsync(g_trace, 0, 8 * 512 * sizeof(long long), stream);
+  p.trace = g_trace;
+#endif
   const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   const int grid = (int)(tiles < jf_num_sms() ? tiles : jf_num_sms());
   const bool fast = mode == JF_MODE_FAST;
   const bool partials = out_kind == OUT_I32;
+  if (h16p) {
+    static int hprobe = -1;
+    if (hprobe < 0) {
+      const char *e = getenv("JF_GEMM_PROBE");
+      hprobe = e ? atoi(e) : 0;
+    }
+    void (*hk)(const CUtensorMap, const CUtensorMap, const Params) =
+        hprobe == 6 ? (fast ? gemm_h16_kernel<true, 1> : gemm_h16_kernel<false, 1>)
+        : hprobe == 7 ? (fast ? gemm_h16_kernel<true, 2> : gemm_h16_kernel<false, 2>)
+                      : (fast ? gemm_h16_kernel<true> : gemm_h16_kernel<false>);
+    static bool hdone[2] = {};
+    if (!hdone[fast]) {
+      if (cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h16::kSmemBytes) !=
+          cudaSuccess)
+        return jf_launch_check("gemm_h16 attr");
+      hdone[fast] = true;
+    }
+    hk<<<grid, h16::kWarps * 32, h16::kSmemBytes, stream>>>(ta, tb, p);
+    return jf_launch_check("gemm_h16");
+  }
   void (*kern)(const CUtensorMap, const CUtensorMap, const Params) =
       partials ? gemm_i8_kernel<false, true> : (fast ? gemm_i8_kernel<true, false> : gemm_i8_kernel<false, false>);
   static int probe = -1;
