@@ -8,7 +8,7 @@ Dropout, QuantLinear and TransformerBlock — with every kernel in
 ``include/jetfire.h``).  There is no CPU fallback.
 """
 
-from . import runtime
+from . import autograd, dist, runtime
 from ._lib import JetfireUnavailable, load_library
 from .qgemm import (
     COUNTER_CSV_HEADER,
@@ -57,7 +57,7 @@ __all__ = [
     "add_forward", "block_mm_forward", "block_mm_grad_input", "block_mm_grad_weight", "block_partials",
     "check_errors", "column_sum", "count_elementwise", "dequantize", "dropout_backward",
     "dropout_forward", "gelu_backward", "gelu_forward", "layernorm_backward", "layernorm_forward",
-    "load_library", "micro_mm_16", "quantize_per_block", "require_cuda", "runtime", "set_error_check",
+    "autograd", "dist", "load_library", "micro_mm_16", "quantize_per_block", "require_cuda", "runtime", "set_error_check",
     "set_promotion", "snap_to_f16", "zeros_like",
 ]
 

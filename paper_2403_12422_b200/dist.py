@@ -1,0 +1,83 @@
+"""Data parallelism over the token batch.
+
+Sequences are independent, so each rank runs the INT8 block on its own
+whole sequences with no data-path collective.  The single exchange step is
+the sum of the FP32 parameter gradients — dequantized dW
+(``qlayers.py:181``), dbias, dγ/dβ — all-reduced over NCCL (NVLink /
+NVSwitch) in flat buckets and scaled by 1/world.  INT8 codes are never
+all-reduced: per-rank block scales differ, so the format is not sum-closed.
+The functions are backend-agnostic (NCCL on the GPU box, gloo in the CPU
+tests).
+"""
+
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+DEFAULT_BUCKET_BYTES = 64 << 20
+
+
+def shard_sequences(batch: int, rank: int, world: int) -> tuple[int, int]:
+    """[start, stop) of this rank's sequences; every rank gets whole sequences."""
+    if batch % world:
+        raise ValueError(f"batch {batch} does not split over {world} ranks")
+    per = batch // world
+    return rank * per, (rank + 1) * per
+
+
+def _buckets(keys, grads, bucket_bytes):
+    cur, size = [], 0
+    for k in keys:
+        nb = grads[k].numel() * grads[k].element_size()
+        if cur and size + nb > bucket_bytes:
+            yield cur
+            cur, size = [], 0
+        cur.append(k)
+        size += nb
+    if cur:
+        yield cur
+
+
+def allreduce_mean(grads: dict, group=None, bucket_bytes: int = DEFAULT_BUCKET_BYTES,
+                   async_op: bool = False):
+    """Average FP32 parameter gradients over the process group, in place.
+
+    Keys are visited in sorted order so every rank packs identical buckets.
+    Gradients that are ``None`` (no bias) are skipped.  With ``async_op``
+    the collectives are launched and a list of (work, bucket, flat) is
+    returned for ``finish_allreduce``; otherwise the call completes.
+    """
+    world = dist.get_world_size(group)
+    keys = sorted(k for k, v in grads.items() if v is not None)
+    for k in keys:
+        if grads[k].dtype != torch.float32:
+            raise TypeError(f"gradient {k!r} must be float32, got {grads[k].dtype}")
+    pending = []
+    for bucket in _buckets(keys, grads, bucket_bytes):
+        flat = torch.cat([grads[k].reshape(-1) for k in bucket])
+        work = dist.all_reduce(flat, group=group, async_op=async_op)
+        pending.append((work, bucket, flat))
+    if async_op:
+        return pending
+    _unpack(pending, grads, world)
+    return None
+
+
+def finish_allreduce(pending, grads: dict, group=None) -> None:
+    for work, _, _ in pending:
+        work.wait()
+    _unpack(pending, grads, dist.get_world_size(group))
+
+
+def _unpack(pending, grads, world):
+    for _, bucket, flat in pending:
+        flat.div_(world)
+        off = 0
+        for k in bucket:
+            n = grads[k].numel()
+            grads[k].copy_(flat[off:off + n].view_as(grads[k]))
+            off += n
+
+
+__all__ = ["allreduce_mean", "finish_allreduce", "shard_sequences"]
