@@ -207,6 +207,19 @@ JF_DEV void mbar_wait_u32_sleep(uint32_t addr, uint32_t parity, uint32_t hint_ns
       : "memory");
 }
 
+// Non-blocking phase test.
+JF_DEV bool mbar_test_u32(uint32_t addr, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
 JF_DEV void mbar_arrive_u32(uint32_t addr) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(addr) : "memory");
 }

@@ -6,24 +6,32 @@
 // a 32x32 block requantization (qgemm.py:266-279).
 //
 // Design (one persistent CTA per SM, warp-specialized, 128x128 output tiles):
-//   warp 0      TMA producer: 128x128-byte K-major SW128 tiles of A and B into
-//               a 6-stage smem ring (4 K chunks per stage).
-//   warp 1      MMA issuer: one tcgen05.mma.kind::i8 (M=128, N=128, K=32) per
-//               K chunk, accumulate = 0 (every 32-deep product is a fresh int32
-//               partial because the reference promotes each one separately);
-//               chunks go out in pairs, one commit per pair.
-//   warps 2..17 promotion/epilogue, 32 columns each (TMEM lane quarter =
-//               warp % 4).  Per pair: tcgen05.ld both partials, free the TMEM
-//               pair, promote in packed f32x2 ops:
-//                 EXACT: acc = fl(acc + fl(fl(P*sa)*sb))   (bit-exact)
-//                 FAST : acc = fma(P, sa*sb, acc)          (sa*sb exact)
-//               After the last chunk: +bias, 32x32 absmax (warp = 32 rows),
-//               binary16 scale, RNE codes, INT8 + scale stores.
-// Bound: per output element per 32 MACs the
-// promotion costs one I2F (ALU pipe, half rate) and 3 (exact) / 1 (fast)
-// FP32 ops; at 128 FP32 ops/clk/SM the exact mode cannot exceed 384 clk per
-// 128x128x32 chunk (16.7% of the 64-clk tensor rate), fast mode is held to
-// 256 clk by the I2F rate.
+//   warp 0        TMA producer: 128x128-byte K-major SW128 tiles of A and B
+//                 into a 6-stage smem ring (4 K chunks per stage).
+//   warp 1        MMA issuer: one tcgen05.mma.kind::i8 (M=128, N=128, K=32)
+//                 per K chunk into TMEM buffer (chunk % 4), accumulate = 0:
+//                 every chunk is a fresh int32 partial because the reference
+//                 promotes each 32-deep product separately.
+//   warps 2..17   promotion/epilogue (16 warps, 32 columns each; TMEM lane
+//                 quarter = warp % 4).  Per chunk a thread tcgen05.ld's its 32
+//                 int32 partials, frees the buffer, and promotes in packed
+//                 f32x2 ops:
+//                   EXACT: acc = fl(acc + fl(fl(P*sa)*sb))   (bit-exact)
+//                   FAST : acc = fma(P, sa*sb, acc)          (sa*sb exact)
+//                 After the last chunk: +bias, 32x32 absmax (warp = 32 rows),
+//                 binary16 scale, RNE codes, INT8 + scale stores.
+// Bound: per output element per 32 MACs the promotion
+// costs one I2F (ALU pipe, half rate) and 3 (exact) / 1 (fast) FP32 ops; at
+// 128 FP32 ops/clk/SM exact mode cannot beat 384 clk per 128x128x32 chunk
+// (16.7% of the 64-clk tensor rate), fast mode is held to 256 clk by I2F.
+// Variants measured A/B in one session (mlp1 fwd, 4096x16384x4096, exact):
+// this per-chunk hand-off 1294 us; chunk pairs per barrier 1345 us; MMA issue
+// folded into a promotion warp 1842 us; 8 promotion warps x 64 columns 1406
+// us; 3 MMA issuers 1318 us; "phase" issue (4 MMAs after all 4 buffers
+// drain) 1356 us.  The remaining gap to the 403-clk/chunk standalone
+// promotion loop (profiles/r1e_microbench.jsonl) is sub-partition skew: the
+// four sub-partitions each serve one TMEM lane quarter, the buffer release
+// waits for the slowest, and the one hosting the MMA issuer lags.
 #include <string.h>
 
 #include "common.cuh"
@@ -36,9 +44,10 @@ constexpr int BN = 128;
 constexpr int BK = 128;  // bytes of K per stage (4 chunks)
 constexpr int kStages = 6;
 constexpr int kChunksPerStage = BK / 32;
-constexpr int kPairSlots = 2;      // TMEM: 2 slots x 2 chunk buffers x 128 int32 columns
-constexpr int kTmemCols = kPairSlots * 2 * BN;  // 512 = all of TMEM
-constexpr int kEpiWarps = 16;
+constexpr int kTmemBufs = 4;  // == kChunksPerStage: chunk c of a stage uses buffer c
+constexpr int kEpiWarps = 16;  // promotion warps (kind::f16 path)
+constexpr int kPairSlots = 2;  // kind::f16 path: 2 slots x 2 chunk buffers x 128 f32 columns
+constexpr int kTmemCols = kPairSlots * 2 * BN;
 constexpr uint32_t kStageBytesA = BM * BK;
 constexpr uint32_t kStageBytesB = BN * BK;
 
@@ -57,14 +66,14 @@ struct Params {
   int32_t *err;
   int out_kind;
   float zero;  // always 0.0f; opaque to ptxas (blocks FMUL2+FADD2 contraction)
-  long long *trace;  // JF_GEMM_TRACE builds only: CTA 0 event clocks [8][512]
+  long long *trace;  // JF_GEMM_TRACE builds only (f16 path): CTA 0 event clocks [8][512]
 };
 
 struct Smem {
   uint64_t full[kStages];
   uint64_t empty[kStages];
-  uint64_t tfull[kPairSlots];
-  uint64_t tempty[kPairSlots];
+  uint64_t tfull[kTmemBufs];
+  uint64_t tempty[kTmemBufs];
   uint32_t tmem_base;
 };
 
@@ -155,21 +164,13 @@ JF_DEV int finish_block(const Params &p, float *acc, int64_t I, int64_t J, int l
   return lane == 0 ? f : 0;
 }
 
-// One persistent CTA per SM.  Warp 0: TMA producer.  Warp 1: MMA issuer.
-// Warps 2..17: promotion (16 warps; warp w owns TMEM lane quarter w % 4 and
-// 32 of the 128 tile columns).  Chunks are handed over in PAIRS: the issuer
-// writes chunks 2q and 2q+1 into TMEM buffers 2(q%2) and 2(q%2)+1 and makes
-// one commit; a promotion warp waits once, loads both partials, frees both
-// buffers with one arrive, then promotes them.  Halving the per-chunk barrier
-// and commit traffic matters because the promotion is issue-bound (ncu:
-// 71% issue slots busy, ~20 bookkeeping instructions per warp-chunk).
-// kProbe (diagnostics only, JF_GEMM_PROBE): 1 = skip the promotion math,
-// 2 = skip the MMAs (commit only), 3 = skip the TMEM loads, 4 = no TMEM
-// loads and no hand-off waits at all (pure promotion-loop throughput).
-template <bool kFast, bool kPartials, int kProbe = 0>
-__global__ void __launch_bounds__((2 + kEpiWarps) * 32, 1)
+// kEpi promotion warps (8 or 16) in (kEpi/4) column groups of kCols = BN*4/kEpi;
+// kIss MMA issuer warps (1, or 3 when nchunks % 4 == 0).
+template <bool kFast, bool kPartials, int kEpi, int kIss>
+__global__ void __launch_bounds__((1 + kIss + kEpi) * 32, 1)
     gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const Params p) {
+  constexpr int kCtrl = 1 + kIss;  // warp 0: TMA, warps 1..kIss: MMA issuers
   extern __shared__ uint8_t smem_raw[];
   uint8_t *base = reinterpret_cast<uint8_t *>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -183,6 +184,7 @@ __global__ void __launch_bounds__((2 + kEpiWarps) * 32, 1)
   const int64_t ntiles = mt * nt;
   const int nchunks = (int)(p.K / 32);
   const int nstages_k = (nchunks + kChunksPerStage - 1) / kChunksPerStage;
+  const int my_tiles = (int)((ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x);
   const uint32_t bar_full = smem_u32(&S.full[0]), bar_empty = smem_u32(&S.empty[0]);
   const uint32_t bar_tfull = smem_u32(&S.tfull[0]), bar_tempty = smem_u32(&S.tempty[0]);
 
@@ -191,15 +193,15 @@ __global__ void __launch_bounds__((2 + kEpiWarps) * 32, 1)
     prefetch_tmap(&tmB);
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&S.full[s], 1);
-      mbar_init(&S.empty[s], 1);
+      mbar_init(&S.empty[s], kIss > 1 ? kChunksPerStage : 1);  // multi-issuer: one commit per chunk
     }
-    for (int b = 0; b < kPairSlots; ++b) {
+    for (int b = 0; b < kTmemBufs; ++b) {
       mbar_init(&S.tfull[b], 1);
-      mbar_init(&S.tempty[b], kEpiWarps);
+      mbar_init(&S.tempty[b], kEpi);
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(&S.tmem_base, kTmemCols);
+  if (warp == 1) tmem_alloc(&S.tmem_base, kTmemBufs * BN);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -213,7 +215,7 @@ __global__ void __launch_bounds__((2 + kEpiWarps) * 32, 1)
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int m0 = (int)((tile % mt) * BM), n0 = (int)((tile / mt) * BN);
         for (int ks = 0; ks < nstages_k; ++ks) {
-          mbar_wait_u32_sleep(bar_empty + 8 * stage, phase ^ 1, 20);
+          mbar_wait_u32(bar_empty + 8 * stage, phase ^ 1);
           mbar_arrive_expect_tx(&S.full[stage], kStageBytesA + kStageBytesB);
           tma_load_2d(sA + stage * kStageBytesA, &tmA, &S.full[stage], ks * BK, m0);
           tma_load_2d(sB + stage * kStageBytesB, &tmB, &S.full[stage], ks * BK, n0);
@@ -224,33 +226,51 @@ __global__ void __launch_bounds__((2 + kEpiWarps) * 32, 1)
         }
       }
     }
-  } else if (warp == 1) {
-    // ───────────── MMA issuer (one thread) ─────────────
-    if (lane == 0) {
-      const uint64_t adesc0 = smem_desc_sw128(smem_u32(sA), 16, 1024);
-      const uint64_t bdesc0 = smem_desc_sw128(smem_u32(sB), 16, 1024);
-      constexpr uint32_t idesc = idesc_i8(BM, BN, 0, 0);
-      int stage = 0;
-      uint32_t phase = 0, q = 0;  // q: pairs issued by this CTA
+  } else if (warp < kCtrl) {
+    // ───────────── MMA issuers ─────────────
+    // Descriptors are precomputed: the per-chunk path is wait -> fence -> MMA -> commit.
+    const uint64_t adesc0 = smem_desc_sw128(smem_u32(sA), 16, 1024);
+    const uint64_t bdesc0 = smem_desc_sw128(smem_u32(sB), 16, 1024);
+    constexpr uint32_t idesc = idesc_i8(BM, BN, 0, 0);
+    if (kIss > 1) {
+      // issuer j takes global chunks g = j, j+kIss, ...: stage seq g/4, buffer (and
+      // K slice within the stage) g%4, and this is buffer g%4's (g/4)-th use.
+      if (lane == 0) {
+        const int total = my_tiles * nchunks;
+        for (int g = warp - 1; g < total; g += kIss) {
+          const int G = g >> 2, c = g & 3, slot = G % kStages;
+          mbar_wait_u32(bar_full + 8 * slot, (uint32_t)(G / kStages) & 1);
+          mbar_wait_u32(bar_tempty + 8 * c, ((uint32_t)G & 1) ^ 1);
+          tc_fence_after();
+          mma_i8_ss(tmem + c * BN, adesc0 + (uint64_t)((slot * kStageBytesA + c * 32) >> 4),
+                    bdesc0 + (uint64_t)((slot * kStageBytesB + c * 32) >> 4), idesc, 0u);
+          mma_commit(&S.tfull[c]);
+          mma_commit(&S.empty[slot]);
+        }
+      }
+    } else if (lane == 0) {
+      // single issuer (generic K): chunk ci of every tile lands in TMEM buffer ci % 4
+      int stage = 0, gk = 0;
+      uint32_t phase = 0, tphase = 0;
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         for (int ks = 0; ks < nstages_k; ++ks) {
-          mbar_wait_u32_sleep(bar_full + 8 * stage, phase, 20);
+          mbar_wait_u32(bar_full + 8 * stage, phase);
+          tc_fence_after();
           const uint64_t ad = adesc0 + (uint64_t)((stage * kStageBytesA) >> 4);
           const uint64_t bd = bdesc0 + (uint64_t)((stage * kStageBytesB) >> 4);
           const int nch = min(kChunksPerStage, nchunks - ks * kChunksPerStage);
-          for (int c = 0; c < nch; c += 2, ++q) {
-            const uint32_t slot = q & 1;
-            if (kProbe != 4) mbar_wait_u32(bar_tempty + 8 * slot, ((q >> 1) & 1) ^ 1);
-            tc_fence_after();
-            const uint32_t d0 = tmem + slot * (2 * BN);
-            // K chunk c of the stage starts 32 bytes (2 descriptor units) further in
-            if (kProbe != 2) {
-              mma_i8_ss(d0, ad + 2 * c, bd + 2 * c, idesc, 0u);
-              if (c + 1 < nch) mma_i8_ss(d0 + BN, ad + 2 * (c + 1), bd + 2 * (c + 1), idesc, 0u);
+#pragma unroll
+          for (int c = 0; c < kChunksPerStage; ++c) {
+            if (c < nch) {
+              mbar_wait_u32(bar_tempty + 8 * c, ((tphase >> c) & 1) ^ 1);
+              tphase ^= 1u << c;
+              tc_fence_after();
+              mma_i8_ss(tmem + c * BN, ad + 2 * c, bd + 2 * c, idesc, 0u);
+              mma_commit(&S.tfull[c]);
             }
-            mma_commit(&S.tfull[slot]);
           }
           mma_commit(&S.empty[stage]);
+          gk += nch;
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
@@ -260,104 +280,111 @@ __global__ void __launch_bounds__((2 + kEpiWarps) * 32, 1)
     }
   } else {
     // ───────────── promotion + epilogue ─────────────
-    const int ew = warp - 2;
-    const int lq = warp & 3;  // TMEM lane quarter == 32-row block of the tile
-    const int cg = ew >> 2;   // 32-column group of the tile
-    const uint32_t tcol = tmem + ((uint32_t)(lq * 32) << 16) + cg * 32;
+    constexpr int kCols = BN * 4 / kEpi;        // columns per warp: 64 (8 warps) or 32 (16 warps)
+    constexpr int kBlk = kCols / 32;            // 32-column blocks per warp
+    const int lq = warp & 3;                    // TMEM lane quarter == 32-row block of the tile
+    const int cgp = (warp - kCtrl) >> 2;        // column group
+    const uint32_t tcol = tmem + ((uint32_t)(lq * 32) << 16) + cgp * kCols;
     const bool vec_scales = (p.sa_s1 == 1) && (p.sb_s1 == 1) && (nchunks % 4 == 0);
-    uint32_t q = 0;
+    uint32_t tphase = 0;
     int flags = 0;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      const int64_t I = (tile % mt) * (BM / 32) + lq;  // 32-row block index
-      const int64_t J = (tile / mt) * (BN / 32) + cg;  // 32-col block index
-      const bool valid = (I * 32 < p.M) && (J * 32 < p.N);
-      float acc[32];
+    int lt = 0;  // this CTA's local tile index
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {
+      const int64_t I = (tile % mt) * (BM / 32) + lq;              // 32-row block index
+      const int64_t J0 = (tile / mt) * (BN / 32) + kBlk * cgp;     // first 32-col block
+      const bool vrow = I * 32 < p.M;
+      bool vb[kBlk];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) acc[j] = 0.0f;
-      const float *pa = p.sa + (kPartials || !valid ? 0 : I * p.sa_s0);
-      const float *pb = p.sb + (kPartials || !valid ? 0 : J * p.sb_s0);
-      // scales of the next 4 chunks, loaded one group ahead
-      float4 nsa = make_float4(0.f, 0.f, 0.f, 0.f), nsb = nsa;
-      auto load_scales = [&](int cb, float4 &a4, float4 &b4) {
-        if (kPartials || !valid || cb >= nchunks) return;
-        if (vec_scales) {
-          a4 = __ldg(reinterpret_cast<const float4 *>(pa + cb));
-          b4 = __ldg(reinterpret_cast<const float4 *>(pb + cb));
-        } else {
-          float t[4], u[4];
+      for (int q = 0; q < kBlk; ++q) vb[q] = vrow && ((J0 + q) * 32 < p.N);
+      float acc[kBlk][32];
 #pragma unroll
-          for (int b = 0; b < 4; ++b) {
-            t[b] = cb + b < nchunks ? __ldg(pa + (cb + b) * p.sa_s1) : 0.f;
-            u[b] = cb + b < nchunks ? __ldg(pb + (cb + b) * p.sb_s1) : 0.f;
-          }
-          a4 = make_float4(t[0], t[1], t[2], t[3]);
-          b4 = make_float4(u[0], u[1], u[2], u[3]);
-        }
-      };
-      load_scales(0, nsa, nsb);
-      for (int cb = 0; cb < nchunks; cb += 4) {
-        const float sav[4] = {nsa.x, nsa.y, nsa.z, nsa.w};
-        const float sbv[4] = {nsb.x, nsb.y, nsb.z, nsb.w};
-        load_scales(cb + 4, nsa, nsb);
+      for (int q = 0; q < kBlk; ++q)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int c0 = cb + 2 * h;
-          if (c0 >= nchunks) break;
-          const bool two = c0 + 1 < nchunks;
-          const uint32_t slot = q & 1;
-          if (kProbe != 4) mbar_wait_u32(bar_tfull + 8 * slot, (q >> 1) & 1);
-          ++q;
-          tc_fence_after();
-          // one register set: promote the first partial while the pair is still
-          // held, then load the second and release both TMEM buffers
-          uint32_t r[32];
-          const uint32_t t0 = tcol + slot * (2 * BN);
-          if (kProbe < 3) {
-            tmem_ld_32x32b_x32(t0, r);
-            tmem_wait_ld();
-          } else {
+        for (int j = 0; j < 32; ++j) acc[q][j] = 0.0f;
+      const float *pa = p.sa + (kPartials || !vrow ? 0 : I * p.sa_s0);
+      const float *pb[kBlk];
 #pragma unroll
-            for (int j = 0; j < 32; ++j) r[j] = (uint32_t)(lane * 33 + j + c0);
-          }
-          if (kProbe == 1) {
+      for (int q = 0; q < kBlk; ++q) pb[q] = p.sb + (kPartials || !vb[q] ? 0 : (J0 + q) * p.sb_s0);
+      for (int cb = 0; cb < nchunks; cb += kTmemBufs) {
+        float sav[4] = {0.f, 0.f, 0.f, 0.f}, sbv[kBlk][4];
 #pragma unroll
-            for (int j = 0; j < 32; ++j) acc[j] = __uint_as_float((__float_as_uint(acc[j]) ^ r[j]) & 0x3fffffffu);
-          } else if (kPartials) {
-            // debug: raw int32 partials of the (single) chunk
-            if (valid) {
-              int32_t *dst = reinterpret_cast<int32_t *>(p.yf) + (I * 32 + lane) * p.N + J * 32;
-#pragma unroll
-              for (int j = 0; j < 32; j += 4)
-                *reinterpret_cast<int4 *>(dst + j) = make_int4((int)r[j], (int)r[j + 1], (int)r[j + 2], (int)r[j + 3]);
+        for (int q = 0; q < kBlk; ++q) sbv[q][0] = sbv[q][1] = sbv[q][2] = sbv[q][3] = 0.f;
+        if (!kPartials) {
+          if (vec_scales) {  // K-contiguous scale grids: 4 chunks per 16-byte load
+            if (vrow) {
+              const float4 t = __ldg(reinterpret_cast<const float4 *>(pa + cb));
+              sav[0] = t.x; sav[1] = t.y; sav[2] = t.z; sav[3] = t.w;
             }
+#pragma unroll
+            for (int q = 0; q < kBlk; ++q)
+              if (vb[q]) {
+                const float4 t = __ldg(reinterpret_cast<const float4 *>(pb[q] + cb));
+                sbv[q][0] = t.x; sbv[q][1] = t.y; sbv[q][2] = t.z; sbv[q][3] = t.w;
+              }
           } else {
-            promote32<kFast>(acc, r, sav[2 * h], sbv[2 * h], p.zero);
+#pragma unroll
+            for (int b = 0; b < kTmemBufs; ++b)
+              if (cb + b < nchunks) {
+                if (vrow) sav[b] = __ldg(pa + (cb + b) * p.sa_s1);
+#pragma unroll
+                for (int q = 0; q < kBlk; ++q)
+                  if (vb[q]) sbv[q][b] = __ldg(pb[q] + (cb + b) * p.sb_s1);
+              }
           }
-          if (two && kProbe < 3) {
-            tmem_ld_32x32b_x32(t0 + BN, r);
-            tmem_wait_ld();
-          }
+        }
+#pragma unroll
+        for (int b = 0; b < kTmemBufs; ++b) {
+          if (cb + b >= nchunks) break;
+          mbar_wait_u32(bar_tfull + 8 * b, (tphase >> b) & 1);
+          tphase ^= 1u << b;
+          tc_fence_after();
+          uint32_t r[kBlk][32];
+#pragma unroll
+          for (int q = 0; q < kBlk; ++q) tmem_ld_32x32b_x32(tcol + b * BN + 32 * q, r[q]);
+          tmem_wait_ld();
           tc_fence_before();
           __syncwarp();
-          if (lane == 0 && kProbe != 4) mbar_arrive_u32(bar_tempty + 8 * slot);
-          if (kProbe == 1) {
+          if (lane == 0) mbar_arrive_u32(bar_tempty + 8 * b);
+          if (kPartials) {
+            // debug: raw int32 partials of the (single) chunk
 #pragma unroll
-            for (int j = 0; j < 32; ++j) acc[j] = __uint_as_float((__float_as_uint(acc[j]) ^ r[j]) & 0x3fffffffu);
-          } else if (two && !kPartials) {
-            promote32<kFast>(acc, r, sav[2 * h + 1], sbv[2 * h + 1], p.zero);
+            for (int q = 0; q < kBlk; ++q)
+              if (vb[q]) {
+                int32_t *dst = reinterpret_cast<int32_t *>(p.yf) + (I * 32 + lane) * p.N + (J0 + q) * 32;
+#pragma unroll
+                for (int j = 0; j < 32; j += 4)
+                  *reinterpret_cast<int4 *>(dst + j) =
+                      make_int4((int)r[q][j], (int)r[q][j + 1], (int)r[q][j + 2], (int)r[q][j + 3]);
+              }
+          } else {
+#pragma unroll
+            for (int q = 0; q < kBlk; ++q) promote32<kFast>(acc[q], r[q], sav[b], sbv[q][b], p.zero);
           }
         }
       }
-      if (!kPartials && valid) flags |= finish_block(p, acc, I, J, lane);
+      if (kPartials) continue;
+#pragma unroll
+      for (int q = 0; q < kBlk; ++q)
+        if (vb[q]) flags |= finish_block(p, acc[q], I, J0 + q, lane);
     }
     if (lane == 0) raise_flags(p.err, flags);
   }
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, kTmemCols);
+  if (warp == 1) tmem_dealloc(tmem, kTmemBufs * BN);
 }
 
+#ifdef JF_GEMM_TRACE
+#define JF_TR(ev, i)                                                                        \
+  do {                                                                                      \
+    if (blockIdx.x == 0 && (i) < 512 && p.trace) p.trace[(ev) * 512 + (i)] = clock64();     \
+  } while (0)
+#else
+#define JF_TR(ev, i) \
+  do {               \
+  } while (0)
+#endif
 
 // ─────────────── kind::f16 variant: int8 codes in HBM, f16 tiles in smem ───────────────
 // The tensor core's int32 output forces one I2F per output element per chunk
@@ -372,17 +399,6 @@ __global__ void __launch_bounds__((2 + kEpiWarps) * 32, 1)
 //   warps 0..15  promotion/epilogue (as in gemm_i8_kernel); warp 0 lane 0
 //                also issues the MMAs right after its TMEM slot is released
 //   warps 16..19 converters; warp 16 lane 0 is also the TMA producer
-#ifdef JF_GEMM_TRACE
-#define JF_TR(ev, i)                                                                        \
-  do {                                                                                      \
-    if (blockIdx.x == 0 && (i) < 512 && p.trace) p.trace[(ev) * 512 + (i)] = clock64();     \
-  } while (0)
-#else
-#define JF_TR(ev, i) \
-  do {               \
-  } while (0)
-#endif
-
 namespace h16 {
 constexpr int BKH = 64;                       // K per stage (2 chunks)
 constexpr int kHStages = 3;                   // f16 ring depth (tensor-core operands)
@@ -672,9 +688,7 @@ int jf_gemm_launch(const int8_t *A, int64_t lda, const int8_t *Bt, int64_t ldb, 
   }
   Params p{M, N, K, sa, sa_s0, sa_s1, sb, sb_s0, sb_s1, bias, yq, ys, (float *)yf, err, out_kind, 0.0f, nullptr};
 #ifdef JF_GEMM_TRACE
-  if (!g_trace) {
-    cudaMalloc(&g_trace, 8 * 512 * sizeof(long long));
-  }
+  if (!g_trace) cudaMalloc(&g_trace, 8 * 512 * sizeof(long long));
   cudaMemsetAsync(g_trace, 0, 8 * 512 * sizeof(long long), stream);
   p.trace = g_trace;
 #endif
@@ -683,15 +697,8 @@ int jf_gemm_launch(const int8_t *A, int64_t lda, const int8_t *Bt, int64_t ldb, 
   const bool fast = mode == JF_MODE_FAST;
   const bool partials = out_kind == OUT_I32;
   if (h16p) {
-    static int hprobe = -1;
-    if (hprobe < 0) {
-      const char *e = getenv("JF_GEMM_PROBE");
-      hprobe = e ? atoi(e) : 0;
-    }
     void (*hk)(const CUtensorMap, const CUtensorMap, const Params) =
-        hprobe == 6 ? (fast ? gemm_h16_kernel<true, 1> : gemm_h16_kernel<false, 1>)
-        : hprobe == 7 ? (fast ? gemm_h16_kernel<true, 2> : gemm_h16_kernel<false, 2>)
-                      : (fast ? gemm_h16_kernel<true> : gemm_h16_kernel<false>);
+        fast ? gemm_h16_kernel<true> : gemm_h16_kernel<false>;
     static bool hdone[2] = {};
     if (!hdone[fast]) {
       if (cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h16::kSmemBytes) !=
@@ -702,27 +709,36 @@ int jf_gemm_launch(const int8_t *A, int64_t lda, const int8_t *Bt, int64_t ldb, 
     hk<<<grid, h16::kWarps * 32, h16::kSmemBytes, stream>>>(ta, tb, p);
     return jf_launch_check("gemm_h16");
   }
-  void (*kern)(const CUtensorMap, const CUtensorMap, const Params) =
-      partials ? gemm_i8_kernel<false, true> : (fast ? gemm_i8_kernel<true, false> : gemm_i8_kernel<false, false>);
-  static int probe = -1;
-  if (probe < 0) {
-    const char *e = getenv("JF_GEMM_PROBE");
-    probe = e ? atoi(e) : 0;
+  static int epi = 0, iss_env = -1;
+  if (epi == 0) {
+    const char *e = getenv("JF_GEMM_EPI");
+    epi = (e && atoi(e) == 8) ? 8 : 16;  // default: 16 promotion warps (measured best)
+    const char *i = getenv("JF_GEMM_ISSUERS");
+    iss_env = (i && atoi(i) == 3) ? 3 : 1;  // default: one issuer (3 measured no faster)
   }
-  if (!partials && probe == 1) kern = gemm_i8_kernel<false, false, 1>;
-  if (!partials && probe == 2) kern = gemm_i8_kernel<false, false, 2>;
-  if (!partials && probe == 3) kern = gemm_i8_kernel<false, false, 3>;
-  if (!partials && probe == 4) kern = gemm_i8_kernel<false, false, 4>;
-  if (!partials && probe == 5) kern = gemm_i8_kernel<true, false, 4>;
-  static bool attr_done[8] = {};
-  const int ki = partials ? 2 : (probe >= 1 && probe <= 5 ? 2 + probe : (fast ? 1 : 0));
-  if (!attr_done[ki]) {
+  // multi-issuer pipeline needs whole 4-chunk stages (K % 128 == 0)
+  const int iss = (!partials && K % BK == 0) ? iss_env : 1;
+  void (*kern)(const CUtensorMap, const CUtensorMap, const Params);
+#define JF_PICK(E, IS)                                                                 \
+  kern = partials ? gemm_i8_kernel<false, true, E, 1>                                  \
+                  : (fast ? gemm_i8_kernel<true, false, E, IS> : gemm_i8_kernel<false, false, E, IS>);
+  if (epi == 16) {
+    if (iss == 3) { JF_PICK(16, 3) } else { JF_PICK(16, 1) }
+  } else {
+    if (iss == 3) { JF_PICK(8, 3) } else { JF_PICK(8, 1) }
+  }
+#undef JF_PICK
+  static bool attr_done[2][2][3] = {};
+  const int ki = partials ? 2 : (fast ? 1 : 0);
+  bool &done = attr_done[epi == 16][iss == 3][ki];
+  if (!done) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes) !=
         cudaSuccess)
       return jf_launch_check("gemm attr");
-    attr_done[ki] = true;
+    done = true;
   }
-  kern<<<grid, (2 + kEpiWarps) * 32, kSmemBytes, stream>>>(ta, tb, p);
+  const int threads = (1 + iss + epi) * 32;
+  kern<<<grid, threads, kSmemBytes, stream>>>(ta, tb, p);
   return jf_launch_check("gemm_i8");
 }
 

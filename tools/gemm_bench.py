@@ -30,7 +30,11 @@ def main():
     ap.add_argument("--ops", default="fwd,dgrad,wgrad")
     ap.add_argument("--modes", default="exact,fast")
     ap.add_argument("--shapes", default="mlp1,proj")
+    ap.add_argument("--lib", default=None, help="alternative libjetfire build (A/B experiments)")
     a = ap.parse_args()
+    if a.lib:
+        from paper_2403_12422_b200 import _lib
+        _lib.load_library(a.lib)
     jf.require_cuda()
     jf.set_error_check("deferred")
     for name in a.shapes.split(","):

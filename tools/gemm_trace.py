@@ -1,4 +1,4 @@
-"""CTA-0 event timeline of the f16-path GEMM (diagnostics; needs `make trace`).
+"""CTA-0 event timeline of the f16-path GEMM (JF_GEMM_IMPL=h16; diagnostics; needs `make trace`).
 
 python tools/gemm_trace.py [--shape proj] [--mode fast]
 Loads libjetfire_trace.so in place of libjetfire.so, runs one GEMM, and
@@ -25,7 +25,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--shape", default="proj")
     ap.add_argument("--mode", default="fast")
+    ap.add_argument("--impl", default="h16", choices=["h16"])
     a = ap.parse_args()
+    os.environ["JF_GEMM_IMPL"] = a.impl
     _lib.load_library(os.path.join(ROOT, "paper_2403_12422_b200", "libjetfire_trace.so"))
     import paper_2403_12422_b200 as jf
 
@@ -56,7 +58,6 @@ def main():
     print(f"period per stage (epilogue tfull-to-tfull): {per.mean():.0f} clk")
     print(f"converter: wait int8 {avg(1, 0):.0f}, wait f16 slot {avg(2, 1):.0f}, convert {avg(3, 2):.0f}")
     print(f"issuer: wait hfull {avg(5, 4):.0f}, wait tempty {avg(6, 5):.0f}")
-
 
 if __name__ == "__main__":
     main()

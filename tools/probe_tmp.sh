@@ -1,5 +1,7 @@
-mkdir -p gpurun_out/h16d
-timeout 600 python -m pytest tests -m gpu -x -q -k "gemm or partial or linear or block" > gpurun_out/h16d/pytest.log 2>&1
-timeout 300 python tools/gemm_bench.py --shapes mlp1,proj --ops fwd > gpurun_out/h16d/h16.jsonl 2>&1
-JF_GEMM_PROBE=6 timeout 300 python tools/gemm_bench.py --shapes mlp1 --ops fwd > gpurun_out/h16d/h16_noconv.jsonl 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemm_h16 -s 3 -c 1 -o gpurun_out/h16d/h16_fast -f python tools/gemm_bench.py --shapes proj --ops fwd --modes fast --iters 1 > gpurun_out/h16d/ncu1.log 2>&1
+mkdir -p gpurun_out/ab2
+B="python tools/gemm_bench.py --shapes mlp1 --ops fwd"
+timeout 300 $B --lib paper_2403_12422_b200/libjetfire_v1.so > gpurun_out/ab2/v1.jsonl 2>&1
+timeout 300 $B --lib paper_2403_12422_b200/libjetfire_v1p.so > gpurun_out/ab2/v1p.jsonl 2>&1
+JF_GEMM_EPI=8 timeout 300 $B --lib paper_2403_12422_b200/libjetfire_v1.so > gpurun_out/ab2/v1_epi8.jsonl 2>&1
+JF_GEMM_ISSUERS=3 timeout 300 $B --lib paper_2403_12422_b200/libjetfire_v1.so > gpurun_out/ab2/v1_iss3.jsonl 2>&1
+JF_GEMM_EPI=8 timeout 300 $B --lib paper_2403_12422_b200/libjetfire_v1p.so > gpurun_out/ab2/v1p_epi8.jsonl 2>&1
