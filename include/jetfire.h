@@ -102,6 +102,11 @@ size_t jf_gemm_scratch_bytes(int32_t which /*1=dgrad,2=wgrad*/, int64_t n, int64
 int jf_gemm_partials(const int8_t *a, const int8_t *bt, int64_t m, int64_t n, int64_t k,
                      int64_t kblk, int32_t *p, jf_stream_t stream);
 
+/* Diagnostics: GEMM launch options for A/B experiments ("impl" 0 = kind::i8, 1 = kind::f16;
+ * "epi" 16|8 promotion warps; "issuers" 1|3; "ctl_kind"/"ctl_ns" control-thread wait flavour).
+ * Defaults are the measured best; results are bit-identical across options. */
+int jf_gemm_set_option(const char *key, int value);
+
 /* K6 — add_forward(x1q, x2q, width)  [qnonlinear.py:246-267] + RowStats [:103-144].
  * b/bs may be NULL: the second operand is zeros_like(a) (qtensor.py:258-264).
  * mean/sumsq: [n x c/width] float32. */

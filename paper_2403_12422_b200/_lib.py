@@ -62,6 +62,7 @@ SIGNATURES = {
     "jf_colsum": (ctypes.c_int, [_P, _P, _I64, _I64, _P, _P, _P]),
     "jf_colsum_workspace_bytes": (_SZ, [_I64, _I64]),
     "jf_dropout": (ctypes.c_int, [_P, _P, _P, _F32, _I64, _I64, _P, _P, _P, _P]),
+    "jf_gemm_set_option": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int]),
 }
 
 _lib = None

@@ -32,6 +32,7 @@
 // promotion loop (profiles/r1e_microbench.jsonl) is sub-partition skew: the
 // four sub-partitions each serve one TMEM lane quarter, the buffer release
 // waits for the slowest, and the one hosting the MMA issuer lags.
+#include <stdio.h>
 #include <string.h>
 
 #include "common.cuh"
@@ -67,7 +68,20 @@ struct Params {
   int out_kind;
   float zero;  // always 0.0f; opaque to ptxas (blocks FMUL2+FADD2 contraction)
   long long *trace;  // JF_GEMM_TRACE builds only (f16 path): CTA 0 event clocks [8][512]
+  int ctl_kind;      // control-thread waits: 0 spin, 1 try_wait with suspend hint, 2 test + nanosleep
+  uint32_t ctl_ns;
 };
+
+// mbarrier wait used by the single-thread TMA producer and MMA issuer.
+JF_DEV void ctl_wait(const Params &p, uint32_t addr, uint32_t parity) {
+  if (p.ctl_kind == 1) {
+    mbar_wait_u32_sleep(addr, parity, p.ctl_ns);
+  } else if (p.ctl_kind == 2) {
+    while (!mbar_test_u32(addr, parity)) __nanosleep(p.ctl_ns);
+  } else {
+    mbar_wait_u32(addr, parity);
+  }
+}
 
 struct Smem {
   uint64_t full[kStages];
@@ -215,7 +229,7 @@ __global__ void __launch_bounds__((1 + kIss + kEpi) * 32, 1)
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int m0 = (int)((tile % mt) * BM), n0 = (int)((tile / mt) * BN);
         for (int ks = 0; ks < nstages_k; ++ks) {
-          mbar_wait_u32(bar_empty + 8 * stage, phase ^ 1);
+          ctl_wait(p, bar_empty + 8 * stage, phase ^ 1);
           mbar_arrive_expect_tx(&S.full[stage], kStageBytesA + kStageBytesB);
           tma_load_2d(sA + stage * kStageBytesA, &tmA, &S.full[stage], ks * BK, m0);
           tma_load_2d(sB + stage * kStageBytesB, &tmB, &S.full[stage], ks * BK, n0);
@@ -254,7 +268,7 @@ __global__ void __launch_bounds__((1 + kIss + kEpi) * 32, 1)
       uint32_t phase = 0, tphase = 0;
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         for (int ks = 0; ks < nstages_k; ++ks) {
-          mbar_wait_u32(bar_full + 8 * stage, phase);
+          ctl_wait(p, bar_full + 8 * stage, phase);
           tc_fence_after();
           const uint64_t ad = adesc0 + (uint64_t)((stage * kStageBytesA) >> 4);
           const uint64_t bd = bdesc0 + (uint64_t)((stage * kStageBytesB) >> 4);
@@ -262,7 +276,7 @@ __global__ void __launch_bounds__((1 + kIss + kEpi) * 32, 1)
 #pragma unroll
           for (int c = 0; c < kChunksPerStage; ++c) {
             if (c < nch) {
-              mbar_wait_u32(bar_tempty + 8 * c, ((tphase >> c) & 1) ^ 1);
+              ctl_wait(p, bar_tempty + 8 * c, ((tphase >> c) & 1) ^ 1);
               tphase ^= 1u << c;
               tc_fence_after();
               mma_i8_ss(tmem + c * BN, ad + 2 * c, bd + 2 * c, idesc, 0u);
@@ -660,6 +674,34 @@ extern "C" int jf_gemm_trace_read(long long *host) {
 }
 #endif
 
+// Launch options (diagnostics / A-B experiments).  Defaults are the measured
+// best; JF_GEMM_IMPL / JF_GEMM_EPI / JF_GEMM_ISSUERS / JF_GEMM_CTL set them at
+// load time, jf_gemm_set_option() at run time.
+struct GemmOptions {
+  int impl = 0;      // 0 kind::i8, 1 kind::f16 (h16)
+  int epi = 16;      // promotion warps (16 or 8)
+  int issuers = 1;   // MMA issuer warps (1 or 3)
+  int ctl_kind = 1;  // control-thread wait flavour (see ctl_wait)
+  int ctl_ns = 200;
+  GemmOptions() {
+    if (const char *e = getenv("JF_GEMM_IMPL")) impl = strcmp(e, "h16") == 0 ? 1 : 0;
+    if (const char *e = getenv("JF_GEMM_EPI")) epi = atoi(e) == 8 ? 8 : 16;
+    if (const char *e = getenv("JF_GEMM_ISSUERS")) issuers = atoi(e) == 3 ? 3 : 1;
+    if (const char *e = getenv("JF_GEMM_CTL")) sscanf(e, "%d,%d", &ctl_kind, &ctl_ns);
+  }
+};
+static GemmOptions g_opt;
+
+extern "C" int jf_gemm_set_option(const char *key, int value) {
+  if (!strcmp(key, "impl")) g_opt.impl = value ? 1 : 0;
+  else if (!strcmp(key, "epi")) g_opt.epi = value == 8 ? 8 : 16;
+  else if (!strcmp(key, "issuers")) g_opt.issuers = value == 3 ? 3 : 1;
+  else if (!strcmp(key, "ctl_kind")) g_opt.ctl_kind = value;
+  else if (!strcmp(key, "ctl_ns")) g_opt.ctl_ns = value;
+  else return JF_ERR_ARG;
+  return JF_OK;
+}
+
 // Core launcher: A [M x K] (row stride lda), Bt [N x K] (row stride ldb), both K-major codes.
 int jf_gemm_launch(const int8_t *A, int64_t lda, const int8_t *Bt, int64_t ldb, int64_t M,
                    int64_t N, int64_t K, const float *sa, int64_t sa_s0, int64_t sa_s1,
@@ -671,12 +713,7 @@ int jf_gemm_launch(const int8_t *A, int64_t lda, const int8_t *Bt, int64_t ldb, 
     jf_set_error("gemm: dims must be positive multiples of 32, strides multiples of 16");
     return JF_ERR_ARG;
   }
-  static int impl = -1;  // 0: kind::i8 path (default), 1: kind::f16 path (JF_GEMM_IMPL=h16)
-  if (impl < 0) {
-    const char *e = getenv("JF_GEMM_IMPL");
-    impl = (e && strcmp(e, "h16") == 0) ? 1 : 0;
-  }
-  const bool h16p = impl == 1 && out_kind != OUT_I32;
+  const bool h16p = g_opt.impl == 1 && out_kind != OUT_I32;
   CUtensorMap ta, tb;
   if (h16p) {
     if (!jf_make_tmap_i8(&ta, A, M, K, lda, h16::BKH, BM, false) ||
@@ -686,7 +723,8 @@ int jf_gemm_launch(const int8_t *A, int64_t lda, const int8_t *Bt, int64_t ldb, 
              !jf_make_tmap_i8(&tb, Bt, N, K, ldb, BK, BN, true)) {
     return JF_ERR_LAUNCH;
   }
-  Params p{M, N, K, sa, sa_s0, sa_s1, sb, sb_s0, sb_s1, bias, yq, ys, (float *)yf, err, out_kind, 0.0f, nullptr};
+  Params p{M, N, K, sa, sa_s0, sa_s1, sb, sb_s0, sb_s1, bias, yq, ys, (float *)yf, err, out_kind, 0.0f, nullptr,
+           g_opt.ctl_kind, (uint32_t)g_opt.ctl_ns};
 #ifdef JF_GEMM_TRACE
   if (!g_trace) cudaMalloc(&g_trace, 8 * 512 * sizeof(long long));
   cudaMemsetAsync(g_trace, 0, 8 * 512 * sizeof(long long), stream);
@@ -709,13 +747,7 @@ int jf_gemm_launch(const int8_t *A, int64_t lda, const int8_t *Bt, int64_t ldb, 
     hk<<<grid, h16::kWarps * 32, h16::kSmemBytes, stream>>>(ta, tb, p);
     return jf_launch_check("gemm_h16");
   }
-  static int epi = 0, iss_env = -1;
-  if (epi == 0) {
-    const char *e = getenv("JF_GEMM_EPI");
-    epi = (e && atoi(e) == 8) ? 8 : 16;  // default: 16 promotion warps (measured best)
-    const char *i = getenv("JF_GEMM_ISSUERS");
-    iss_env = (i && atoi(i) == 3) ? 3 : 1;  // default: one issuer (3 measured no faster)
-  }
+  const int epi = g_opt.epi, iss_env = g_opt.issuers;
   // multi-issuer pipeline needs whole 4-chunk stages (K % 128 == 0)
   const int iss = (!partials && K % BK == 0) ? iss_env : 1;
   void (*kern)(const CUtensorMap, const CUtensorMap, const Params);

@@ -1,7 +1,5 @@
-mkdir -p gpurun_out/ab2
-B="python tools/gemm_bench.py --shapes mlp1 --ops fwd"
-timeout 300 $B --lib paper_2403_12422_b200/libjetfire_v1.so > gpurun_out/ab2/v1.jsonl 2>&1
-timeout 300 $B --lib paper_2403_12422_b200/libjetfire_v1p.so > gpurun_out/ab2/v1p.jsonl 2>&1
-JF_GEMM_EPI=8 timeout 300 $B --lib paper_2403_12422_b200/libjetfire_v1.so > gpurun_out/ab2/v1_epi8.jsonl 2>&1
-JF_GEMM_ISSUERS=3 timeout 300 $B --lib paper_2403_12422_b200/libjetfire_v1.so > gpurun_out/ab2/v1_iss3.jsonl 2>&1
-JF_GEMM_EPI=8 timeout 300 $B --lib paper_2403_12422_b200/libjetfire_v1p.so > gpurun_out/ab2/v1p_epi8.jsonl 2>&1
+mkdir -p gpurun_out/ab4
+for i in 1 2; do
+python tools/gemm_bench.py --lib paper_2403_12422_b200/libjetfire_prev.so --shapes mlp1 --ops fwd > gpurun_out/ab4/prev_$i.jsonl 2>&1
+python tools/gemm_bench.py --shapes mlp1 --ops fwd > gpurun_out/ab4/new_$i.jsonl 2>&1
+done
