@@ -75,6 +75,28 @@ bool jf_make_tmap_i8(CUtensorMap *map, const void *ptr, int64_t rows, int64_t co
   return true;
 }
 
+// 2-D fp32 tensor map (scale grids): rows x cols, row stride ld elements, no swizzle.
+bool jf_make_tmap_f32(CUtensorMap *map, const void *ptr, int64_t rows, int64_t cols, int64_t ld,
+                      int box_cols, int box_rows) {
+  auto enc = get_encode();
+  if (!enc) {
+    jf_set_error("cuTensorMapEncodeTiled unavailable");
+    return false;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void *>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    snprintf(g_err, sizeof(g_err), "cuTensorMapEncodeTiled(f32) failed (%d)", (int)r);
+    return false;
+  }
+  return true;
+}
+
 extern "C" int jf_version(void) { return 1; }
 extern "C" const char *jf_last_error(void) { return g_err; }
 extern "C" int jf_sm_count(void) { return jf_num_sms(); }

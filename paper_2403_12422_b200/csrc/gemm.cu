@@ -389,6 +389,184 @@ __global__ void __launch_bounds__((1 + kIss + kEpi) * 32, 1)
   if (warp == 1) tmem_dealloc(tmem, kTmemBufs * BN);
 }
 
+
+// ─────────────── gemm_i8s_kernel: the same pipeline, scales staged by TMA ───────────────
+// Used when M, N, K are multiples of 128 (every transformer-block shape).  The
+// TMA producer also brings each stage's 4x4 sub-grids of sA and sB (64 B each)
+// into shared memory, so the promotion warps read their scale factors with
+// one LDS per 4 chunks instead of two L2-latency LDGs (hand-off microbenchmark:
+// 471 clk/chunk floor, +66 with global scale loads).  A stage is released only
+// when the MMAs consumed its tiles AND all promotion warps read its scales
+// (empty barrier count 1 + 16).  No partial tiles, so no validity predicates.
+struct SmemS {
+  uint64_t full[kStages];
+  uint64_t empty[kStages];
+  uint64_t tfull[kTmemBufs];
+  uint64_t tempty[kTmemBufs];
+  uint32_t tmem_base;
+};
+constexpr uint32_t kScaleBytes = 256;  // per stage: A box at +0, B box at +128 (16 floats each)
+constexpr size_t kSmemBytesS =
+    1024 + kStages * (kStageBytesA + kStageBytesB) + kStages * kScaleBytes + sizeof(SmemS) + 64;
+
+template <bool kFast>
+__global__ void __launch_bounds__((2 + 16) * 32, 1)
+    gemm_i8s_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const __grid_constant__ CUtensorMap tmSA, const __grid_constant__ CUtensorMap tmSB,
+                    const Params p, const int saT, const int sbT) {
+  constexpr int kEpi = 16;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *base = reinterpret_cast<uint8_t *>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *sA = base;
+  uint8_t *sB = base + kStages * kStageBytesA;
+  uint8_t *sS = sB + kStages * kStageBytesB;  // scale boxes, 128-byte aligned
+  SmemS &S = *reinterpret_cast<SmemS *>(sS + kStages * kScaleBytes);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t mt = p.M / BM, nt = p.N / BN;
+  const int64_t ntiles = mt * nt;
+  const int nstages_k = (int)(p.K / BK);
+  const uint32_t bar_full = smem_u32(&S.full[0]), bar_empty = smem_u32(&S.empty[0]);
+  const uint32_t bar_tfull = smem_u32(&S.tfull[0]), bar_tempty = smem_u32(&S.tempty[0]);
+
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+    prefetch_tmap(&tmSA);
+    prefetch_tmap(&tmSB);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&S.full[s], 1);
+      mbar_init(&S.empty[s], 1 + kEpi);
+    }
+    for (int b = 0; b < kTmemBufs; ++b) {
+      mbar_init(&S.tfull[b], 1);
+      mbar_init(&S.tempty[b], kEpi);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(&S.tmem_base, kTmemBufs * BN);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = S.tmem_base;
+
+  if (warp == 0) {
+    // ───────────── TMA producer: int8 tiles + scale sub-grids ─────────────
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int m0 = (int)((tile % mt) * BM), n0 = (int)((tile / mt) * BN);
+        for (int ks = 0; ks < nstages_k; ++ks) {
+          ctl_wait(p, bar_empty + 8 * stage, phase ^ 1);
+          mbar_arrive_expect_tx(&S.full[stage], kStageBytesA + kStageBytesB + 128);
+          tma_load_2d(sA + stage * kStageBytesA, &tmA, &S.full[stage], ks * BK, m0);
+          tma_load_2d(sB + stage * kStageBytesB, &tmB, &S.full[stage], ks * BK, n0);
+          uint8_t *ss = sS + stage * kScaleBytes;
+          // box {4, 4}: K-contiguous grids -> [row block][chunk], else [chunk][row block]
+          if (saT) tma_load_2d(ss, &tmSA, &S.full[stage], m0 / 32, ks * 4);
+          else tma_load_2d(ss, &tmSA, &S.full[stage], ks * 4, m0 / 32);
+          if (sbT) tma_load_2d(ss + 128, &tmSB, &S.full[stage], n0 / 32, ks * 4);
+          else tma_load_2d(ss + 128, &tmSB, &S.full[stage], ks * 4, n0 / 32);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ───────────── MMA issuer: chunk c of every stage -> TMEM buffer c ─────────────
+    if (lane == 0) {
+      const uint64_t adesc0 = smem_desc_sw128(smem_u32(sA), 16, 1024);
+      const uint64_t bdesc0 = smem_desc_sw128(smem_u32(sB), 16, 1024);
+      constexpr uint32_t idesc = idesc_i8(BM, BN, 0, 0);
+      int stage = 0;
+      uint32_t phase = 0, tphase = 0;
+      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        for (int ks = 0; ks < nstages_k; ++ks) {
+          ctl_wait(p, bar_full + 8 * stage, phase);
+          tc_fence_after();
+          const uint64_t ad = adesc0 + (uint64_t)((stage * kStageBytesA) >> 4);
+          const uint64_t bd = bdesc0 + (uint64_t)((stage * kStageBytesB) >> 4);
+#pragma unroll
+          for (int c = 0; c < kChunksPerStage; ++c) {
+            ctl_wait(p, bar_tempty + 8 * c, ((tphase >> c) & 1) ^ 1);
+            tphase ^= 1u << c;
+            tc_fence_after();
+            mma_i8_ss(tmem + c * BN, ad + 2 * c, bd + 2 * c, idesc, 0u);
+            mma_commit(&S.tfull[c]);
+          }
+          mma_commit(&S.empty[stage]);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else {
+    // ───────────── promotion + epilogue ─────────────
+    const int lq = warp & 3;          // TMEM lane quarter == 32-row block of the tile
+    const int cg = (warp - 2) >> 2;   // 32-column group of the tile
+    const uint32_t tcol = tmem + ((uint32_t)(lq * 32) << 16) + cg * 32;
+    const uint32_t ssa0 = smem_u32(sS), ssb0 = ssa0 + 128;
+    // float offsets of this warp's 4 scale factors inside the 4x4 boxes
+    const uint32_t oa = saT ? (uint32_t)lq * 4 : (uint32_t)lq * 16;
+    const uint32_t ob = sbT ? (uint32_t)cg * 4 : (uint32_t)cg * 16;
+    const uint32_t da = saT ? 16 : 4, db = sbT ? 16 : 4;  // byte step between chunks
+    uint32_t tphase = 0;
+    int flags = 0;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const int64_t I = (tile % mt) * (BM / 32) + lq;
+      const int64_t J = (tile / mt) * (BN / 32) + cg;
+      float acc[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) acc[j] = 0.0f;
+      for (int ks = 0; ks < nstages_k; ++ks) {
+        // the stage's scales: acquire the TMA writes, read, release the stage
+        mbar_wait_u32(bar_full + 8 * stage, phase);
+        const uint32_t sa_addr = ssa0 + stage * kScaleBytes + oa, sb_addr = ssb0 + stage * kScaleBytes + ob;
+        float sav[4], sbv[4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          sav[b] = lds_f32(sa_addr + b * da);
+          sbv[b] = lds_f32(sb_addr + b * db);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive_u32(bar_empty + 8 * stage);
+        if (++stage == kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+#pragma unroll
+        for (int b = 0; b < kTmemBufs; ++b) {
+          mbar_wait_u32(bar_tfull + 8 * b, (tphase >> b) & 1);
+          tphase ^= 1u << b;
+          tc_fence_after();
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tcol + b * BN, r);
+          tmem_wait_ld();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_u32(bar_tempty + 8 * b);
+          promote32<kFast>(acc, r, sav[b], sbv[b], p.zero);
+        }
+      }
+      flags |= finish_block(p, acc, I, J, lane);
+    }
+    if (lane == 0) raise_flags(p.err, flags);
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, kTmemBufs * BN);
+}
+
 #ifdef JF_GEMM_TRACE
 #define JF_TR(ev, i)                                                                        \
   do {                                                                                      \
@@ -665,6 +843,8 @@ void jf_set_error(const char *msg);
 int jf_num_sms();
 bool jf_make_tmap_i8(CUtensorMap *map, const void *ptr, int64_t rows, int64_t cols, int64_t ld,
                      int box_cols, int box_rows, bool swizzle128);
+bool jf_make_tmap_f32(CUtensorMap *map, const void *ptr, int64_t rows, int64_t cols, int64_t ld,
+                      int box_cols, int box_rows);
 
 #ifdef JF_GEMM_TRACE
 static long long *g_trace = nullptr;
@@ -683,6 +863,7 @@ struct GemmOptions {
   int issuers = 1;   // MMA issuer warps (1 or 3)
   int ctl_kind = 1;  // control-thread wait flavour (see ctl_wait)
   int ctl_ns = 200;
+  int tma_scales = 1;  // gemm_i8s_kernel when the shape allows
   GemmOptions() {
     if (const char *e = getenv("JF_GEMM_IMPL")) impl = strcmp(e, "h16") == 0 ? 1 : 0;
     if (const char *e = getenv("JF_GEMM_EPI")) epi = atoi(e) == 8 ? 8 : 16;
@@ -698,6 +879,7 @@ extern "C" int jf_gemm_set_option(const char *key, int value) {
   else if (!strcmp(key, "issuers")) g_opt.issuers = value == 3 ? 3 : 1;
   else if (!strcmp(key, "ctl_kind")) g_opt.ctl_kind = value;
   else if (!strcmp(key, "ctl_ns")) g_opt.ctl_ns = value;
+  else if (!strcmp(key, "tma_scales")) g_opt.tma_scales = value;
   else return JF_ERR_ARG;
   return JF_OK;
 }
@@ -746,6 +928,33 @@ int jf_gemm_launch(const int8_t *A, int64_t lda, const int8_t *Bt, int64_t ldb, 
     }
     hk<<<grid, h16::kWarps * 32, h16::kSmemBytes, stream>>>(ta, tb, p);
     return jf_launch_check("gemm_h16");
+  }
+  if (!partials && g_opt.tma_scales && M % 128 == 0 && N % 128 == 0 && K % 128 == 0) {
+    // scale grids by TMA: each must be contiguous along K or along M/N, 16-byte row pitch
+    const int64_t kb = K / 32;
+    auto grid_ok = [&](const float *s, int64_t s0, int64_t s1) {
+      return ((uintptr_t)s % 16 == 0) && ((s1 == 1 && s0 % 4 == 0) || (s0 == 1 && s1 % 4 == 0));
+    };
+    if (grid_ok(sa, sa_s0, sa_s1) && grid_ok(sb, sb_s0, sb_s1)) {
+      const int saT = sa_s1 != 1, sbT = sb_s1 != 1;
+      CUtensorMap tsa, tsb;
+      const bool ok = (saT ? jf_make_tmap_f32(&tsa, sa, kb, M / 32, sa_s1, 4, 4)
+                           : jf_make_tmap_f32(&tsa, sa, M / 32, kb, sa_s0, 4, 4)) &&
+                      (sbT ? jf_make_tmap_f32(&tsb, sb, kb, N / 32, sb_s1, 4, 4)
+                           : jf_make_tmap_f32(&tsb, sb, N / 32, kb, sb_s0, 4, 4));
+      if (!ok) return JF_ERR_LAUNCH;
+      void (*ks)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap, const Params,
+                 const int, const int) = fast ? gemm_i8s_kernel<true> : gemm_i8s_kernel<false>;
+      static bool sdone[2] = {};
+      if (!sdone[fast]) {
+        if (cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytesS) !=
+            cudaSuccess)
+          return jf_launch_check("gemm_i8s attr");
+        sdone[fast] = true;
+      }
+      ks<<<grid, 18 * 32, kSmemBytesS, stream>>>(ta, tb, tsa, tsb, p, saT, sbT);
+      return jf_launch_check("gemm_i8s");
+    }
   }
   const int epi = g_opt.epi, iss_env = g_opt.issuers;
   // multi-issuer pipeline needs whole 4-chunk stages (K % 128 == 0)

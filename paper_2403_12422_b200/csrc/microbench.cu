@@ -388,6 +388,199 @@ void run_mmasync(long long *d_cyc, float *d_out) {
   printf("{\"bench\": \"mma.sync m16n8k32 s8 (16 warps)\", \"mac_per_clk_per_sm\": %.1f}\n", macs / cyc);
 }
 
+
+// Promotion (exact, gemm form) by 16 warps on TMEM columns 0..127 while warp 16
+// lane 0 streams MMAs (M=128,N=128,K=32) into columns 256..511, optionally
+// throttled: one MMA per `gap` clk.  Measures TMEM read/compute contention with
+// concurrent tensor-core writes.
+__global__ void __launch_bounds__(544, 1) promote_vs_mma_kernel(float *out, long long *cyc, float sa, float sb,
+                                                                 float zero, int nmma, int gap) {
+  extern __shared__ uint8_t smraw[];
+  uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint32_t tbase;
+  __shared__ uint64_t bar;
+  __shared__ volatile int done;
+  const int warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < 256 * 128 / 4; i += blockDim.x) reinterpret_cast<uint32_t *>(sm)[i] = 0x01010101u * (i & 7);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+    done = 0;
+  }
+  if (warp == 0) tmem_alloc(&tbase, 512);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 16) {
+    if ((threadIdx.x & 31) == 0 && nmma > 0) {
+      const uint32_t a0 = smem_u32(sm), b0 = smem_u32(sm + 128 * 128);
+      for (int i = 0; i < nmma; ++i) {
+        long long t0 = clock64();
+        mma_i8_ss(tbase + 256 + (i & 1) * 128, smem_desc_sw128(a0 + (i & 3) * 32, 16, 1024),
+                  smem_desc_sw128(b0 + (i & 3) * 32, 16, 1024), idesc_i8(128, 128, 0, 0), 0u);
+        if (gap > 0)
+          while (clock64() - t0 < gap) {
+          }
+      }
+      mma_commit(&bar);
+      mbar_wait(&bar, 0);
+    }
+  } else {
+    const uint32_t t = tbase + ((uint32_t)((warp & 3) * 32) << 16) + (warp >> 2) * 32;
+    float acc[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) acc[j] = 0.f;
+    uint32_t r[32];
+    long long t0 = clock64();
+    for (int it = 0; it < ITERS / 4; ++it) {
+      tmem_ld_32x32b_x32(t, r);
+      tmem_wait_ld();
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) {
+        float t0f, t1f;
+        fmul2_rn(t0f, t1f, __int2float_rn((int)r[j]), __int2float_rn((int)r[j + 1]), sa, sa);
+        ffma2_rn(t0f, t1f, t0f, t1f, sb, sb, zero, zero);
+        fadd2_rn(acc[j], acc[j + 1], acc[j], acc[j + 1], t0f, t1f);
+      }
+    }
+    long long t1 = clock64();
+    float s = 0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) s += acc[j];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+    if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tbase, 512);
+}
+
+void run_promote_vs_mma(long long *d_cyc, float *d_out, int nmma, int gap) {
+  const size_t smem = 1024 + 256 * 128;
+  CK(cudaFuncSetAttribute(promote_vs_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  for (int rep = 0; rep < 2; ++rep) {
+    promote_vs_mma_kernel<<<g_sms, 544, smem>>>(d_out, d_cyc, 0.01f, 0.02f, 0.0f, nmma, gap);
+    CK(cudaDeviceSynchronize());
+  }
+  double cyc = median_cycles(d_cyc, g_sms);
+  double elems = 16.0 * 32 * 32 * (ITERS / 4);
+  printf("{\"bench\": \"promote_exact_vs_mma nmma=%d gap=%d\", \"elems_per_clk_per_sm\": %.1f, \"clk_per_16k\": %.0f}\n",
+         nmma, gap, elems / cyc, 16384.0 * cyc / elems);
+}
+
+
+// The GEMM's TMEM hand-off in isolation: warp 16 lane 0 issues one MMA per
+// chunk into buffer c % 4 after all 16 promotion warps released it (tempty,
+// count 16) and commits tfull; the promotion warps wait tfull, load, release,
+// promote (exact, gemm form).  WAITK selects the promotion-warp wait: 0 spin
+// try_wait, 1 try_wait with a suspend hint.
+template <int WAITK, int SCALES>
+__global__ void __launch_bounds__(544, 1) handoff_kernel(float *out, long long *cyc, float sa, float sb, float zero,
+                                                         int nchunk, const float *gsa, const float *gsb) {
+  extern __shared__ uint8_t smraw[];
+  uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint32_t tbase;
+  __shared__ uint64_t tfull[4], tempty[4];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < 256 * 128 / 4; i += blockDim.x) reinterpret_cast<uint32_t *>(sm)[i] = 0x01010101u * (i & 7);
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < 4; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 16);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc(&tbase, 512);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t bf = smem_u32(&tfull[0]), be = smem_u32(&tempty[0]);
+  if (warp == 16) {
+    if (lane == 0) {
+      const uint32_t a0 = smem_u32(sm), b0 = smem_u32(sm + 128 * 128);
+      for (int c = 0; c < nchunk; ++c) {
+        const int b = c & 3;
+        mbar_wait_u32(be + 8 * b, ((c >> 2) & 1) ^ 1);
+        tc_fence_after();
+        mma_i8_ss(tbase + b * 128, smem_desc_sw128(a0 + (c & 3) * 32, 16, 1024),
+                  smem_desc_sw128(b0 + (c & 3) * 32, 16, 1024), idesc_i8(128, 128, 0, 0), 0u);
+        mma_commit(&tfull[b]);
+      }
+    }
+  } else {
+    const uint32_t t = tbase + ((uint32_t)((warp & 3) * 32) << 16) + (warp >> 2) * 32;
+    float acc[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) acc[j] = 0.f;
+    long long t0 = clock64();
+    __shared__ float ssc[2][16];
+    if (threadIdx.x < 32) ssc[threadIdx.x >> 4][threadIdx.x & 15] = threadIdx.x < 16 ? sa : sb;
+    asm volatile("bar.sync 1, 512;" ::: "memory");
+    for (int c0 = 0; c0 < nchunk; c0 += 4) {
+      float sav[4] = {sa, sa, sa, sa}, sbv[4] = {sb, sb, sb, sb};
+      if (SCALES == 1) {  // as gemm_i8_kernel: one float4 of each grid per 4 chunks, from global
+        const float4 x = __ldg(reinterpret_cast<const float4 *>(gsa + (warp & 3) * 4096 + c0));
+        const float4 y = __ldg(reinterpret_cast<const float4 *>(gsb + (warp >> 2) * 4096 + c0));
+        sav[0] = x.x; sav[1] = x.y; sav[2] = x.z; sav[3] = x.w;
+        sbv[0] = y.x; sbv[1] = y.y; sbv[2] = y.z; sbv[3] = y.w;
+      }
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int c = c0 + b;
+        if (WAITK == 1) mbar_wait_u32_sleep(bf + 8 * b, (c >> 2) & 1, 50);
+        else mbar_wait_u32(bf + 8 * b, (c >> 2) & 1);
+        tc_fence_after();
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(t + b * 128, r);
+        if (SCALES == 2) {  // scales staged in shared memory (as a TMA-fed ring would)
+          sav[b] = ssc[0][(warp & 3) * 4 + b];
+          sbv[b] = ssc[1][(warp >> 2) * 4 + b];
+        }
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_u32(be + 8 * b);
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+          float t0f, t1f;
+          fmul2_rn(t0f, t1f, __int2float_rn((int)r[j]), __int2float_rn((int)r[j + 1]), sav[b], sav[b]);
+          ffma2_rn(t0f, t1f, t0f, t1f, sbv[b], sbv[b], zero, zero);
+          fadd2_rn(acc[j], acc[j + 1], acc[j], acc[j + 1], t0f, t1f);
+        }
+      }
+    }
+    long long t1 = clock64();
+    float s = 0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) s += acc[j];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+    if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tbase, 512);
+}
+
+template <int WAITK, int SCALES = 0>
+void run_handoff(long long *d_cyc, float *d_out) {
+  const size_t smem = 1024 + 256 * 128;
+  const int n = 1024;
+  static float *gs = nullptr;
+  if (!gs) {
+    CK(cudaMalloc(&gs, 2 * 4 * 4096 * sizeof(float)));
+    CK(cudaMemset(gs, 0, 2 * 4 * 4096 * sizeof(float)));
+  }
+  CK(cudaFuncSetAttribute(handoff_kernel<WAITK, SCALES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  for (int rep = 0; rep < 2; ++rep) {
+    handoff_kernel<WAITK, SCALES><<<g_sms, 544, smem>>>(d_out, d_cyc, 0.01f, 0.02f, 0.0f, n, gs, gs + 4 * 4096);
+    CK(cudaDeviceSynchronize());
+  }
+  double cyc = median_cycles(d_cyc, g_sms);
+  printf("{\"bench\": \"handoff_exact wait=%d scales=%d\", \"clk_per_chunk\": %.0f}\n", WAITK, SCALES, cyc / n);
+}
+
 int main() {
   CK(cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, 0));
   int clk_khz = 0;
@@ -425,6 +618,15 @@ int main() {
   run_mma<128, 7>(d_cyc);   // accumulate=1, commit per MMA, 4 rotating buffers
   run_mma<128, 8>(d_cyc);   // accumulate=0, no per-MMA commit
   run_mmasync(d_cyc, d_out);
+  // ITERS/4 = 1024 promotion iterations per warp = 1024 chunks; MMAs over the same span
+  run_handoff<0>(d_cyc, d_out);
+  run_handoff<1>(d_cyc, d_out);
+  run_handoff<0, 1>(d_cyc, d_out);
+  run_handoff<0, 2>(d_cyc, d_out);
+  run_promote_vs_mma(d_cyc, d_out, 0, 0);
+  run_promote_vs_mma(d_cyc, d_out, 1024, 400);
+  run_promote_vs_mma(d_cyc, d_out, 1024, 200);
+  run_promote_vs_mma(d_cyc, d_out, 4096, 0);
   run_mma_ld<16, 32>(d_cyc, d_out);
   run_mma_ld<8, 32>(d_cyc, d_out);
   run_mma_ld<8, 64>(d_cyc, d_out);
