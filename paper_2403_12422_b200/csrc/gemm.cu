@@ -409,12 +409,15 @@ constexpr uint32_t kScaleBytes = 256;  // per stage: A box at +0, B box at +128 
 constexpr size_t kSmemBytesS =
     1024 + kStages * (kStageBytesA + kStageBytesB) + kStages * kScaleBytes + sizeof(SmemS) + 64;
 
-template <bool kFast>
-__global__ void __launch_bounds__((2 + 16) * 32, 1)
+// kEpi = 16: 32 columns per promotion warp, one TMEM load per chunk.
+// kEpi = 8: 64 columns per warp (2 per sub-partition, up to 168 registers), the
+// two 32-column halves software-pipelined against each other and against the
+// next chunk's load, so TMEM load latency hides behind promotion math.
+template <bool kFast, int kEpi = 16>
+__global__ void __launch_bounds__((2 + kEpi) * 32, 1)
     gemm_i8s_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmSA, const __grid_constant__ CUtensorMap tmSB,
                     const Params p, const int saT, const int sbT) {
-  constexpr int kEpi = 16;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *base = reinterpret_cast<uint8_t *>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -509,33 +512,50 @@ __global__ void __launch_bounds__((2 + 16) * 32, 1)
     }
   } else {
     // ───────────── promotion + epilogue ─────────────
-    const int lq = warp & 3;          // TMEM lane quarter == 32-row block of the tile
-    const int cg = (warp - 2) >> 2;   // 32-column group of the tile
-    const uint32_t tcol = tmem + ((uint32_t)(lq * 32) << 16) + cg * 32;
+    constexpr int kCols = BN * 4 / kEpi;  // 32 or 64 columns per warp
+    const int lq = warp & 3;              // TMEM lane quarter == 32-row block of the tile
+    const int cg = (warp - 2) >> 2;       // column group of the tile
+    const uint32_t tcol = tmem + ((uint32_t)(lq * 32) << 16) + cg * kCols;
     const uint32_t ssa0 = smem_u32(sS), ssb0 = ssa0 + 128;
-    // float offsets of this warp's 4 scale factors inside the 4x4 boxes
+    // float offsets of this warp's scale factors inside the 4x4 boxes
     const uint32_t oa = saT ? (uint32_t)lq * 4 : (uint32_t)lq * 16;
-    const uint32_t ob = sbT ? (uint32_t)cg * 4 : (uint32_t)cg * 16;
     const uint32_t da = saT ? 16 : 4, db = sbT ? 16 : 4;  // byte step between chunks
+    constexpr int kBlk = kCols / 32;
+    uint32_t ob[kBlk];
+#pragma unroll
+    for (int q = 0; q < kBlk; ++q) {
+      const int jl = cg * kBlk + q;  // 32-col block within the tile
+      ob[q] = sbT ? (uint32_t)jl * 4 : (uint32_t)jl * 16;
+    }
     uint32_t tphase = 0;
     int flags = 0;
     int stage = 0;
     uint32_t phase = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       const int64_t I = (tile % mt) * (BM / 32) + lq;
-      const int64_t J = (tile / mt) * (BN / 32) + cg;
-      float acc[32];
+      const int64_t J0 = (tile / mt) * (BN / 32) + cg * kBlk;
+      float acc[kBlk][32];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) acc[j] = 0.0f;
+      for (int q = 0; q < kBlk; ++q)
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[q][j] = 0.0f;
+      uint32_t r0[32], r1[32];
+      if (kEpi == 8 && tile == blockIdx.x) {  // prologue: first half of the first chunk
+        mbar_wait_u32(bar_tfull, tphase & 1);
+        tphase ^= 1u;
+        tc_fence_after();
+        tmem_ld_32x32b_x32(tcol, r0);
+      }
       for (int ks = 0; ks < nstages_k; ++ks) {
         // the stage's scales: acquire the TMA writes, read, release the stage
         mbar_wait_u32(bar_full + 8 * stage, phase);
-        const uint32_t sa_addr = ssa0 + stage * kScaleBytes + oa, sb_addr = ssb0 + stage * kScaleBytes + ob;
-        float sav[4], sbv[4];
+        const uint32_t sa_addr = ssa0 + stage * kScaleBytes + oa;
+        float sav[4], sbv[kBlk][4];
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
           sav[b] = lds_f32(sa_addr + b * da);
-          sbv[b] = lds_f32(sb_addr + b * db);
+#pragma unroll
+          for (int q = 0; q < kBlk; ++q) sbv[q][b] = lds_f32(ssb0 + stage * kScaleBytes + ob[q] + b * db);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive_u32(bar_empty + 8 * stage);
@@ -545,19 +565,40 @@ __global__ void __launch_bounds__((2 + 16) * 32, 1)
         }
 #pragma unroll
         for (int b = 0; b < kTmemBufs; ++b) {
-          mbar_wait_u32(bar_tfull + 8 * b, (tphase >> b) & 1);
-          tphase ^= 1u << b;
-          tc_fence_after();
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(tcol + b * BN, r);
-          tmem_wait_ld();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive_u32(bar_tempty + 8 * b);
-          promote32<kFast>(acc, r, sav[b], sbv[b], p.zero);
+          if (kEpi == 16) {
+            mbar_wait_u32(bar_tfull + 8 * b, (tphase >> b) & 1);
+            tphase ^= 1u << b;
+            tc_fence_after();
+            tmem_ld_32x32b_x32(tcol + b * BN, r0);
+            tmem_wait_ld();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_u32(bar_tempty + 8 * b);
+            promote32<kFast>(acc[0], r0, sav[b], sbv[0][b], p.zero);
+          } else {
+            // r0 = this chunk's cols 0..31, in flight or ready
+            tmem_wait_ld();
+            tmem_ld_32x32b_x32(tcol + b * BN + 32, r1);
+            promote32<kFast>(acc[0], r0, sav[b], sbv[0][b], p.zero);
+            tmem_wait_ld();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_u32(bar_tempty + 8 * b);
+            // next chunk's first half (the next tile's after this tile's last chunk)
+            const int nb = (b + 1) & 3;
+            const bool more = (b < kTmemBufs - 1) || (ks + 1 < nstages_k) || (tile + gridDim.x < ntiles);
+            if (more) {
+              mbar_wait_u32(bar_tfull + 8 * nb, (tphase >> nb) & 1);
+              tphase ^= 1u << nb;
+              tc_fence_after();
+              tmem_ld_32x32b_x32(tcol + nb * BN, r0);
+            }
+            promote32<kFast>(acc[kBlk - 1], r1, sav[b], sbv[kBlk - 1][b], p.zero);
+          }
         }
       }
-      flags |= finish_block(p, acc, I, J, lane);
+#pragma unroll
+      for (int q = 0; q < kBlk; ++q) flags |= finish_block(p, acc[q], I, J0 + q, lane);
     }
     if (lane == 0) raise_flags(p.err, flags);
   }
@@ -864,11 +905,13 @@ struct GemmOptions {
   int ctl_kind = 1;  // control-thread wait flavour (see ctl_wait)
   int ctl_ns = 200;
   int tma_scales = 1;  // gemm_i8s_kernel when the shape allows
+  int s_epi = 16;      // gemm_i8s_kernel promotion warps: 16, or 8 with pipelined TMEM loads
   GemmOptions() {
     if (const char *e = getenv("JF_GEMM_IMPL")) impl = strcmp(e, "h16") == 0 ? 1 : 0;
     if (const char *e = getenv("JF_GEMM_EPI")) epi = atoi(e) == 8 ? 8 : 16;
     if (const char *e = getenv("JF_GEMM_ISSUERS")) issuers = atoi(e) == 3 ? 3 : 1;
     if (const char *e = getenv("JF_GEMM_CTL")) sscanf(e, "%d,%d", &ctl_kind, &ctl_ns);
+    if (const char *e = getenv("JF_GEMM_SEPI")) s_epi = atoi(e) == 8 ? 8 : 16;
   }
 };
 static GemmOptions g_opt;
@@ -880,6 +923,7 @@ extern "C" int jf_gemm_set_option(const char *key, int value) {
   else if (!strcmp(key, "ctl_kind")) g_opt.ctl_kind = value;
   else if (!strcmp(key, "ctl_ns")) g_opt.ctl_ns = value;
   else if (!strcmp(key, "tma_scales")) g_opt.tma_scales = value;
+  else if (!strcmp(key, "s_epi")) g_opt.s_epi = value == 8 ? 8 : 16;
   else return JF_ERR_ARG;
   return JF_OK;
 }
@@ -943,16 +987,19 @@ int jf_gemm_launch(const int8_t *A, int64_t lda, const int8_t *Bt, int64_t ldb, 
                       (sbT ? jf_make_tmap_f32(&tsb, sb, kb, N / 32, sb_s1, 4, 4)
                            : jf_make_tmap_f32(&tsb, sb, N / 32, kb, sb_s0, 4, 4));
       if (!ok) return JF_ERR_LAUNCH;
+      const bool e8 = g_opt.s_epi == 8;
       void (*ks)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap, const Params,
-                 const int, const int) = fast ? gemm_i8s_kernel<true> : gemm_i8s_kernel<false>;
-      static bool sdone[2] = {};
-      if (!sdone[fast]) {
+                 const int, const int) =
+          e8 ? (fast ? gemm_i8s_kernel<true, 8> : gemm_i8s_kernel<false, 8>)
+             : (fast ? gemm_i8s_kernel<true, 16> : gemm_i8s_kernel<false, 16>);
+      static bool sdone[2][2] = {};
+      if (!sdone[e8][fast]) {
         if (cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytesS) !=
             cudaSuccess)
           return jf_launch_check("gemm_i8s attr");
-        sdone[fast] = true;
+        sdone[e8][fast] = true;
       }
-      ks<<<grid, 18 * 32, kSmemBytesS, stream>>>(ta, tb, tsa, tsb, p, saT, sbT);
+      ks<<<grid, (e8 ? 10 : 18) * 32, kSmemBytesS, stream>>>(ta, tb, tsa, tsb, p, saT, sbT);
       return jf_launch_check("gemm_i8s");
     }
   }
