@@ -169,8 +169,8 @@ def build_block(jf, w, attn_dtype, seed=0):
     ln = lambda: jf.NormParams(torch.ones(c, device="cuda"), torch.zeros(c, device="cuda"), cfg.eps)  # noqa: E731
     blk = jf.TransformerBlock(cfg, lin(3 * c, c), lin(c, c), lin(h, c), lin(c, h), ln(), ln(),
                               attn_dtype=attn_dtype)
-    for lyr in (blk.qkv, blk.proj, blk.mlp1, blk.mlp2):  # INT8 weights (+ transposes) built once
-        lyr.weight_q, lyr.weight_qt
+    for lyr in (blk.qkv, blk.proj, blk.mlp1, blk.mlp2):  # INT8 weights built once (dgrad reads W MN-major)
+        lyr.weight_q
     return blk
 
 

@@ -22,7 +22,7 @@ import torch
 import torch.nn as nn
 from torch.utils._pytree import tree_map
 
-from .qgemm import block_mm_forward, block_mm_grad_input, block_mm_grad_weight
+from .qgemm import block_mm_forward, block_mm_grad_input, block_mm_grad_weight, mn_major_ok
 from .qlayers import AttentionCore, BlockConfig, QuantLinear
 from .qnonlinear import (
     NormParams,
@@ -127,7 +127,8 @@ class Linear(torch.autograd.Function):
     def backward(ctx, g):
         dyq = as_block_quant(g)
         lay = ctx.layer
-        dxq = block_mm_grad_input(dyq, lay.weight_q, wt=lay.weight_qt)
+        d, c = lay.master_weight.shape
+        dxq = block_mm_grad_input(dyq, lay.weight_q, wt=None if mn_major_ok(dyq.rows, d, c) else lay.weight_qt)
         _, dw = block_mm_grad_weight(dyq, ctx.xq, out="int8+deq")
         db = column_sum(dyq) if ctx.has_bias else None
         return QTensor(dxq), dw, db, None

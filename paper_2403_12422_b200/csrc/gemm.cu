@@ -409,15 +409,17 @@ constexpr uint32_t kScaleBytes = 256;  // per stage: A box at +0, B box at +128 
 constexpr size_t kSmemBytesS =
     1024 + kStages * (kStageBytesA + kStageBytesB) + kStages * kScaleBytes + sizeof(SmemS) + 64;
 
-// kEpi = 16: 32 columns per promotion warp, one TMEM load per chunk.
-// kEpi = 8: 64 columns per warp (2 per sub-partition, up to 168 registers), the
-// two 32-column halves software-pipelined against each other and against the
-// next chunk's load, so TMEM load latency hides behind promotion math.
-template <bool kFast, int kEpi = 16>
-__global__ void __launch_bounds__((2 + kEpi) * 32, 1)
+// kAmn / kBmn: the operand is MN-major in memory (the UMMA reads int8
+// MN-major tiles directly, so dgrad consumes W [d x c] and wgrad consumes
+// dY [n x d] and X [n x c] as stored -- no transposed copies).  An MN-major
+// stage is a TMA box of 128 K-rows x 128 MN-bytes (SW128); chunk c starts
+// 32 rows = 4096 bytes further, versus 32 bytes for a K-major stage.
+template <bool kFast, bool kAmn, bool kBmn>
+__global__ void __launch_bounds__((2 + 16) * 32, 1)
     gemm_i8s_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmSA, const __grid_constant__ CUtensorMap tmSB,
                     const Params p, const int saT, const int sbT) {
+  constexpr int kEpi = 16;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *base = reinterpret_cast<uint8_t *>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -465,8 +467,11 @@ __global__ void __launch_bounds__((2 + kEpi) * 32, 1)
         for (int ks = 0; ks < nstages_k; ++ks) {
           ctl_wait(p, bar_empty + 8 * stage, phase ^ 1);
           mbar_arrive_expect_tx(&S.full[stage], kStageBytesA + kStageBytesB + 128);
-          tma_load_2d(sA + stage * kStageBytesA, &tmA, &S.full[stage], ks * BK, m0);
-          tma_load_2d(sB + stage * kStageBytesB, &tmB, &S.full[stage], ks * BK, n0);
+          // tensor-map coordinates are {inner, outer}
+          if (kAmn) tma_load_2d(sA + stage * kStageBytesA, &tmA, &S.full[stage], m0, ks * BK);
+          else tma_load_2d(sA + stage * kStageBytesA, &tmA, &S.full[stage], ks * BK, m0);
+          if (kBmn) tma_load_2d(sB + stage * kStageBytesB, &tmB, &S.full[stage], n0, ks * BK);
+          else tma_load_2d(sB + stage * kStageBytesB, &tmB, &S.full[stage], ks * BK, n0);
           uint8_t *ss = sS + stage * kScaleBytes;
           // box {4, 4}: K-contiguous grids -> [row block][chunk], else [chunk][row block]
           if (saT) tma_load_2d(ss, &tmSA, &S.full[stage], m0 / 32, ks * 4);
@@ -485,7 +490,9 @@ __global__ void __launch_bounds__((2 + kEpi) * 32, 1)
     if (lane == 0) {
       const uint64_t adesc0 = smem_desc_sw128(smem_u32(sA), 16, 1024);
       const uint64_t bdesc0 = smem_desc_sw128(smem_u32(sB), 16, 1024);
-      constexpr uint32_t idesc = idesc_i8(BM, BN, 0, 0);
+      constexpr uint32_t idesc = idesc_i8(BM, BN, kAmn ? 1 : 0, kBmn ? 1 : 0);
+      constexpr uint32_t kStepA = kAmn ? (32 * 128) >> 4 : 2;  // descriptor units (16 B) per chunk
+      constexpr uint32_t kStepB = kBmn ? (32 * 128) >> 4 : 2;
       int stage = 0;
       uint32_t phase = 0, tphase = 0;
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -499,7 +506,7 @@ __global__ void __launch_bounds__((2 + kEpi) * 32, 1)
             ctl_wait(p, bar_tempty + 8 * c, ((tphase >> c) & 1) ^ 1);
             tphase ^= 1u << c;
             tc_fence_after();
-            mma_i8_ss(tmem + c * BN, ad + 2 * c, bd + 2 * c, idesc, 0u);
+            mma_i8_ss(tmem + c * BN, ad + kStepA * c, bd + kStepB * c, idesc, 0u);
             mma_commit(&S.tfull[c]);
           }
           mma_commit(&S.empty[stage]);
@@ -512,50 +519,33 @@ __global__ void __launch_bounds__((2 + kEpi) * 32, 1)
     }
   } else {
     // ───────────── promotion + epilogue ─────────────
-    constexpr int kCols = BN * 4 / kEpi;  // 32 or 64 columns per warp
-    const int lq = warp & 3;              // TMEM lane quarter == 32-row block of the tile
-    const int cg = (warp - 2) >> 2;       // column group of the tile
-    const uint32_t tcol = tmem + ((uint32_t)(lq * 32) << 16) + cg * kCols;
+    const int lq = warp & 3;          // TMEM lane quarter == 32-row block of the tile
+    const int cg = (warp - 2) >> 2;   // 32-column group of the tile
+    const uint32_t tcol = tmem + ((uint32_t)(lq * 32) << 16) + cg * 32;
     const uint32_t ssa0 = smem_u32(sS), ssb0 = ssa0 + 128;
-    // float offsets of this warp's scale factors inside the 4x4 boxes
+    // float offsets of this warp's 4 scale factors inside the 4x4 boxes
     const uint32_t oa = saT ? (uint32_t)lq * 4 : (uint32_t)lq * 16;
+    const uint32_t ob = sbT ? (uint32_t)cg * 4 : (uint32_t)cg * 16;
     const uint32_t da = saT ? 16 : 4, db = sbT ? 16 : 4;  // byte step between chunks
-    constexpr int kBlk = kCols / 32;
-    uint32_t ob[kBlk];
-#pragma unroll
-    for (int q = 0; q < kBlk; ++q) {
-      const int jl = cg * kBlk + q;  // 32-col block within the tile
-      ob[q] = sbT ? (uint32_t)jl * 4 : (uint32_t)jl * 16;
-    }
     uint32_t tphase = 0;
     int flags = 0;
     int stage = 0;
     uint32_t phase = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       const int64_t I = (tile % mt) * (BM / 32) + lq;
-      const int64_t J0 = (tile / mt) * (BN / 32) + cg * kBlk;
-      float acc[kBlk][32];
+      const int64_t J = (tile / mt) * (BN / 32) + cg;
+      float acc[32];
 #pragma unroll
-      for (int q = 0; q < kBlk; ++q)
-#pragma unroll
-        for (int j = 0; j < 32; ++j) acc[q][j] = 0.0f;
-      uint32_t r0[32], r1[32];
-      if (kEpi == 8 && tile == blockIdx.x) {  // prologue: first half of the first chunk
-        mbar_wait_u32(bar_tfull, tphase & 1);
-        tphase ^= 1u;
-        tc_fence_after();
-        tmem_ld_32x32b_x32(tcol, r0);
-      }
+      for (int j = 0; j < 32; ++j) acc[j] = 0.0f;
       for (int ks = 0; ks < nstages_k; ++ks) {
         // the stage's scales: acquire the TMA writes, read, release the stage
         mbar_wait_u32(bar_full + 8 * stage, phase);
-        const uint32_t sa_addr = ssa0 + stage * kScaleBytes + oa;
-        float sav[4], sbv[kBlk][4];
+        const uint32_t sa_addr = ssa0 + stage * kScaleBytes + oa, sb_addr = ssb0 + stage * kScaleBytes + ob;
+        float sav[4], sbv[4];
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
           sav[b] = lds_f32(sa_addr + b * da);
-#pragma unroll
-          for (int q = 0; q < kBlk; ++q) sbv[q][b] = lds_f32(ssb0 + stage * kScaleBytes + ob[q] + b * db);
+          sbv[b] = lds_f32(sb_addr + b * db);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive_u32(bar_empty + 8 * stage);
@@ -565,40 +555,19 @@ __global__ void __launch_bounds__((2 + kEpi) * 32, 1)
         }
 #pragma unroll
         for (int b = 0; b < kTmemBufs; ++b) {
-          if (kEpi == 16) {
-            mbar_wait_u32(bar_tfull + 8 * b, (tphase >> b) & 1);
-            tphase ^= 1u << b;
-            tc_fence_after();
-            tmem_ld_32x32b_x32(tcol + b * BN, r0);
-            tmem_wait_ld();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_u32(bar_tempty + 8 * b);
-            promote32<kFast>(acc[0], r0, sav[b], sbv[0][b], p.zero);
-          } else {
-            // r0 = this chunk's cols 0..31, in flight or ready
-            tmem_wait_ld();
-            tmem_ld_32x32b_x32(tcol + b * BN + 32, r1);
-            promote32<kFast>(acc[0], r0, sav[b], sbv[0][b], p.zero);
-            tmem_wait_ld();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_u32(bar_tempty + 8 * b);
-            // next chunk's first half (the next tile's after this tile's last chunk)
-            const int nb = (b + 1) & 3;
-            const bool more = (b < kTmemBufs - 1) || (ks + 1 < nstages_k) || (tile + gridDim.x < ntiles);
-            if (more) {
-              mbar_wait_u32(bar_tfull + 8 * nb, (tphase >> nb) & 1);
-              tphase ^= 1u << nb;
-              tc_fence_after();
-              tmem_ld_32x32b_x32(tcol + nb * BN, r0);
-            }
-            promote32<kFast>(acc[kBlk - 1], r1, sav[b], sbv[kBlk - 1][b], p.zero);
-          }
+          mbar_wait_u32(bar_tfull + 8 * b, (tphase >> b) & 1);
+          tphase ^= 1u << b;
+          tc_fence_after();
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tcol + b * BN, r);
+          tmem_wait_ld();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_u32(bar_tempty + 8 * b);
+          promote32<kFast>(acc, r, sav[b], sbv[b], p.zero);
         }
       }
-#pragma unroll
-      for (int q = 0; q < kBlk; ++q) flags |= finish_block(p, acc[q], I, J0 + q, lane);
+      flags |= finish_block(p, acc, I, J, lane);
     }
     if (lane == 0) raise_flags(p.err, flags);
   }
@@ -905,13 +874,11 @@ struct GemmOptions {
   int ctl_kind = 1;  // control-thread wait flavour (see ctl_wait)
   int ctl_ns = 200;
   int tma_scales = 1;  // gemm_i8s_kernel when the shape allows
-  int s_epi = 16;      // gemm_i8s_kernel promotion warps: 16, or 8 with pipelined TMEM loads
   GemmOptions() {
     if (const char *e = getenv("JF_GEMM_IMPL")) impl = strcmp(e, "h16") == 0 ? 1 : 0;
     if (const char *e = getenv("JF_GEMM_EPI")) epi = atoi(e) == 8 ? 8 : 16;
     if (const char *e = getenv("JF_GEMM_ISSUERS")) issuers = atoi(e) == 3 ? 3 : 1;
     if (const char *e = getenv("JF_GEMM_CTL")) sscanf(e, "%d,%d", &ctl_kind, &ctl_ns);
-    if (const char *e = getenv("JF_GEMM_SEPI")) s_epi = atoi(e) == 8 ? 8 : 16;
   }
 };
 static GemmOptions g_opt;
@@ -923,9 +890,64 @@ extern "C" int jf_gemm_set_option(const char *key, int value) {
   else if (!strcmp(key, "ctl_kind")) g_opt.ctl_kind = value;
   else if (!strcmp(key, "ctl_ns")) g_opt.ctl_ns = value;
   else if (!strcmp(key, "tma_scales")) g_opt.tma_scales = value;
-  else if (!strcmp(key, "s_epi")) g_opt.s_epi = value == 8 ? 8 : 16;
   else return JF_ERR_ARG;
   return JF_OK;
+}
+
+// gemm_i8s_kernel launch.  A is [M x K] (K-major) or [K x M] (a_mn: MN-major), row
+// stride lda bytes; likewise B as [N x K] or [K x N].  Returns -1 when the shape
+// or the scale-grid layout does not qualify (caller falls back).
+static int launch_i8s(const int8_t *A, bool a_mn, int64_t lda, const int8_t *B, bool b_mn, int64_t ldb, int64_t M,
+                      int64_t N, int64_t K, const float *sa, int64_t sa_s0, int64_t sa_s1, const float *sb,
+                      int64_t sb_s0, int64_t sb_s1, const float *bias, int mode, int out_kind, int8_t *yq,
+                      float *ys, void *yf, int32_t *err, cudaStream_t stream) {
+  using namespace jf::gemm;
+  if (!g_opt.tma_scales || out_kind == OUT_I32 || M % 128 || N % 128 || K % 128 || lda % 16 || ldb % 16 ||
+      (uintptr_t)A % 16 || (uintptr_t)B % 16)
+    return -1;
+  // scale grids: each contiguous along K or along M/N, 16-byte row pitch
+  auto grid_ok = [](const float *s, int64_t s0, int64_t s1) {
+    return ((uintptr_t)s % 16 == 0) && ((s1 == 1 && s0 % 4 == 0) || (s0 == 1 && s1 % 4 == 0));
+  };
+  if (!grid_ok(sa, sa_s0, sa_s1) || !grid_ok(sb, sb_s0, sb_s1)) return -1;
+  const int64_t kb = K / 32;
+  const int saT = sa_s1 != 1, sbT = sb_s1 != 1;
+  CUtensorMap ta, tb, tsa, tsb;
+  const bool ok =
+      (a_mn ? jf_make_tmap_i8(&ta, A, K, M, lda, BM, BK, true) : jf_make_tmap_i8(&ta, A, M, K, lda, BK, BM, true)) &&
+      (b_mn ? jf_make_tmap_i8(&tb, B, K, N, ldb, BN, BK, true) : jf_make_tmap_i8(&tb, B, N, K, ldb, BK, BN, true)) &&
+      (saT ? jf_make_tmap_f32(&tsa, sa, kb, M / 32, sa_s1, 4, 4) : jf_make_tmap_f32(&tsa, sa, M / 32, kb, sa_s0, 4, 4)) &&
+      (sbT ? jf_make_tmap_f32(&tsb, sb, kb, N / 32, sb_s1, 4, 4) : jf_make_tmap_f32(&tsb, sb, N / 32, kb, sb_s0, 4, 4));
+  if (!ok) return JF_ERR_LAUNCH;
+  Params p{M, N, K, sa, sa_s0, sa_s1, sb, sb_s0, sb_s1, bias, yq, ys, (float *)yf, err, out_kind, 0.0f, nullptr,
+           g_opt.ctl_kind, (uint32_t)g_opt.ctl_ns};
+  const bool fast = mode == JF_MODE_FAST;
+  using KFn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap, const Params,
+                       const int, const int);
+  KFn ks;
+  int ki;
+  if (!a_mn && !b_mn) {
+    ks = fast ? gemm_i8s_kernel<true, false, false> : gemm_i8s_kernel<false, false, false>;
+    ki = 0;
+  } else if (!a_mn && b_mn) {
+    ks = fast ? gemm_i8s_kernel<true, false, true> : gemm_i8s_kernel<false, false, true>;
+    ki = 1;
+  } else if (a_mn && b_mn) {
+    ks = fast ? gemm_i8s_kernel<true, true, true> : gemm_i8s_kernel<false, true, true>;
+    ki = 2;
+  } else {
+    return -1;
+  }
+  static bool done[3][2] = {};
+  if (!done[ki][fast]) {
+    if (cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytesS) != cudaSuccess)
+      return jf_launch_check("gemm_i8s attr");
+    done[ki][fast] = true;
+  }
+  const int64_t tiles = (M / BM) * (N / BN);
+  const int grid = (int)(tiles < jf_num_sms() ? tiles : jf_num_sms());
+  ks<<<grid, 18 * 32, kSmemBytesS, stream>>>(ta, tb, tsa, tsb, p, saT, sbT);
+  return jf_launch_check("gemm_i8s");
 }
 
 // Core launcher: A [M x K] (row stride lda), Bt [N x K] (row stride ldb), both K-major codes.
@@ -973,35 +995,10 @@ int jf_gemm_launch(const int8_t *A, int64_t lda, const int8_t *Bt, int64_t ldb, 
     hk<<<grid, h16::kWarps * 32, h16::kSmemBytes, stream>>>(ta, tb, p);
     return jf_launch_check("gemm_h16");
   }
-  if (!partials && g_opt.tma_scales && M % 128 == 0 && N % 128 == 0 && K % 128 == 0) {
-    // scale grids by TMA: each must be contiguous along K or along M/N, 16-byte row pitch
-    const int64_t kb = K / 32;
-    auto grid_ok = [&](const float *s, int64_t s0, int64_t s1) {
-      return ((uintptr_t)s % 16 == 0) && ((s1 == 1 && s0 % 4 == 0) || (s0 == 1 && s1 % 4 == 0));
-    };
-    if (grid_ok(sa, sa_s0, sa_s1) && grid_ok(sb, sb_s0, sb_s1)) {
-      const int saT = sa_s1 != 1, sbT = sb_s1 != 1;
-      CUtensorMap tsa, tsb;
-      const bool ok = (saT ? jf_make_tmap_f32(&tsa, sa, kb, M / 32, sa_s1, 4, 4)
-                           : jf_make_tmap_f32(&tsa, sa, M / 32, kb, sa_s0, 4, 4)) &&
-                      (sbT ? jf_make_tmap_f32(&tsb, sb, kb, N / 32, sb_s1, 4, 4)
-                           : jf_make_tmap_f32(&tsb, sb, N / 32, kb, sb_s0, 4, 4));
-      if (!ok) return JF_ERR_LAUNCH;
-      const bool e8 = g_opt.s_epi == 8;
-      void (*ks)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap, const Params,
-                 const int, const int) =
-          e8 ? (fast ? gemm_i8s_kernel<true, 8> : gemm_i8s_kernel<false, 8>)
-             : (fast ? gemm_i8s_kernel<true, 16> : gemm_i8s_kernel<false, 16>);
-      static bool sdone[2][2] = {};
-      if (!sdone[e8][fast]) {
-        if (cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytesS) !=
-            cudaSuccess)
-          return jf_launch_check("gemm_i8s attr");
-        sdone[e8][fast] = true;
-      }
-      ks<<<grid, (e8 ? 10 : 18) * 32, kSmemBytesS, stream>>>(ta, tb, tsa, tsb, p, saT, sbT);
-      return jf_launch_check("gemm_i8s");
-    }
+  if (!partials && !h16p) {
+    const int rc = launch_i8s(A, false, lda, Bt, false, ldb, M, N, K, sa, sa_s0, sa_s1, sb, sb_s0, sb_s1, bias,
+                              mode, out_kind, yq, ys, yf, err, stream);
+    if (rc >= 0) return rc;
   }
   const int epi = g_opt.epi, iss_env = g_opt.issuers;
   // multi-issuer pipeline needs whole 4-chunk stages (K % 128 == 0)
@@ -1048,6 +1045,12 @@ extern "C" int jf_gemm_dgrad(const int8_t *dy, const float *dys, const int8_t *w
                              const int8_t *wt, const float *wts, int64_t n, int64_t d, int64_t c,
                              int32_t mode, int32_t out_kind, int8_t *dxq, float *dxs, float *dxf,
                              void *scratch, int32_t *err, jf_stream_t stream) {
+  // W [d x c] is the MN-major B operand as stored (no W^T needed)
+  {
+    const int rc = launch_i8s(dy, false, d, w, true, c, n, c, d, dys, d / 32, 1, ws, 1, c / 32, nullptr, mode,
+                              out_kind, dxq, dxs, dxf, err, (cudaStream_t)stream);
+    if (rc >= 0) return rc;
+  }
   if (wt == nullptr) {
     if (scratch == nullptr) return JF_ERR_ARG;
     int8_t *t = static_cast<int8_t *>(scratch);
@@ -1069,6 +1072,12 @@ extern "C" int jf_gemm_wgrad(const int8_t *dy, const float *dys, const int8_t *x
                              const float *xts, int64_t n, int64_t d, int64_t c, int32_t mode,
                              int32_t out_kind, int8_t *dwq, float *dws, float *dwf, void *scratch,
                              int32_t *err, jf_stream_t stream) {
+  // dY [n x d] and X [n x c] are the MN-major A and B operands as stored (no transposes)
+  {
+    const int rc = launch_i8s(dy, true, d, x, true, c, d, c, n, dys, 1, d / 32, xs, 1, c / 32, nullptr, mode,
+                              out_kind, dwq, dws, dwf, err, (cudaStream_t)stream);
+    if (rc >= 0) return rc;
+  }
   int8_t *s8 = static_cast<int8_t *>(scratch);
   if (dyt == nullptr) {
     if (scratch == nullptr) return JF_ERR_ARG;

@@ -240,6 +240,12 @@ def block_mm_forward(xq: BlockQuantTensor, wq: BlockQuantTensor, cfg: TileConfig
     return _finish(yq, yf, mode, out)
 
 
+def mn_major_ok(*dims: int) -> bool:
+    """True when the GEMM reads MN-major operands as stored (every dim a multiple of 128):
+    dgrad then needs no W^T and wgrad no transposed dY / X (libjetfire gemm_i8s_kernel)."""
+    return _rt.gemm_option("tma_scales") != 0 and all(d % 128 == 0 for d in dims)
+
+
 def block_mm_grad_input(dyq: BlockQuantTensor, wq: BlockQuantTensor, cfg: TileConfig | None = None,
                         mode: ExecMode = ExecMode.INT8_DATA_FLOW,
                         counters: AccessCounters | None = None, *, threads: int = 1,
@@ -260,12 +266,12 @@ def block_mm_grad_input(dyq: BlockQuantTensor, wq: BlockQuantTensor, cfg: TileCo
         _count_call(counters, dyq.rows, dyq.cols, wq.cols, cfg, mode, quantize)
     L = _lib.lib()
     n, d, c = dyq.rows, dyq.cols, wq.cols
-    if wt is None:
+    if wt is None and not mn_major_ok(n, d, c):
         wt = wq.transposed()
     yq, yf = _outputs(n, c, dyq.device, out)
     _lib.check(_timed("dgrad", 2 * n * d * c, lambda: L.jf_gemm_dgrad(
         dyq.values.data_ptr(), dyq.scales.data_ptr(), wq.values.data_ptr(), wq.scales.data_ptr(),
-        wt.values.data_ptr(), wt.scales.data_ptr(), n, d, c,
+        _lib.ptr(wt and wt.values), _lib.ptr(wt and wt.scales), n, d, c,
         _rt.promotion_code(promotion), _OUT_KIND[out], _lib.ptr(yq and yq.values),
         _lib.ptr(yq and yq.scales), _lib.ptr(yf), None, _rt.err_ptr(),
         _lib.stream_handle())), "gemm_dgrad")
@@ -288,12 +294,15 @@ def block_mm_grad_weight(dyq: BlockQuantTensor, xq: BlockQuantTensor, cfg: TileC
         _count_call(counters, dyq.cols, dyq.rows, xq.cols, cfg, mode, quantize)
     L = _lib.lib()
     n, d, c = dyq.rows, dyq.cols, xq.cols
-    dyt = dyq.transposed()   # dY^T [d x n]: the K(=tokens)-major operands (codes + grid)
-    xt = xq.transposed()     # X^T [c x n]
+    dyt = xt = None
+    if not mn_major_ok(n, d, c):  # generic shapes: K(=tokens)-major transposed copies
+        dyt = dyq.transposed()   # dY^T [d x n] (codes + grid)
+        xt = xq.transposed()     # X^T [c x n]
     yq, yf = _outputs(d, c, dyq.device, out)
     _lib.check(_timed("wgrad", 2 * n * d * c, lambda: L.jf_gemm_wgrad(
         dyq.values.data_ptr(), dyq.scales.data_ptr(), xq.values.data_ptr(), xq.scales.data_ptr(),
-        dyt.values.data_ptr(), dyt.scales.data_ptr(), xt.values.data_ptr(), xt.scales.data_ptr(), n, d, c,
+        _lib.ptr(dyt and dyt.values), _lib.ptr(dyt and dyt.scales), _lib.ptr(xt and xt.values),
+        _lib.ptr(xt and xt.scales), n, d, c,
         _rt.promotion_code(promotion), _OUT_KIND[out],
         _lib.ptr(yq and yq.values), _lib.ptr(yq and yq.scales), _lib.ptr(yf), None, _rt.err_ptr(),
         _lib.stream_handle())), "gemm_wgrad")

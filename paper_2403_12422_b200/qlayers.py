@@ -17,7 +17,14 @@ import numpy as np
 import torch
 import torch.nn.functional as F
 
-from .qgemm import AccessCounters, TileConfig, block_mm_forward, block_mm_grad_input, block_mm_grad_weight
+from .qgemm import (
+    AccessCounters,
+    TileConfig,
+    block_mm_forward,
+    block_mm_grad_input,
+    block_mm_grad_weight,
+    mn_major_ok,
+)
 from .qnonlinear import (
     DropoutState,
     NormParams,
@@ -106,7 +113,8 @@ class QuantLinear:
 
     @property
     def weight_qt(self) -> BlockQuantTensor:
-        """W^T codes + scales, cached with weight_q (operand of the dgrad GEMM)."""
+        """W^T codes + scales, cached with weight_q (dgrad operand for shapes that are not
+        multiples of 128; otherwise the GEMM reads W MN-major as stored)."""
         if self._weight_qt is None:
             self._weight_qt = self.weight_q.transposed()
         return self._weight_qt
@@ -126,8 +134,10 @@ class QuantLinear:
         """(dX quantized, dW FP32 = deq(requant(dY^T X)), dbias FP32)."""
         if self.saved_input is None:
             raise RuntimeError("backward called before forward")
+        d, c = self.master_weight.shape
+        wt = None if mn_major_ok(dyq.rows, d, c) else self.weight_qt  # W^T only for generic shapes
         dxq = block_mm_grad_input(dyq, self.weight_q, cfg=self.cfg, counters=counters,
-                                  threads=threads, wt=self.weight_qt)
+                                  threads=threads, wt=wt)
         _, dw = block_mm_grad_weight(dyq, self.saved_input, cfg=self.cfg, counters=counters,
                                      threads=threads, out="int8+deq")
         dbias = None if self.bias is None else column_sum(dyq)

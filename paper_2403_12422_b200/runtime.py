@@ -21,6 +21,7 @@ _MSG_OVERFLOW = "scale overflows the binary16 range; input magnitude too large"
 
 _state = threading.local()
 _config = {"error_check": "eager", "promotion": "exact"}
+_gemm_options = {"tma_scales": 1}
 
 
 def set_error_check(mode: str) -> None:
@@ -39,6 +40,20 @@ def set_promotion(mode: str) -> None:
     if mode not in ("exact", "fast"):
         raise ValueError(f"promotion must be 'exact' or 'fast', got {mode!r}")
     _config["promotion"] = mode
+
+
+def set_gemm_option(key: str, value: int) -> None:
+    """Diagnostics / A-B: libjetfire GEMM launch option (jf_gemm_set_option).  Results are
+    bit-identical for every option; ``tma_scales=0`` also brings back the transposed
+    operand copies the generic kernel needs."""
+    rc = _lib.lib().jf_gemm_set_option(key.encode(), int(value))
+    if rc != 0:
+        raise ValueError(f"unknown GEMM option {key!r}")
+    _gemm_options[key] = int(value)
+
+
+def gemm_option(key: str) -> int | None:
+    return _gemm_options.get(key)
 
 
 def get_promotion() -> str:

@@ -196,6 +196,36 @@ def test_gemm_random_exact_vs_oracle(jf, n, c, d):
     assert same(jf.block_mm_grad_weight(DY, X, quantize=False), acc)
 
 
+@pytest.mark.parametrize("promotion", ["exact", "fast"])
+def test_gemm_paths_bit_identical(jf, promotion):
+    """Staged-scales kernel with MN-major operands (dgrad reads W, wgrad reads dY and X as
+    stored) vs the generic kernel on transposed copies: same bits, every output kind."""
+    from paper_2403_12422_b200 import runtime
+
+    rng = np.random.default_rng(5)
+    n, c, d = 256, 384, 512
+    X = bqt(jf, *_rand_q(rng, (n, c)))
+    W = bqt(jf, *_rand_q(rng, (d, c), 1 / np.sqrt(c)))
+    DY = bqt(jf, *_rand_q(rng, (n, d), 0.1))
+    bias = cu((0.1 * rng.standard_normal(d)).astype(np.float32))
+    def run():
+        return (jf.block_mm_forward(X, W, bias=bias, promotion=promotion),
+                jf.block_mm_grad_input(DY, W, promotion=promotion, wt=W.transposed()),
+                jf.block_mm_grad_weight(DY, X, promotion=promotion, out="int8+deq"),
+                jf.block_mm_grad_weight(DY, X, promotion=promotion, quantize=False))
+    try:
+        staged = run()
+        runtime.set_gemm_option("tma_scales", 0)
+        generic = run()
+    finally:
+        runtime.set_gemm_option("tma_scales", 1)
+    for a, b in ((staged[0], generic[0]), (staged[1], generic[1])):
+        assert torch.equal(a.values, b.values) and torch.equal(a.scales, b.scales)
+    assert torch.equal(staged[2][0].values, generic[2][0].values)
+    assert torch.equal(staged[2][1], generic[2][1])
+    assert torch.equal(staged[3], generic[3])
+
+
 def test_gemm_fast_mode_tolerance(jf):
     if True:
         rng = np.random.default_rng(77)

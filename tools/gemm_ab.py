@@ -15,17 +15,15 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2403_12422_b200 as jf  # noqa: E402
-from paper_2403_12422_b200 import _lib  # noqa: E402
 
 SHAPES = {"qkv": (4096, 4096, 12288), "proj": (4096, 4096, 4096), "mlp1": (4096, 4096, 16384),
           "mlp2": (4096, 16384, 4096)}
 
 
 def apply(cfg: str):
-    L = _lib.lib()
     for kv in filter(None, cfg.split(",")):
         k, v = kv.split("=")
-        assert L.jf_gemm_set_option(k.encode(), int(v)) == 0, kv
+        jf.runtime.set_gemm_option(k, int(v))
 
 
 def main():
