@@ -67,6 +67,18 @@ int jf_dequantize_f32(const int8_t *q, const float *s, int64_t n, int64_t c, flo
 int jf_dequantize_bf16(const int8_t *q, const float *s, int64_t n, int64_t c, uint16_t *y,
                        jf_stream_t stream);
 
+/* The attention boundary (qlayers.py:350-351 forward, :406-408 backward).
+ * jf_dequantize_qkv_heads: QKV codes [n x 3c] (n = batch*seq, c = heads*head_dim) -> q, k, v
+ *   bf16, each contiguous [batch, heads, seq, head_dim] (head_dim % 16 == 0).
+ * jf_quantize_heads_bf16: bf16 x[batch, seq, heads, head_dim] with element strides
+ *   (sb, ss, sh, 1) -> codes/scales of an [n x c] block tensor written into a column slice:
+ *   q (row stride ldq bytes) and s (row stride lds floats) point at the slice. */
+int jf_dequantize_qkv_heads(const int8_t *q, const float *s, int64_t batch, int64_t seq, int64_t heads,
+                            int64_t head_dim, uint16_t *yq, uint16_t *yk, uint16_t *yv, jf_stream_t stream);
+int jf_quantize_heads_bf16(const uint16_t *x, int64_t batch, int64_t seq, int64_t heads, int64_t head_dim,
+                           int64_t sb, int64_t ss, int64_t sh, int8_t *q, int64_t ldq, float *s, int64_t lds,
+                           int32_t *err, jf_stream_t stream);
+
 /* BlockQuantTensor.transposed()  [qtensor.py:130-136]: qt [c x n], st [c/32 x n/32]. */
 int jf_transpose(const int8_t *q, const float *s, int64_t n, int64_t c, int8_t *qt, float *st,
                  jf_stream_t stream);

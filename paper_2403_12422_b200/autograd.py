@@ -185,13 +185,18 @@ class Attention(torch.autograd.Function):
     @staticmethod
     def forward(ctx, qkv, batch, seq, heads, dtype):
         core = AttentionCore(heads, qkv.shape[1] // 3 // heads, dtype=dtype)
-        out = core.forward(dequantize(qkv.bq, dtype), batch, seq)
         ctx.core, ctx.batch, ctx.seq = core, batch, seq
+        if core.supports_q():
+            return QTensor(core.forward_q(qkv.bq, batch, seq))
+        out = core.forward(dequantize(qkv.bq, dtype), batch, seq)
         return QTensor(quantize_per_block(out))
 
     @staticmethod
     def backward(ctx, g):
-        d = ctx.core.backward(dequantize(as_block_quant(g), ctx.core.dtype), ctx.batch, ctx.seq)
+        core = ctx.core
+        if core.supports_q():
+            return QTensor(core.backward_q(as_block_quant(g), ctx.batch, ctx.seq)), None, None, None, None
+        d = core.backward(dequantize(as_block_quant(g), core.dtype), ctx.batch, ctx.seq)
         return QTensor(quantize_per_block(d)), None, None, None, None
 
 

@@ -91,6 +91,74 @@ __global__ void __launch_bounds__(256) dequantize_kernel(const int8_t *__restric
   }
 }
 
+// ── the attention boundary (qlayers.py:350-351, 406-408) ────────────────
+// The FP island runs torch SDPA on per-head [batch, heads, seq, head_dim]
+// bf16 tensors.  These two kernels move between that layout and the INT8
+// [tokens, channels] BlockQuantTensors directly, so no transposed / sliced
+// copies are materialized around the attention call.
+
+// QKV codes [n x 3c] (n = batch*seq, c = heads*hd) -> q, k, v bf16, each
+// contiguous [batch, heads, seq, hd].  16 codes per thread (hd % 16 == 0).
+__global__ void __launch_bounds__(256) dequant_qkv_heads_kernel(const int8_t *__restrict__ q,
+                                                                const float *__restrict__ s, int64_t n,
+                                                                int64_t c, int64_t seq, int64_t heads,
+                                                                int64_t hd, uint16_t *yq, uint16_t *yk,
+                                                                uint16_t *yv) {
+  const int64_t c3 = 3 * c;
+  const int64_t total = n * c3 / 16;
+  const int64_t cb = c3 >> 5;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = i * 16;
+    const int64_t r = e / c3, cc = e - r * c3;
+    const float sc = __ldg(s + (r >> 5) * cb + (cc >> 5));
+    const uint4 w = __ldg(reinterpret_cast<const uint4 *>(q) + i);
+    const uint32_t u[4] = {w.x, w.y, w.z, w.w};
+    uint32_t o[8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float f0 = __fmul_rn(code_at(u[k], 0), sc), f1 = __fmul_rn(code_at(u[k], 1), sc);
+      const float f2 = __fmul_rn(code_at(u[k], 2), sc), f3 = __fmul_rn(code_at(u[k], 3), sc);
+      __nv_bfloat162 a = __floats2bfloat162_rn(f0, f1), b = __floats2bfloat162_rn(f2, f3);
+      o[2 * k] = *reinterpret_cast<uint32_t *>(&a);
+      o[2 * k + 1] = *reinterpret_cast<uint32_t *>(&b);
+    }
+    const int64_t which = cc / c, jj = cc - which * c;
+    const int64_t h = jj / hd, d = jj - h * hd;
+    const int64_t b = r / seq, sq = r - b * seq;
+    uint16_t *base = which == 0 ? yq : (which == 1 ? yk : yv);
+    uint4 *dst = reinterpret_cast<uint4 *>(base + ((b * heads + h) * seq + sq) * hd + d);
+    dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
+    dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
+  }
+}
+
+// bf16 x[batch, seq, heads, hd] with element strides (sb, ss, sh, 1) -> INT8
+// [n x c] block tensor written into a column slice (codes stride ldq, grid
+// stride lds).  Quantization as K1 (qtensor.py:219-246).
+__global__ void __launch_bounds__(kTileThreads) quantize_heads_kernel(
+    const uint16_t *__restrict__ x, int64_t n, int64_t c, int64_t seq, int64_t hd, int64_t sb, int64_t ss,
+    int64_t sh, int8_t *q, int64_t ldq, float *s, int64_t lds, int32_t *err) {
+  __shared__ uint32_t red[64];
+  const TilePos t = tile_pos(n, c);
+  float v[4][8];
+  if (t.active) {
+    const int64_t j = t.col(), h = j / hd, d = j - h * hd;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t r = t.row(i), b = r / seq, sq = r - b * seq;
+      const uint4 w = __ldg(reinterpret_cast<const uint4 *>(x + b * sb + sq * ss + h * sh + d));
+      const uint32_t u[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        v[i][2 * k] = __uint_as_float(u[k] << 16);
+        v[i][2 * k + 1] = __uint_as_float(u[k] & 0xffff0000u);
+      }
+    }
+  }
+  quant_store_ld(t, v, q, ldq, s, lds, red, err);
+}
+
 // Transpose codes [n x c] -> [c x n] via a 64x64 smem tile; scales transpose
 // alongside (the 2x2 scale blocks of the tile).
 __global__ void __launch_bounds__(256) transpose_kernel(const int8_t *__restrict__ q,
@@ -169,6 +237,26 @@ extern "C" int jf_dequantize_bf16(const int8_t *q, const float *s, int64_t n, in
   if (n % 32 || c % 32 || n <= 0 || c <= 0) return JF_ERR_ARG;
   dequantize_kernel<true><<<dq_grid(n, c), 256, 0, (cudaStream_t)stream>>>(q, s, n, c, y);
   return jf_launch_check("dequantize_bf16");
+}
+
+extern "C" int jf_dequantize_qkv_heads(const int8_t *q, const float *s, int64_t batch, int64_t seq,
+                                       int64_t heads, int64_t head_dim, uint16_t *yq, uint16_t *yk, uint16_t *yv,
+                                       jf_stream_t stream) {
+  const int64_t n = batch * seq, c = heads * head_dim;
+  if (n % 32 || c % 32 || n <= 0 || c <= 0 || head_dim % 16) return JF_ERR_ARG;
+  dequant_qkv_heads_kernel<<<dq_grid(n, 3 * c), 256, 0, (cudaStream_t)stream>>>(q, s, n, c, seq, heads, head_dim,
+                                                                              yq, yk, yv);
+  return jf_launch_check("dequant_qkv_heads");
+}
+
+extern "C" int jf_quantize_heads_bf16(const uint16_t *x, int64_t batch, int64_t seq, int64_t heads,
+                                      int64_t head_dim, int64_t sb, int64_t ss, int64_t sh, int8_t *q, int64_t ldq,
+                                      float *s, int64_t lds, int32_t *err, jf_stream_t stream) {
+  const int64_t n = batch * seq, c = heads * head_dim;
+  if (n % 32 || c % 32 || n <= 0 || c <= 0 || head_dim % 8 || ldq < c || (sb | ss | sh) % 8) return JF_ERR_ARG;
+  quantize_heads_kernel<<<tile_grid(n, c), kTileThreads, 0, (cudaStream_t)stream>>>(
+      x, n, c, seq, head_dim, sb, ss, sh, q, ldq, s, lds, err);
+  return jf_launch_check("quantize_heads");
 }
 
 extern "C" int jf_transpose(const int8_t *q, const float *s, int64_t n, int64_t c, int8_t *qt,

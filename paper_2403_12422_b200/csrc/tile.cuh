@@ -96,6 +96,46 @@ JF_DEV void quant_store(const TilePos &t, const float (&v)[4][8], int8_t *__rest
   __syncthreads();
 }
 
+// quant_store into a column slice of a wider BlockQuantTensor: codes row stride
+// ldq, scale grid row stride lds (q and s already offset to the slice).
+JF_DEV void quant_store_ld(const TilePos &t, const float (&v)[4][8], int8_t *__restrict__ q, int64_t ldq,
+                           float *__restrict__ s, int64_t lds, uint32_t *red, int32_t *err) {
+  uint32_t m = 0;
+  if (t.active) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) m = max(m, abs_bits(v[i][j]));
+  }
+  m = max(m, __shfl_xor_sync(0xffffffffu, m, 1));
+  m = max(m, __shfl_xor_sync(0xffffffffu, m, 2));
+  const int qb = t.lane >> 2;
+  if ((t.lane & 3) == 0) red[t.warp * 8 + qb] = m;
+  __syncthreads();
+  uint32_t am = 0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) am = max(am, red[w * 8 + qb]);
+  int flags = 0;
+  const float sc = block_scale(am, flags);
+  const float rc = __frcp_rn(sc);
+  if (t.active) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      uint2 w;
+      w.x = pack4(quant_code_fast(v[i][0], sc, rc), quant_code_fast(v[i][1], sc, rc),
+                  quant_code_fast(v[i][2], sc, rc), quant_code_fast(v[i][3], sc, rc));
+      w.y = pack4(quant_code_fast(v[i][4], sc, rc), quant_code_fast(v[i][5], sc, rc),
+                  quant_code_fast(v[i][6], sc, rc), quant_code_fast(v[i][7], sc, rc));
+      *reinterpret_cast<uint2 *>(q + t.row(i) * ldq + t.col()) = w;
+    }
+    if (t.warp == 0 && (t.lane & 3) == 0) {
+      s[(t.r0 >> 5) * lds + (t.col() >> 5)] = sc;
+      raise_flags(err, flags);
+    }
+  }
+  __syncthreads();
+}
+
 inline dim3 tile_grid(int64_t n, int64_t c) {
   return dim3((unsigned)((c + kTileCols - 1) / kTileCols), (unsigned)(n / kTileRows));
 }

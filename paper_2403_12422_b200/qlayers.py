@@ -37,7 +37,9 @@ from .qnonlinear import (
     layernorm_backward,
     layernorm_forward,
 )
-from .qtensor import BlockQuantTensor, dequantize, quantize_per_block
+from . import _lib
+from . import runtime as _rt
+from .qtensor import BlockQuantTensor, dequantize, empty_like_shape, quantize_per_block
 
 
 @dataclass(frozen=True)
@@ -184,6 +186,62 @@ class AttentionCore:
         self._saved = None
         return g
 
+    # ── INT8 boundary without dense intermediates (BF16 island) ──
+    def supports_q(self) -> bool:
+        return self.dtype == torch.bfloat16 and self.head_dim % 16 == 0
+
+    def forward_q(self, qkv_q: BlockQuantTensor, batch: int, seq: int) -> BlockQuantTensor:
+        """deq(QKV) -> SDPA -> quantize (qlayers.py:350-351), per-head layouts end to end:
+        the codes are dequantized straight into contiguous [b, h, s, d] q/k/v and the
+        attention output is quantized from whatever strides SDPA returns."""
+        c = self.heads * self.head_dim
+        if qkv_q.shape != (batch * seq, 3 * c):
+            raise ValueError(f"expected ({batch * seq}, {3 * c}), got {qkv_q.shape}")
+        L = _lib.lib()
+        shape = (batch, self.heads, seq, self.head_dim)
+        q, k, v = (torch.empty(shape, dtype=torch.bfloat16, device=qkv_q.device) for _ in range(3))
+        _lib.check(L.jf_dequantize_qkv_heads(qkv_q.values.data_ptr(), qkv_q.scales.data_ptr(), batch, seq,
+                                             self.heads, self.head_dim, q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                                             _lib.stream_handle()), "dequant_qkv_heads")
+        q.requires_grad_(True)
+        k.requires_grad_(True)
+        v.requires_grad_(True)
+        with torch.enable_grad():
+            o = F.scaled_dot_product_attention(q, k, v, is_causal=self.causal)
+        self._saved = (q, k, v, o)
+        out = empty_like_shape(batch * seq, c, qkv_q.device)
+        _quantize_heads(o.detach(), out, 0)
+        return out
+
+    def backward_q(self, dattn_q: BlockQuantTensor, batch: int, seq: int) -> BlockQuantTensor:
+        """deq(dO) -> SDPA backward -> quantize dQ|dK|dV into one [N, 3C] tensor (qlayers.py:406-408)."""
+        if self._saved is None:
+            raise RuntimeError("backward called before forward")
+        q, k, v, o = self._saved
+        self._saved = None
+        c = self.heads * self.head_dim
+        dout = dequantize(dattn_q, torch.bfloat16).view(batch, seq, self.heads, self.head_dim).transpose(1, 2)
+        dq, dk, dv = torch.autograd.grad(o, (q, k, v), dout)
+        dqkv = empty_like_shape(batch * seq, 3 * c, dattn_q.device)
+        for i, g in enumerate((dq, dk, dv)):
+            _quantize_heads(g, dqkv, i * c)
+        return dqkv
+
+
+def _quantize_heads(t: torch.Tensor, out: BlockQuantTensor, col0: int) -> None:
+    """bf16 t [b, h, s, d] (any strides with a contiguous d) -> columns [col0, col0 + h*d) of out."""
+    b, h, s, d = t.shape
+    sb, sh, ss, sd = t.stride()
+    if sd != 1:
+        t = t.contiguous()
+        sb, sh, ss, sd = t.stride()
+    L = _lib.lib()
+    n, ctot = out.shape
+    _lib.check(L.jf_quantize_heads_bf16(t.data_ptr(), b, s, h, d, sb, ss, sh, out.values.data_ptr() + col0,
+                                        ctot, out.scales.data_ptr() + 4 * (col0 // 32), ctot // 32,
+                                        _rt.err_ptr(), _lib.stream_handle()), "quantize_heads")
+    _rt.maybe_check()
+
 
 @dataclass
 class _SavedForward:
@@ -262,8 +320,11 @@ class TransformerBlock:
         a1, stats1 = add_forward(xq, None, width, counters)           # Add(x, zeros_like(x))
         ln1_out, ctx1 = layernorm_forward(a1, stats1, self.ln1, counters)
         qkv_q = self.qkv.forward(ln1_out, counters, threads)
-        attn = self.attn.forward(dequantize(qkv_q, self.attn.dtype), batch, seq)
-        attn_q = quantize_per_block(attn, cfg.block)
+        if self.attn.supports_q():
+            attn_q = self.attn.forward_q(qkv_q, batch, seq)
+        else:
+            attn = self.attn.forward(dequantize(qkv_q, self.attn.dtype), batch, seq)
+            attn_q = quantize_per_block(attn, cfg.block)
         proj_q = self.proj.forward(attn_q, counters, threads)
         drop1 = DropoutState.generate(p, (dropout_seed, 1), proj_q.shape)
         branch1 = dropout_forward(proj_q, drop1, counters)
@@ -298,8 +359,11 @@ class TransformerBlock:
 
         dproj = dropout_backward(dh, s.drop1, counters)
         dattn_q, dw_proj, db_proj = self.proj.backward(dproj, counters, threads)
-        dqkv = self.attn.backward(dequantize(dattn_q, self.attn.dtype), s.batch, s.seq)
-        dqkv_q = quantize_per_block(dqkv, self.config.block)
+        if self.attn.supports_q():
+            dqkv_q = self.attn.backward_q(dattn_q, s.batch, s.seq)
+        else:
+            dqkv = self.attn.backward(dequantize(dattn_q, self.attn.dtype), s.batch, s.seq)
+            dqkv_q = quantize_per_block(dqkv, self.config.block)
         dln1, dw_qkv, db_qkv = self.qkv.backward(dqkv_q, counters, threads)
         da1_branch, dgamma1, dbeta1 = layernorm_backward(s.ctx1, dln1, self.ln1, counters)
         dx, _ = add_forward(da1_branch, dh, width, counters)

@@ -444,3 +444,39 @@ def test_block_counters_closed_form(jf):
     n, c, h = batch * seq, 64, 128
     assert ctr.int_mac == 3 * n * (3 * c * c + c * c + h * c + c * h)
     assert ctr.fp16_load_store == 0
+
+
+def test_attention_boundary_kernels(jf):
+    """jf_dequantize_qkv_heads / jf_quantize_heads_bf16 == dequantize + view / quantize_per_block."""
+    from paper_2403_12422_b200 import qlayers
+
+    rng = np.random.default_rng(11)
+    b, s, h, d = 2, 64, 4, 32
+    c = h * d
+    QKV = bqt(jf, *_rand_q(rng, (b * s, 3 * c)))
+    core = jf.AttentionCore(h, d, dtype=torch.bfloat16)
+    out = core.forward_q(QKV, b, s)
+    q, k, v, o = core._saved
+    dense = jf.dequantize(QKV, torch.bfloat16)
+    for i, t in enumerate((q, k, v)):
+        want = dense[:, i * c:(i + 1) * c].reshape(b, s, h, d).transpose(1, 2)
+        assert torch.equal(t.detach(), want)
+    ref = jf.quantize_per_block(o.detach().transpose(1, 2).reshape(b * s, c).float())
+    assert torch.equal(out.values, ref.values) and torch.equal(out.scales, ref.scales)
+    # slice writes: three strided sources into one [N, 3C] tensor
+    dq = jf.BlockQuantTensor(torch.zeros(b * s, 3 * c, dtype=torch.int8, device="cuda"),
+                             torch.ones(b * s // 32, 3 * c // 32, device="cuda"))
+    srcs = [torch.randn(b, h, s, d, device="cuda").to(torch.bfloat16) for _ in range(3)]
+    for i, t in enumerate(srcs):
+        qlayers._quantize_heads(t, dq, i * c)
+    full = torch.cat([t.transpose(1, 2).reshape(b * s, c) for t in srcs], dim=1).float()
+    ref = jf.quantize_per_block(full)
+    assert torch.equal(dq.values, ref.values) and torch.equal(dq.scales, ref.scales)
+    # backward path runs and matches the dense island within bf16 attention noise
+    dattn = jf.quantize_per_block(0.1 * torch.randn(b * s, c, device="cuda"))
+    dqkv = core.backward_q(dattn, b, s)
+    core2 = jf.AttentionCore(h, d, dtype=torch.bfloat16)
+    core2.forward(dense, b, s)
+    g = core2.backward(jf.dequantize(dattn, torch.bfloat16), b, s).float()
+    got = dqkv.dequantize()
+    assert (got - g).abs().max() <= 0.05 * g.abs().max()
