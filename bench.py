@@ -42,6 +42,10 @@ WORKLOADS = {
     "block_h4096_s2048": dict(c=4096, heads=32, hidden=16384, seq=2048, batch=2),
     # BASELINE.json configs[1]
     "block_h1024_s1024": dict(c=1024, heads=16, hidden=4096, seq=1024, batch=8),
+    # BASELINE.json configs[2]: GPT-2 medium full pretraining step (24 layers, hidden 1024)
+    "gpt2_medium": dict(model="gpt2_medium", c=1024, heads=16, hidden=4096, seq=1024, batch=8),
+    # BASELINE.json configs[4] model (data-parallel at 2/4/8 GPUs): GPT-2 large
+    "gpt2_large": dict(model="gpt2_large", c=1280, heads=20, hidden=5120, seq=1024, batch=8),
 }
 
 
@@ -183,6 +187,100 @@ def allreduce_grads(grads: dict, world: int):
     allreduce_mean(grads)
 
 
+class BlockWorkload:
+    """One TransformerBlock fwd+bwd (+ DP all-reduce of its FP32 grads) per step."""
+
+    def __init__(self, jf, w, args, world, rank):
+        self.jf, self.w, self.world = jf, w, world
+        self.b, self.s, self.c = w["batch"], w["seq"], w["c"]
+        self.n = self.b * self.s
+        attn_dtype = torch.bfloat16 if args.attn_dtype == "bf16" else torch.float32
+        self.blk = build_block(jf, w, attn_dtype, seed=0)
+        g = torch.Generator(device="cuda").manual_seed(1000 + rank)
+        self.x = torch.randn((self.n, self.c), generator=g, device="cuda")
+        self.dy = 0.1 * torch.randn((self.n, self.c), generator=g, device="cuda")
+        self.xq = jf.quantize_per_block(self.x)
+        self.dyq = jf.quantize_per_block(self.dy)
+
+    def step(self):
+        self.blk.forward(self.xq, self.b, self.s)
+        dx, grads = self.blk.backward(self.dyq)
+        allreduce_grads(grads, self.world)
+
+    def e2e_setup(self):
+        n, c = self.n, self.c
+        self.hx, self.hdy = self.x.cpu().pin_memory(), self.dy.cpu().pin_memory()
+        self.hq = torch.empty((n, c), dtype=torch.int8).pin_memory()
+        self.hs = torch.empty((n // 32, c // 32), dtype=torch.float32).pin_memory()
+        return int(2 * n * c * 4), int(n * c + (n * c // 1024) * 4)
+
+    def e2e_step(self):
+        """Host pinned FP32 x, dY in; dX codes + scales out (the public API end to end)."""
+        jf, n, c = self.jf, self.n, self.c
+        dx_ = torch.empty((n, c), device="cuda")
+        dd_ = torch.empty((n, c), device="cuda")
+        dx_.copy_(self.hx, non_blocking=True)
+        dd_.copy_(self.hdy, non_blocking=True)
+        self.blk.forward(jf.quantize_per_block(dx_), self.b, self.s)
+        gx, grads = self.blk.backward(jf.quantize_per_block(dd_))
+        allreduce_grads(grads, self.world)
+        self.hq.copy_(gx.values, non_blocking=True)
+        self.hs.copy_(gx.scales, non_blocking=True)
+
+    def config(self):
+        w = self.w
+        return {"hidden": self.c, "heads": w["heads"], "mlp_hidden": w["hidden"], "seq_len": self.s,
+                "batch_per_gpu": self.b, "tokens_per_gpu": self.n,
+                "l2": "working set (201 MB INT8 weights + activations) larger than the 126 MB L2"}
+
+
+class ModelWorkload:
+    """GPT-2-style pretraining step: embedding, INT8 blocks, BF16 head + FP32 loss,
+    backward, DP all-reduce, fused AdamW (paper_2403_12422_b200.model)."""
+
+    def __init__(self, jf, w, args, world, rank):
+        from paper_2403_12422_b200.model import AdamW, JetfireLM, ModelConfig
+
+        self.world = world
+        self.name = w["model"]
+        self.cfg = getattr(ModelConfig, w["model"])()
+        self.b, self.s = w["batch"], w["seq"]
+        self.n = self.b * self.s
+        self.model = JetfireLM(self.cfg, seed=0)
+        self.opt = AdamW(self.model, lr=1e-4, weight_decay=0.1)
+        g = torch.Generator(device="cuda").manual_seed(1000 + rank)
+        self.x = torch.randint(0, self.cfg.vocab, (self.b, self.s), generator=g, device="cuda")
+        self.y = torch.roll(self.x, -1, dims=1)
+
+    def step(self, x=None, y=None):
+        loss, grads = self.model.loss_and_grads(self.x if x is None else x, self.y if y is None else y)
+        allreduce_grads(grads, self.world)
+        self.opt.step(grads)
+        return loss
+
+    def e2e_setup(self):
+        self.hx, self.hy = self.x.cpu().pin_memory(), self.y.cpu().pin_memory()
+        self.hloss = torch.empty((), dtype=torch.float32).pin_memory()
+        return int(2 * self.n * 8), 4
+
+    def e2e_step(self):
+        """Host pinned token ids in, loss out."""
+        x = torch.empty_like(self.x)
+        y = torch.empty_like(self.y)
+        x.copy_(self.hx, non_blocking=True)
+        y.copy_(self.hy, non_blocking=True)
+        loss = self.step(x, y)
+        self.hloss.copy_(loss, non_blocking=True)
+
+    def config(self):
+        c = self.cfg
+        return {"model": self.name, "layers": c.layers, "hidden": c.c_model,
+                "heads": c.heads, "mlp_hidden": c.hidden, "vocab": c.vocab, "seq_len": self.s,
+                "batch_per_gpu": self.b, "tokens_per_gpu": self.n, "head": c.head_dtype + " head, fp32 loss",
+                "optimizer": "AdamW (torch fused), INT8 weights re-derived each step",
+                "l2": "working set (GBs of weights, grads, Adam state) larger than the 126 MB L2"}
+
+
 def run_ours(args, world, rank, local):
     import paper_2403_12422_b200 as jf
     from paper_2403_12422_b200 import _lib
@@ -194,25 +292,12 @@ def run_ours(args, world, rank, local):
     w = dict(WORKLOADS[args.workload])
     if args.batch:
         w["batch"] = args.batch
-    b, s, c = w["batch"], w["seq"], w["c"]
-    n = b * s
-    attn_dtype = torch.bfloat16 if args.attn_dtype == "bf16" else torch.float32
-    blk = build_block(jf, w, attn_dtype, seed=0)
-    g = torch.Generator(device="cuda").manual_seed(1000 + rank)
-    x = torch.randn((n, c), generator=g, device="cuda")
-    dy = 0.1 * torch.randn((n, c), generator=g, device="cuda")
-    xq = jf.quantize_per_block(x)
-    dyq = jf.quantize_per_block(dy)
+    wl = (ModelWorkload if "model" in w else BlockWorkload)(jf, w, args, world, rank)
+    n = wl.n
     stream = torch.cuda.current_stream()
 
-    def step():
-        blk.forward(xq, b, s)
-        dx, grads = blk.backward(dyq)
-        allreduce_grads(grads, world)
-        return dx
-
     for _ in range(args.warmup):
-        step()
+        wl.step()
     jf.check_errors()
     torch.cuda.synchronize()
     barrier(world)
@@ -225,7 +310,7 @@ def run_ours(args, world, rank, local):
         barrier(world)
         start.record(stream)
         for _ in range(args.steps):
-            step()
+            wl.step()
         end.record(stream)
         torch.cuda.synchronize()
         barrier(world)
@@ -238,33 +323,16 @@ def run_ours(args, world, rank, local):
     gemm_ms_step = gsum["ms"] / args.steps
     gemm_tops = gsum["ops"] / (gsum["ms"] / 1e3) / 1e12
 
-    # ── e2e: host pinned FP32 in, dX codes + scales out, every step ──
-    hx = x.cpu().pin_memory()
-    hdy = dy.cpu().pin_memory()
-    hq = torch.empty((n, c), dtype=torch.int8).pin_memory()
-    hs = torch.empty((n // 32, c // 32), dtype=torch.float32).pin_memory()
-
-    def e2e_step():
-        dx_ = torch.empty((n, c), device="cuda")
-        dd_ = torch.empty((n, c), device="cuda")
-        dx_.copy_(hx, non_blocking=True)
-        dd_.copy_(hdy, non_blocking=True)
-        xq_ = jf.quantize_per_block(dx_)
-        dq_ = jf.quantize_per_block(dd_)
-        blk.forward(xq_, b, s)
-        gx, grads = blk.backward(dq_)
-        allreduce_grads(grads, world)
-        hq.copy_(gx.values, non_blocking=True)
-        hs.copy_(gx.scales, non_blocking=True)
-
+    # ── e2e: host inputs copied in, results read back, every step ──
+    h2d, d2h = wl.e2e_setup()
     for _ in range(2):
-        e2e_step()
+        wl.e2e_step()
     torch.cuda.synchronize()
     barrier(world)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
-        e2e_step()
+        wl.e2e_step()
     e1.record(stream)
     torch.cuda.synchronize()
     barrier(world)
@@ -272,18 +340,20 @@ def run_ours(args, world, rank, local):
     e2e_ms = max_over_ranks(e0.elapsed_time(e1), world)
     e2e_val = world * n * args.steps / (e2e_ms / 1e3)
 
+    cfg = {"workload": args.workload}
+    cfg.update(wl.config())
+    cfg.update({"global_tokens": world * n, "block": 32, "promotion": args.promotion,
+                "attention": f"torch SDPA ({args.attn_dtype})",
+                "parallelism": f"dp{world}" if world > 1 else "single"})
     out = {
         "metric": METRIC, "value": round(tokens_per_s, 1), "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8",
-        "data": "synthetic (standard-normal activations, 0.1*normal upstream grads, random-init weights)",
-        "config": {"workload": args.workload, "hidden": c, "heads": w["heads"], "mlp_hidden": w["hidden"],
-                   "seq_len": s, "batch_per_gpu": b, "tokens_per_gpu": n, "global_tokens": world * n,
-                   "block": 32, "promotion": args.promotion, "attention": f"torch SDPA ({args.attn_dtype})",
-                   "parallelism": f"dp{world}" if world > 1 else "single",
-                   "l2": "working set (201 MB INT8 weights + activations) larger than the 126 MB L2"},
-        "e2e": {"value": round(e2e_val, 1), "unit": "tokens/s",
-                "h2d_bytes_per_step": int(2 * n * c * 4), "d2h_bytes_per_step": int(n * c + (n * c // 1024) * 4)},
+        "data": "synthetic (random-init weights; standard-normal activations / 0.1*normal grads, "
+                "or uniform random token ids for model workloads)",
+        "config": cfg,
+        "e2e": {"value": round(e2e_val, 1), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
         "gpu_launches": int(launches),
         "gemm": {"launches_per_step": gsum["launches"] // args.steps, "ms_per_step": round(gemm_ms_step, 4),
                  "tops": round(gemm_tops, 1), "frac_of_int8_peak": round(gemm_tops / INT8_PEAK_TOPS, 4),
@@ -291,7 +361,7 @@ def run_ours(args, world, rank, local):
     }
     out["clocks"] = clocks.summary()
     out["roofline"] = roofline(gemm_tops, args.promotion, clocks_mhz=out["clocks"].get("sm_mhz"))
-    return out, blk, (xq, dyq), w
+    return out, wl, None, w
 
 
 def roofline(gemm_tops: float, promotion: str, clocks_mhz=None) -> dict:
@@ -431,16 +501,16 @@ def main():
         if out is not None:
             print(json.dumps(out), flush=True)
         return
-    out, blk, _, w = run_ours(args, world, rank, local)
+    out, wl, _, w = run_ours(args, world, rank, local)
     if rank == 0:
-        if not args.no_bf16:
+        if not args.no_bf16 and "model" not in w:
             wb = dict(w)
             tps, ms = bf16_block_tokens_per_s(wb, args.steps, args.warmup)
             out["bf16_baseline"] = {"value": round(tps * world, 1), "unit": "tokens/s", "ms_per_step": round(ms, 4),
                                     "what": "same block wiring in torch BF16 (cuBLAS linear, F.layer_norm, "
                                             "exact-erf GELU, SDPA), fwd+bwd autograd, 1 GPU",
                                     "int8_over_bf16": round(out["value"] / (tps * world), 3)}
-        if world == 1 and not args.no_cpu:
+        if world == 1 and not args.no_cpu and "model" not in w:
             out["cpu_baseline"] = cpu_block_sample(w, args.cpu_tokens)
         print(json.dumps(out), flush=True)
     if world > 1:

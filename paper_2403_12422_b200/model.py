@@ -1,0 +1,183 @@
+"""A GPT-2-style language model on the INT8 data flow: embedding, a stack of
+TransformerBlocks, an FP head with cross-entropy, and AdamW — the reference's
+``ToyModel`` + ``AdamW`` (``trainer.py:225-262, 273-427``) on the GPU, and the
+GPT-2 medium pretraining step of BASELINE config 3.
+
+Data flow per step (as the reference):
+  h0 = emb[tokens] * gain (+ wpe[pos] for GPT-2)       FP32, quantized once
+  h  = blocks(h0)                                       INT8 between all operators
+  logits = deq(h) @ head_w^T + head_b                   FP32 (reference) or BF16 head
+  loss = masked mean of -log_softmax(logits)[y]         FP32
+  dh = dlogits @ head_w -> quantize -> blocks backward -> deq -> scatter-add into emb
+Parameters, gradients and AdamW moments are FP32; the INT8 weight copies are
+re-derived lazily after ``step()`` (``QuantLinear.mark_updated``, qlayers.py:139-147).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from .qlayers import BlockConfig, TransformerBlock
+from .qtensor import quantize_per_block
+
+
+@dataclass(frozen=True)
+class ModelConfig:
+    layers: int = 24
+    c_model: int = 1024
+    heads: int = 16
+    hidden: int = 4096
+    vocab: int = 50257
+    max_seq: int = 1024
+    pos_emb: bool = False         # GPT-2 adds learned positions; the reference ToyModel does not
+    head_dtype: str = "fp32"      # "fp32" = reference head; "bf16" = cuBLAS BF16 head, FP32 loss
+    attn_dtype: str = "bf16"
+
+    @staticmethod
+    def gpt2_medium() -> "ModelConfig":
+        return ModelConfig(layers=24, c_model=1024, heads=16, hidden=4096, vocab=50257, max_seq=1024,
+                           pos_emb=True, head_dtype="bf16")
+
+    @staticmethod
+    def gpt2_large() -> "ModelConfig":
+        return ModelConfig(layers=36, c_model=1280, heads=20, hidden=5120, vocab=50257, max_seq=1024,
+                           pos_emb=True, head_dtype="bf16")
+
+
+class JetfireLM:
+    """Embedding -> INT8 TransformerBlocks -> FP head, with hand-driven backward (trainer.py:373-427)."""
+
+    def __init__(self, cfg: ModelConfig, params: dict | None = None, seed: int = 0, device="cuda"):
+        self.cfg = cfg
+        c = cfg.c_model
+        dt = torch.bfloat16 if cfg.attn_dtype == "bf16" else torch.float32
+        bcfg = BlockConfig(c_model=c, heads=cfg.heads, hidden=cfg.hidden, block=32, dropout_p=0.0)
+        if params is None:
+            params = self._init(cfg, seed, device)
+        self.params = {k: (v if isinstance(v, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(v)))
+                       .to(device=device, dtype=torch.float32).contiguous() for k, v in params.items()}
+        self.blocks = []
+        for i in range(cfg.layers):
+            sub = {k[len(f"block{i}."):]: v for k, v in self.params.items() if k.startswith(f"block{i}.")}
+            blk = TransformerBlock.from_parameters(bcfg, sub, attn_dtype=dt)
+            # share storage: the block's masters ARE the model's parameters
+            for name, lin in (("qkv", blk.qkv), ("proj", blk.proj), ("mlp1", blk.mlp1), ("mlp2", blk.mlp2)):
+                lin.master_weight = self.params[f"block{i}.{name}.w"]
+                lin.bias = self.params[f"block{i}.{name}.b"]
+            blk.ln1.gamma, blk.ln1.beta = self.params[f"block{i}.ln1.gamma"], self.params[f"block{i}.ln1.beta"]
+            blk.ln2.gamma, blk.ln2.beta = self.params[f"block{i}.ln2.gamma"], self.params[f"block{i}.ln2.beta"]
+            self.blocks.append(blk)
+        self.gain = self.params.pop("gain", None)
+        self.decay_keys = {k for k in self.params if k.endswith(".w") and k != "emb"}
+
+    @staticmethod
+    def _init(cfg: ModelConfig, seed: int, device) -> dict:
+        g = torch.Generator(device=device).manual_seed(seed)
+        c, h = cfg.c_model, cfg.hidden
+
+        def rn(*shape, scale):
+            return torch.randn(shape, generator=g, device=device) * scale
+
+        p = {"emb": rn(cfg.vocab, c, scale=c ** -0.5), "head.w": rn(cfg.vocab, c, scale=0.1 * c ** -0.5),
+             "head.b": torch.zeros(cfg.vocab, device=device)}
+        if cfg.pos_emb:
+            p["wpe"] = rn(cfg.max_seq, c, scale=0.01)
+        for i in range(cfg.layers):
+            for name, (d, cc) in {"qkv": (3 * c, c), "proj": (c, c), "mlp1": (h, c), "mlp2": (c, h)}.items():
+                p[f"block{i}.{name}.w"] = rn(d, cc, scale=cc ** -0.5)
+                p[f"block{i}.{name}.b"] = torch.zeros(d, device=device)
+            for ln in ("ln1", "ln2"):
+                p[f"block{i}.{ln}.gamma"] = torch.ones(c, device=device)
+                p[f"block{i}.{ln}.beta"] = torch.zeros(c, device=device)
+        return p
+
+    def mark_updated(self) -> None:
+        for blk in self.blocks:
+            blk.mark_updated()
+
+    def _head(self, h: torch.Tensor) -> torch.Tensor:
+        w, b = self.params["head.w"], self.params["head.b"]
+        if self.cfg.head_dtype == "bf16":
+            return torch.addmm(b.to(torch.bfloat16), h.to(torch.bfloat16), w.to(torch.bfloat16).t()).float()
+        return torch.addmm(b, h, w.t())
+
+    def loss_and_grads(self, x: torch.Tensor, y: torch.Tensor, mask: torch.Tensor | None = None):
+        """(loss, grads) for token ids x, targets y [batch, seq] (trainer.py:373-427)."""
+        batch, seq = x.shape
+        flat = x.reshape(-1)
+        h0 = self.params["emb"][flat]
+        if self.gain is not None:
+            h0 = h0 * self.gain
+        if "wpe" in self.params:
+            h0 = h0 + self.params["wpe"][:seq].repeat(batch, 1)
+        hq = quantize_per_block(h0.contiguous())
+        for blk in self.blocks:
+            hq = blk.forward(hq, batch, seq)
+        h = hq.dequantize()
+
+        logits = self._head(h)
+        logp = torch.log_softmax(logits, dim=1)
+        fm = torch.ones(batch * seq, device=h.device) if mask is None else mask.reshape(-1).float()
+        n_live = fm.sum()
+        rows = torch.arange(logits.shape[0], device=h.device)
+        fy = y.reshape(-1)
+        loss = -(logp[rows, fy] * fm).sum() / n_live
+
+        dlogits = logp.exp_()
+        dlogits[rows, fy] -= 1.0
+        dlogits *= (fm / n_live)[:, None]
+        grads = {}
+        if self.cfg.head_dtype == "bf16":
+            dl16 = dlogits.to(torch.bfloat16)
+            grads["head.w"] = (dl16.t() @ h.to(torch.bfloat16)).float()
+            dh = (dl16 @ self.params["head.w"].to(torch.bfloat16)).float()
+        else:
+            grads["head.w"] = dlogits.t() @ h
+            dh = dlogits @ self.params["head.w"]
+        grads["head.b"] = dlogits.sum(dim=0)
+
+        dq = quantize_per_block(dh.contiguous())
+        for i in reversed(range(len(self.blocks))):
+            dq, bg = self.blocks[i].backward(dq)
+            for k, g in bg.items():
+                grads[f"block{i}.{k}"] = g
+        dx = dq.dequantize()
+        if self.gain is not None:
+            dx = dx * self.gain
+        demb = torch.zeros_like(self.params["emb"])
+        demb.index_add_(0, flat, dx)
+        grads["emb"] = demb
+        if "wpe" in self.params:
+            dpos = torch.zeros_like(self.params["wpe"])
+            dpos[:seq] = dx.view(batch, seq, -1).sum(dim=0)
+            grads["wpe"] = dpos
+        return loss, grads
+
+
+class AdamW:
+    """Adam with decoupled weight decay and bias correction, FP32 state (trainer.py:225-262),
+    as torch's fused multi-tensor CUDA kernel; the INT8 weight copies are re-derived lazily."""
+
+    def __init__(self, model: JetfireLM, lr: float, weight_decay: float = 0.0, betas=(0.9, 0.999),
+                 eps: float = 1e-8):
+        self.model = model
+        keys = sorted(model.params)
+        decay = [model.params[k] for k in keys if k in model.decay_keys]
+        rest = [model.params[k] for k in keys if k not in model.decay_keys]
+        self.keys = [k for k in keys if k in model.decay_keys] + [k for k in keys if k not in model.decay_keys]
+        groups = [{"params": decay, "weight_decay": weight_decay}, {"params": rest, "weight_decay": 0.0}]
+        self.opt = torch.optim.AdamW(groups, lr=lr, betas=betas, eps=eps, fused=True)
+
+    def step(self, grads: dict) -> None:
+        for k in self.keys:
+            self.model.params[k].grad = grads[k]
+        self.opt.step()
+        for k in self.keys:
+            self.model.params[k].grad = None
+        self.model.mark_updated()
+
+
+__all__ = ["AdamW", "JetfireLM", "ModelConfig"]

@@ -214,12 +214,42 @@ def layer_cases(qt, ql, qn):
     return out
 
 
+def model_cases():
+    """ToyModel.loss_and_grads (trainer.py:373-427) of the REAL reference: loss + every grad."""
+    from int8flow import trainer
+
+    cfg = trainer.TrainConfig(layers=2, c_model=64, heads=4, mlp_ratio=4, seed=3, batch_size=2,
+                              weight_decay=0.1, lr=1e-3)
+    vocab, seq = 96, 32
+    model = trainer.ToyModel(cfg, vocab)
+    rng = np.random.default_rng(77)
+    x = rng.integers(0, vocab, size=(cfg.batch_size, seq))
+    y = rng.integers(0, vocab, size=(cfg.batch_size, seq))
+    mask = np.ones((cfg.batch_size, seq), dtype=np.float32)
+    mask[1, -5:] = 0.0
+    loss, grads = model.loss_and_grads(x, y, mask, dropout_seed=0)
+    out = {"cfg": np.array([cfg.layers, cfg.c_model, cfg.heads, cfg.hidden, vocab, seq, cfg.batch_size]),
+           "x": x, "y": y, "mask": mask, "loss": np.float64(loss)}
+    for k, v in model.params.items():
+        out["p_" + k] = v.copy()  # AdamW.step below updates the arrays in place
+    for k, v in grads.items():
+        out["g_" + k] = v
+    # one AdamW step (trainer.py:247-262) on those grads
+    opt = trainer.AdamW(model.params, lr=cfg.lr, weight_decay=cfg.weight_decay, decay_keys=model.decay_keys)
+    opt.step(grads)
+    for k, v in model.params.items():
+        out["p1_" + k] = v.copy()
+    out["decay_keys"] = np.array(sorted(model.decay_keys))
+    return out
+
+
 def main():
     qt, qg, qn, ql = _load_reference()
     np.savez_compressed(os.path.join(HERE, "quant.npz"), **quant_cases(qt))
     np.savez_compressed(os.path.join(HERE, "gemm.npz"), **gemm_cases(qt, qg))
     np.savez_compressed(os.path.join(HERE, "nonlinear.npz"), **nonlinear_cases(qt, qn))
     np.savez_compressed(os.path.join(HERE, "layers.npz"), **layer_cases(qt, ql, qn))
+    np.savez_compressed(os.path.join(HERE, "model.npz"), **model_cases())
     meta = {"numpy": np.__version__}
     import scipy
     meta["scipy"] = scipy.__version__
