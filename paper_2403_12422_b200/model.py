@@ -98,11 +98,19 @@ class JetfireLM:
         for blk in self.blocks:
             blk.mark_updated()
 
-    def _head(self, h: torch.Tensor) -> torch.Tensor:
+    def _head_bf16(self):
+        """BF16 head operands with the vocabulary padded to a multiple of 128 (50257 -> 50304):
+        cuBLAS only picks its fast tcgen05 kernels for aligned leading dimensions (an odd
+        vocab fell back to sm75 align1 kernels, 5-7 ms each).  Padded rows are zero and
+        padded biases -inf, so they carry exactly zero probability and gradient."""
         w, b = self.params["head.w"], self.params["head.b"]
-        if self.cfg.head_dtype == "bf16":
-            return torch.addmm(b.to(torch.bfloat16), h.to(torch.bfloat16), w.to(torch.bfloat16).t()).float()
-        return torch.addmm(b, h, w.t())
+        v, c = w.shape
+        vp = (v + 127) // 128 * 128
+        w16 = torch.zeros((vp, c), dtype=torch.bfloat16, device=w.device)
+        w16[:v] = w
+        b16 = torch.full((vp,), float("-inf"), dtype=torch.bfloat16, device=w.device)
+        b16[:v] = b
+        return w16, b16
 
     def loss_and_grads(self, x: torch.Tensor, y: torch.Tensor, mask: torch.Tensor | None = None):
         """(loss, grads) for token ids x, targets y [batch, seq] (trainer.py:373-427)."""
@@ -118,7 +126,12 @@ class JetfireLM:
             hq = blk.forward(hq, batch, seq)
         h = hq.dequantize()
 
-        logits = self._head(h)
+        if self.cfg.head_dtype == "bf16":
+            w16, b16 = self._head_bf16()
+            h16 = h.to(torch.bfloat16)
+            logits = torch.addmm(b16, h16, w16.t()).float()
+        else:
+            logits = torch.addmm(self.params["head.b"], h, self.params["head.w"].t())
         logp = torch.log_softmax(logits, dim=1)
         fm = torch.ones(batch * seq, device=h.device) if mask is None else mask.reshape(-1).float()
         n_live = fm.sum()
@@ -130,14 +143,16 @@ class JetfireLM:
         dlogits[rows, fy] -= 1.0
         dlogits *= (fm / n_live)[:, None]
         grads = {}
+        v = self.cfg.vocab
         if self.cfg.head_dtype == "bf16":
             dl16 = dlogits.to(torch.bfloat16)
-            grads["head.w"] = (dl16.t() @ h.to(torch.bfloat16)).float()
-            dh = (dl16 @ self.params["head.w"].to(torch.bfloat16)).float()
+            grads["head.w"] = (dl16.t() @ h16)[:v].float()
+            dh = (dl16 @ w16).float()
+            grads["head.b"] = dlogits[:, :v].sum(dim=0)
         else:
             grads["head.w"] = dlogits.t() @ h
             dh = dlogits @ self.params["head.w"]
-        grads["head.b"] = dlogits.sum(dim=0)
+            grads["head.b"] = dlogits.sum(dim=0)
 
         dq = quantize_per_block(dh.contiguous())
         for i in reversed(range(len(self.blocks))):
