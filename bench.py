@@ -365,7 +365,7 @@ def run_ours(args, world, rank, local):
 
 
 def roofline(gemm_tops: float, promotion: str, clocks_mhz=None) -> dict:
-    """Dominant kernel = gemm_i8_kernel (88% of the step).
+    """Dominant kernel = gemm_i8s_kernel (87% of the step).
 
     peak: B200 dense INT8 (datasheet 4.5 POPS; our raw kind::i8 microbenchmark
     measures 8178 MAC/clk/SM = 4.76 POPS at 1965 MHz).  The binding bound under
@@ -388,7 +388,7 @@ def roofline(gemm_tops: float, promotion: str, clocks_mhz=None) -> dict:
         traffic, tr_src = t["dram_bytes_per_launch"], t["launch"] + " (" + t["source"] + ")"
     except (OSError, KeyError, ValueError):
         pass
-    return {"kernel": "gemm_i8_kernel (tcgen05 kind::i8)", "bound": "tensor", "achieved": round(gemm_tops, 1),
+    return {"kernel": "gemm_i8s_kernel (tcgen05 kind::i8)", "bound": "tensor", "achieved": round(gemm_tops, 1),
             "peak": INT8_PEAK_TOPS, "unit": "TFLOP/s", "frac": round(gemm_tops / INT8_PEAK_TOPS, 4),
             "traffic": traffic, "traffic_launch": tr_src,
             "peak_source": "B200 dense INT8 datasheet 4.5 POPS (int ops counted as FLOP); "
