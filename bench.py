@@ -253,8 +253,16 @@ class ModelWorkload:
         self.y = torch.roll(self.x, -1, dims=1)
 
     def step(self, x=None, y=None):
-        loss, grads = self.model.loss_and_grads(self.x if x is None else x, self.y if y is None else y)
-        allreduce_grads(grads, self.world)
+        x = self.x if x is None else x
+        y = self.y if y is None else y
+        if self.world > 1:  # DP: per-block all-reduce overlapped with the rest of backward
+            from paper_2403_12422_b200.dist import OverlappedAllReduce
+
+            ov = OverlappedAllReduce()
+            loss, grads = self.model.loss_and_grads(x, y, grad_hook=ov.hook)
+            ov.finish(grads)
+        else:
+            loss, grads = self.model.loss_and_grads(x, y)
         self.opt.step(grads)
         return loss
 

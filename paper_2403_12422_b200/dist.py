@@ -80,4 +80,32 @@ def _unpack(pending, grads, world):
             off += n
 
 
-__all__ = ["allreduce_mean", "finish_allreduce", "shard_sequences"]
+class OverlappedAllReduce:
+    """All-reduce gradients group by group while backward continues.
+
+    Pass ``hook`` as ``JetfireLM.loss_and_grads(..., grad_hook=...)``: each call packs
+    the named FP32 gradients into one flat buffer and launches an async all-reduce (NCCL
+    runs on its own stream, so the transfer overlaps the next block's backward kernels);
+    ``finish(grads)`` waits, averages and unpacks.  Same sums as ``allreduce_mean``.
+    """
+
+    def __init__(self, group=None):
+        self.group = group
+        self.pending = []
+
+    def hook(self, grads: dict, names) -> None:
+        names = [k for k in names if grads.get(k) is not None]
+        if not names:
+            return
+        flat = torch.cat([grads[k].reshape(-1) for k in names])
+        work = dist.all_reduce(flat, group=self.group, async_op=True)
+        self.pending.append((work, names, flat))
+
+    def finish(self, grads: dict) -> None:
+        for work, _, _ in self.pending:
+            work.wait()
+        _unpack(self.pending, grads, dist.get_world_size(self.group))
+        self.pending = []
+
+
+__all__ = ["OverlappedAllReduce", "allreduce_mean", "finish_allreduce", "shard_sequences"]

@@ -112,8 +112,14 @@ class JetfireLM:
         b16[:v] = b
         return w16, b16
 
-    def loss_and_grads(self, x: torch.Tensor, y: torch.Tensor, mask: torch.Tensor | None = None):
-        """(loss, grads) for token ids x, targets y [batch, seq] (trainer.py:373-427)."""
+    def loss_and_grads(self, x: torch.Tensor, y: torch.Tensor, mask: torch.Tensor | None = None,
+                       grad_hook=None):
+        """(loss, grads) for token ids x, targets y [batch, seq] (trainer.py:373-427).
+
+        ``grad_hook(names)`` (optional) is called as soon as the listed FP32 gradients are
+        final — the head's, then each block's in backward order, then the embeddings' — so a
+        data-parallel caller can start their all-reduce while earlier blocks still run
+        backward (``dist.OverlappedAllReduce``)."""
         batch, seq = x.shape
         flat = x.reshape(-1)
         h0 = self.params["emb"][flat]
@@ -154,11 +160,15 @@ class JetfireLM:
             dh = dlogits @ self.params["head.w"]
             grads["head.b"] = dlogits.sum(dim=0)
 
+        if grad_hook is not None:
+            grad_hook(grads, ["head.w", "head.b"])
         dq = quantize_per_block(dh.contiguous())
         for i in reversed(range(len(self.blocks))):
             dq, bg = self.blocks[i].backward(dq)
             for k, g in bg.items():
                 grads[f"block{i}.{k}"] = g
+            if grad_hook is not None:
+                grad_hook(grads, [f"block{i}.{k}" for k in bg if bg[k] is not None])
         dx = dq.dequantize()
         if self.gain is not None:
             dx = dx * self.gain
@@ -169,6 +179,8 @@ class JetfireLM:
             dpos = torch.zeros_like(self.params["wpe"])
             dpos[:seq] = dx.view(batch, seq, -1).sum(dim=0)
             grads["wpe"] = dpos
+        if grad_hook is not None:
+            grad_hook(grads, [k for k in ("emb", "wpe") if k in grads])
         return loss, grads
 
 

@@ -243,6 +243,18 @@ def model_cases():
     return out
 
 
+def format_cases(qt, ql):
+    """int8flow-checkpoint-v1 files and a JQT1 blob written by the REAL reference."""
+    rng = np.random.default_rng(9)
+    params = {"b.w": rng.standard_normal((3, 5)).astype(np.float32), "a": rng.standard_normal(4).astype(np.float32),
+              "scalar": np.array(1.5, dtype=np.float32)}
+    ql.save_params(os.path.join(HERE, "ckpt_ref"), params, {"step": 7, "opt_t": 7, "scheme": "per-block"})
+    x = (rng.standard_normal((32, 64)) * 3).astype(np.float32)
+    with open(os.path.join(HERE, "jqt1_ref.bin"), "wb") as fh:
+        fh.write(qt.quantize_per_block(x, 32).to_bytes())
+    np.save(os.path.join(HERE, "jqt1_ref_input.npy"), x)
+
+
 def main():
     qt, qg, qn, ql = _load_reference()
     np.savez_compressed(os.path.join(HERE, "quant.npz"), **quant_cases(qt))
@@ -250,6 +262,7 @@ def main():
     np.savez_compressed(os.path.join(HERE, "nonlinear.npz"), **nonlinear_cases(qt, qn))
     np.savez_compressed(os.path.join(HERE, "layers.npz"), **layer_cases(qt, ql, qn))
     np.savez_compressed(os.path.join(HERE, "model.npz"), **model_cases())
+    format_cases(qt, ql)
     meta = {"numpy": np.__version__}
     import scipy
     meta["scipy"] = scipy.__version__

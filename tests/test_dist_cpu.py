@@ -7,7 +7,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2403_12422_b200.dist import allreduce_mean, finish_allreduce, shard_sequences
+from paper_2403_12422_b200.dist import OverlappedAllReduce, allreduce_mean, finish_allreduce, shard_sequences
 
 
 def _free_port():
@@ -32,7 +32,13 @@ def _worker(rank, world, port, bucket_bytes, use_async, out):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         grads = _grads(rank)
-        if use_async:
+        if use_async == "overlap":  # groups as a model's backward releases them
+            ov = OverlappedAllReduce()
+            ov.hook(grads, ["qkv.w", "qkv.b"])
+            ov.hook(grads, ["proj.w", "proj.b"])
+            ov.hook(grads, ["ln1.gamma", "ln1.beta"])
+            ov.finish(grads)
+        elif use_async:
             finish_allreduce(allreduce_mean(grads, bucket_bytes=bucket_bytes, async_op=True), grads)
         else:
             allreduce_mean(grads, bucket_bytes=bucket_bytes)
@@ -41,7 +47,8 @@ def _worker(rank, world, port, bucket_bytes, use_async, out):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("bucket_bytes,use_async", [(64 << 20, False), (512, False), (512, True)])
+@pytest.mark.parametrize("bucket_bytes,use_async", [(64 << 20, False), (512, False), (512, True),
+                                                    (0, "overlap")])
 def test_allreduce_mean_world2(bucket_bytes, use_async):
     world = 2
     out = mp.Manager().dict()

@@ -480,3 +480,17 @@ def test_attention_boundary_kernels(jf):
     g = core2.backward(jf.dequantize(dattn, torch.bfloat16), b, s).float()
     got = dqkv.dequantize()
     assert (got - g).abs().max() <= 0.05 * g.abs().max()
+
+
+def test_jqt1_matches_reference_blob(jf):
+    """JQT1 BlockQuantTensor bytes (qtensor.py:152-181) equal to the reference's for the same input."""
+    import os
+
+    gold = os.path.join(os.path.dirname(__file__), "golden")
+    x = np.load(os.path.join(gold, "jqt1_ref_input.npy"))
+    with open(os.path.join(gold, "jqt1_ref.bin"), "rb") as fh:
+        ref = fh.read()
+    xq = jf.quantize_per_block(cu(x))
+    assert xq.to_bytes() == ref
+    back = jf.BlockQuantTensor.from_bytes(ref)
+    assert torch.equal(back.values, xq.values) and torch.equal(back.scales, xq.scales)

@@ -62,3 +62,63 @@ def test_gpt2_shaped_step_runs(jf):
         losses.append(float(loss))
     assert all(np.isfinite(losses)) and abs(losses[0] - np.log(cfg.vocab)) < 0.5
     assert losses[-1] < losses[0]  # same batch three times: the loss must drop
+
+
+def test_training_state_roundtrip(jf, tmp_path):
+    """save -> load into a fresh model resumes bit-identically (trainer.py:462-477, 526-536)."""
+    from paper_2403_12422_b200.checkpoint import load_training_state, save_training_state
+    from paper_2403_12422_b200.model import AdamW, JetfireLM, ModelConfig
+
+    cfg = ModelConfig(layers=1, c_model=64, heads=2, hidden=128, vocab=64, max_seq=32, head_dtype="fp32")
+    x = torch.randint(0, cfg.vocab, (2, 32), device="cuda")
+    y = torch.roll(x, -1, dims=1)
+    a = JetfireLM(cfg, seed=5)
+    oa = AdamW(a, lr=1e-3, weight_decay=0.1)
+    for _ in range(2):
+        oa.step(a.loss_and_grads(x, y)[1])
+    save_training_state(tmp_path / "ck", a, oa, step=2)
+    b = JetfireLM(cfg, seed=6)
+    ob = AdamW(b, lr=1e-3, weight_decay=0.1)
+    assert load_training_state(tmp_path / "ck", b, ob) == 2
+    la, ga = a.loss_and_grads(x, y)
+    lb, gb = b.loss_and_grads(x, y)
+    assert float(la) == float(lb)
+    oa.step(ga)
+    ob.step(gb)
+    for k in a.params:
+        assert torch.equal(a.params[k], b.params[k]), k
+
+
+def test_overlapped_allreduce_hook_nccl_world1(jf):
+    """The DP gradient hook end to end on NCCL (world size 1 here; the sums are exercised
+    at world size 2 over gloo in test_dist_cpu.py)."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2403_12422_b200.dist import OverlappedAllReduce
+    from paper_2403_12422_b200.model import JetfireLM, ModelConfig
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        cfg = ModelConfig(layers=2, c_model=64, heads=2, hidden=128, vocab=64, max_seq=32, pos_emb=True,
+                          head_dtype="bf16")
+        m = JetfireLM(cfg, seed=2)
+        x = torch.randint(0, cfg.vocab, (2, 32), device="cuda")
+        y = torch.roll(x, -1, dims=1)
+        _, g0 = m.loss_and_grads(x, y)
+        ov = OverlappedAllReduce()
+        seen = []
+        _, g1 = m.loss_and_grads(x, y, grad_hook=lambda g, names: (seen.extend(names), ov.hook(g, names)))
+        ov.finish(g1)
+        assert sorted(seen) == sorted(g0)          # every gradient went through exactly one hook call
+        for k in g0:
+            assert torch.equal(g0[k], g1[k]), k
+    finally:
+        dist.destroy_process_group()
