@@ -158,6 +158,14 @@ int jf_colsum(const int8_t *q, const float *s, int64_t n, int64_t c, float *out,
               void *workspace, jf_stream_t stream);
 size_t jf_colsum_workspace_bytes(int64_t n, int64_t c);
 
+/* Loss head (model step, trainer.py:387-406): softmax cross-entropy of bf16 logits [n x ld]
+ * (columns v..ld are padding and get zero gradient; padded logits should be -inf).
+ * row_loss[r] = -mask_r * log_softmax(logits)[r, y_r] / n_live; dlogits (bf16 [n x ld]) =
+ * (softmax - onehot(y)) * mask_r / n_live.  mask may be NULL; n_live is a device scalar. */
+int jf_cross_entropy_bf16(const uint16_t *logits, int64_t n, int64_t v, int64_t ld, const int64_t *y,
+                          const float *mask, const float *n_live, float *row_loss, uint16_t *dlogits,
+                          jf_stream_t stream);
+
 /* Dropout by scale folding  [qnonlinear.py:207-240]: codes zeroed where keep[i]==0,
  * scales snapped f16(s * keep_factor).  keep: [n x c] uint8 (the materialized mask). */
 int jf_dropout(const int8_t *q, const float *s, const uint8_t *keep, float keep_factor,

@@ -20,6 +20,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
+from . import _lib
 from .qlayers import BlockConfig, TransformerBlock
 from .qtensor import quantize_per_block
 
@@ -132,36 +133,44 @@ class JetfireLM:
             hq = blk.forward(hq, batch, seq)
         h = hq.dequantize()
 
-        if self.cfg.head_dtype == "bf16":
-            w16, b16 = self._head_bf16()
-            h16 = h.to(torch.bfloat16)
-            logits = torch.addmm(b16, h16, w16.t()).float()
-        else:
-            logits = torch.addmm(self.params["head.b"], h, self.params["head.w"].t())
-        logp = torch.log_softmax(logits, dim=1)
-        fm = torch.ones(batch * seq, device=h.device) if mask is None else mask.reshape(-1).float()
-        n_live = fm.sum()
-        rows = torch.arange(logits.shape[0], device=h.device)
-        fy = y.reshape(-1)
-        loss = -(logp[rows, fy] * fm).sum() / n_live
-
-        dlogits = logp.exp_()
-        dlogits[rows, fy] -= 1.0
-        dlogits *= (fm / n_live)[:, None]
+        fm = None if mask is None else mask.reshape(-1).float().contiguous()
+        n_tok = batch * seq
         grads = {}
         v = self.cfg.vocab
         if self.cfg.head_dtype == "bf16":
-            dl16 = dlogits.to(torch.bfloat16)
+            # BF16 head; fused softmax cross-entropy straight to bf16 dlogits (libjetfire ce.cu)
+            w16, b16 = self._head_bf16()
+            h16 = h.to(torch.bfloat16)
+            logits = torch.addmm(b16, h16, w16.t())
+            n_live = (torch.full((), float(n_tok), device=h.device) if fm is None else fm.sum()).float()
+            row_loss = torch.empty(n_tok, dtype=torch.float32, device=h.device)
+            dl16 = torch.empty_like(logits)
+            L = _lib.lib()
+            _lib.check(L.jf_cross_entropy_bf16(logits.data_ptr(), n_tok, v, logits.shape[1],
+                                               y.reshape(-1).contiguous().data_ptr(), _lib.ptr(fm),
+                                               n_live.data_ptr(), row_loss.data_ptr(), dl16.data_ptr(),
+                                               _lib.stream_handle()), "cross_entropy")
+            loss = row_loss.sum()
             grads["head.w"] = (dl16.t() @ h16)[:v].float()
             dh = (dl16 @ w16).float()
-            grads["head.b"] = dlogits[:, :v].sum(dim=0)
+            grads["head.b"] = dl16[:, :v].float().sum(dim=0)
         else:
+            logits = torch.addmm(self.params["head.b"], h, self.params["head.w"].t())
+            logp = torch.log_softmax(logits, dim=1)
+            fmv = torch.ones(n_tok, device=h.device) if fm is None else fm
+            n_live = fmv.sum()
+            rows = torch.arange(n_tok, device=h.device)
+            fy = y.reshape(-1)
+            loss = -(logp[rows, fy] * fmv).sum() / n_live
+            dlogits = logp.exp_()
+            dlogits[rows, fy] -= 1.0
+            dlogits *= (fmv / n_live)[:, None]
             grads["head.w"] = dlogits.t() @ h
             dh = dlogits @ self.params["head.w"]
             grads["head.b"] = dlogits.sum(dim=0)
-
         if grad_hook is not None:
             grad_hook(grads, ["head.w", "head.b"])
+
         dq = quantize_per_block(dh.contiguous())
         for i in reversed(range(len(self.blocks))):
             dq, bg = self.blocks[i].backward(dq)

@@ -122,3 +122,30 @@ def test_overlapped_allreduce_hook_nccl_world1(jf):
             assert torch.equal(g0[k], g1[k]), k
     finally:
         dist.destroy_process_group()
+
+
+def test_fused_cross_entropy(jf):
+    """jf_cross_entropy_bf16 == FP32 log_softmax / softmax-minus-onehot of the same bf16 logits."""
+    from paper_2403_12422_b200 import _lib
+
+    torch.manual_seed(0)
+    n, v, ld = 64, 1000, 1024
+    logits = torch.full((n, ld), float("-inf"), device="cuda", dtype=torch.bfloat16)
+    logits[:, :v] = (3 * torch.randn(n, v, device="cuda")).to(torch.bfloat16)
+    y = torch.randint(0, v, (n,), device="cuda")
+    mask = (torch.rand(n, device="cuda") > 0.2).float()
+    n_live = mask.sum()
+    row_loss = torch.empty(n, device="cuda")
+    dl = torch.empty_like(logits)
+    L = _lib.lib()
+    assert L.jf_cross_entropy_bf16(logits.data_ptr(), n, v, ld, y.data_ptr(), mask.data_ptr(), n_live.data_ptr(),
+                                   row_loss.data_ptr(), dl.data_ptr(), _lib.stream_handle()) == 0
+    lp = torch.log_softmax(logits[:, :v].float(), dim=1)
+    ref_loss = -(lp[torch.arange(n), y] * mask).sum() / n_live
+    assert abs(float(row_loss.sum()) - float(ref_loss)) <= 1e-5 * abs(float(ref_loss))
+    ref_d = lp.exp()
+    ref_d[torch.arange(n), y] -= 1.0
+    ref_d *= (mask / n_live)[:, None]
+    got = dl[:, :v].float()
+    assert (got - ref_d).abs().max() <= 2 ** -8 * ref_d.abs().max()  # bf16 output rounding
+    assert torch.count_nonzero(dl[:, v:]) == 0
