@@ -1,5 +1,16 @@
-mkdir -p gpurun_out/pp
-JF_GEMM_PIPE=1 timeout 600 python -m pytest tests -m gpu -x -q -k "gemm or linear or block or model" > gpurun_out/pp/pytest.log 2>&1
-python tools/gemm_ab.py --shape mlp1 --mode exact --rounds 3 --configs "pipe=0" "pipe=1" > gpurun_out/pp/ab.jsonl 2>&1
-python tools/gemm_ab.py --shape mlp1 --mode fast --rounds 3 --configs "pipe=0" "pipe=1" >> gpurun_out/pp/ab.jsonl 2>&1
-python tools/gemm_ab.py --shape proj --mode exact --rounds 3 --configs "pipe=0" "pipe=1" >> gpurun_out/pp/ab.jsonl 2>&1
+mkdir -p gpurun_out/nw2
+cat > /tmp/t.py <<'PY'
+import sys, torch
+sys.path.insert(0, '.')
+import paper_2403_12422_b200 as jf
+jf.require_cuda()
+which = sys.argv[1]
+x = jf.quantize_per_block(torch.randn(256, 256, device='cuda'))
+w = jf.quantize_per_block(torch.randn(256, 256, device='cuda'))
+if which == "fwd": y = jf.block_mm_forward(x, w)
+elif which == "dgrad": y = jf.block_mm_grad_input(x, w)
+else: y = jf.block_mm_grad_weight(x, w)
+torch.cuda.synchronize(); print(which, "ok")
+PY
+for w in fwd dgrad wgrad; do CUDA_LAUNCH_BLOCKING=1 timeout 120 python /tmp/t.py $w >> gpurun_out/nw2/out.txt 2>&1; done
+timeout 300 compute-sanitizer --tool memcheck python /tmp/t.py fwd > gpurun_out/nw2/san.txt 2>&1
