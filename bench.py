@@ -204,8 +204,14 @@ class BlockWorkload:
 
     def step(self):
         self.blk.forward(self.xq, self.b, self.s)
-        dx, grads = self.blk.backward(self.dyq)
-        allreduce_grads(grads, self.world)
+        if self.world > 1:  # DP: the MLP half's all-reduce overlaps the attention half's backward
+            from paper_2403_12422_b200.dist import OverlappedAllReduce
+
+            ov = OverlappedAllReduce()
+            dx, grads = self.blk.backward(self.dyq, grad_hook=ov.hook)
+            ov.finish(grads)
+        else:
+            self.blk.backward(self.dyq)
 
     def e2e_setup(self):
         n, c = self.n, self.c

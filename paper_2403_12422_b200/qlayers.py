@@ -344,7 +344,10 @@ class TransformerBlock:
         return out
 
     def backward(self, dyq: BlockQuantTensor, counters: AccessCounters | None = None,
-                 threads: int = 1):
+                 threads: int = 1, grad_hook=None):
+        """(dX, grads) as qlayers.py:385-427.  ``grad_hook(grads, names)`` (optional) is called
+        as soon as the named FP32 parameter gradients are final, in backward order, so a
+        data-parallel caller can overlap their all-reduce with the rest of backward."""
         if self._saved is None:
             raise RuntimeError("backward called before forward")
         s = self._saved
@@ -355,6 +358,10 @@ class TransformerBlock:
         dm1 = gelu_backward(s.m1, dg, counters)
         dln2, dw_mlp1, db_mlp1 = self.mlp1.backward(dm1, counters, threads)
         dh_branch, dgamma2, dbeta2 = layernorm_backward(s.ctx2, dln2, self.ln2, counters)
+        if grad_hook is not None:
+            grad_hook({"mlp2.w": dw_mlp2, "mlp2.b": db_mlp2, "mlp1.w": dw_mlp1, "mlp1.b": db_mlp1,
+                       "ln2.gamma": dgamma2, "ln2.beta": dbeta2},
+                      ["mlp2.w", "mlp2.b", "mlp1.w", "mlp1.b", "ln2.gamma", "ln2.beta"])
         dh, _ = add_forward(dh_branch, dyq, width, counters)
 
         dproj = dropout_backward(dh, s.drop1, counters)
@@ -368,6 +375,10 @@ class TransformerBlock:
         da1_branch, dgamma1, dbeta1 = layernorm_backward(s.ctx1, dln1, self.ln1, counters)
         dx, _ = add_forward(da1_branch, dh, width, counters)
 
+        if grad_hook is not None:
+            grad_hook({"proj.w": dw_proj, "proj.b": db_proj, "qkv.w": dw_qkv, "qkv.b": db_qkv,
+                       "ln1.gamma": dgamma1, "ln1.beta": dbeta1},
+                      ["proj.w", "proj.b", "qkv.w", "qkv.b", "ln1.gamma", "ln1.beta"])
         grads = {
             "qkv.w": dw_qkv, "qkv.b": db_qkv, "proj.w": dw_proj, "proj.b": db_proj,
             "mlp1.w": dw_mlp1, "mlp1.b": db_mlp1, "mlp2.w": dw_mlp2, "mlp2.b": db_mlp2,

@@ -120,6 +120,19 @@ def test_overlapped_allreduce_hook_nccl_world1(jf):
         assert sorted(seen) == sorted(g0)          # every gradient went through exactly one hook call
         for k in g0:
             assert torch.equal(g0[k], g1[k]), k
+        # the block-level hook (bench.py's DP block step)
+        blk = m.blocks[0]
+        xq = jf.quantize_per_block(torch.randn(64, 64, device="cuda"))
+        dyq = jf.quantize_per_block(0.1 * torch.randn(64, 64, device="cuda"))
+        blk.forward(xq, 2, 32)
+        _, r0 = blk.backward(dyq)
+        blk.forward(xq, 2, 32)
+        ov2, seen2 = OverlappedAllReduce(), []
+        _, r1 = blk.backward(dyq, grad_hook=lambda g, names: (seen2.extend(names), ov2.hook(g, names)))
+        ov2.finish(r1)
+        assert sorted(seen2) == sorted(r0)
+        for k in r0:
+            assert torch.equal(r0[k], r1[k]), k
     finally:
         dist.destroy_process_group()
 
