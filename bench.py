@@ -460,6 +460,70 @@ def bf16_block_tokens_per_s(w, steps, warmup):
     return n * steps / (ms / 1e3), ms / steps
 
 
+def bf16_model_tokens_per_s(w, steps, warmup):
+    """GPT-2-style step in standard PyTorch mixed precision: FP32 params, BF16 autocast
+    (cuBLAS linears, SDPA, exact-erf GELU, LayerNorm), BF16 head + FP32 CE, fused AdamW."""
+    import torch.nn as nn
+    import torch.nn.functional as F
+
+    from paper_2403_12422_b200.model import ModelConfig
+
+    cfg = getattr(ModelConfig, w["model"])()
+    c, h, heads, b, s = cfg.c_model, cfg.hidden, cfg.heads, w["batch"], w["seq"]
+    vp = (cfg.vocab + 127) // 128 * 128
+
+    class Block(nn.Module):
+        def __init__(self):
+            super().__init__()
+            self.ln1, self.ln2 = nn.LayerNorm(c), nn.LayerNorm(c)
+            self.qkv, self.proj = nn.Linear(c, 3 * c), nn.Linear(c, c)
+            self.mlp1, self.mlp2 = nn.Linear(c, h), nn.Linear(h, c)
+
+        def forward(self, x):
+            q, k, v = self.qkv(self.ln1(x)).view(b, s, 3, heads, c // heads).unbind(2)
+            o = F.scaled_dot_product_attention(q.transpose(1, 2), k.transpose(1, 2), v.transpose(1, 2),
+                                               is_causal=True)
+            x = x + self.proj(o.transpose(1, 2).reshape(b, s, c))
+            return x + self.mlp2(F.gelu(self.mlp1(self.ln2(x)), approximate="none"))
+
+    class LM(nn.Module):
+        def __init__(self):
+            super().__init__()
+            self.emb, self.wpe = nn.Embedding(vp, c), nn.Embedding(s, c)
+            self.blocks = nn.ModuleList([Block() for _ in range(cfg.layers)])
+            self.head = nn.Linear(c, vp)
+
+        def forward(self, x, y):
+            hh = self.emb(x) + self.wpe.weight[None]
+            for blk in self.blocks:
+                hh = blk(hh)
+            return F.cross_entropy(self.head(hh).float().view(-1, vp), y.view(-1))
+
+    model = LM().cuda()
+    opt = torch.optim.AdamW(model.parameters(), lr=1e-4, weight_decay=0.1, fused=True)
+    x = torch.randint(0, cfg.vocab, (b, s), device="cuda")
+    y = torch.roll(x, -1, dims=1)
+
+    def step():
+        with torch.autocast("cuda", dtype=torch.bfloat16):
+            loss = model(x, y)
+        loss.backward()
+        opt.step()
+        opt.zero_grad(set_to_none=True)
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(steps):
+        step()
+    e.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(e)
+    return b * s * steps / (ms / 1e3), ms / steps
+
+
 # ── CPU oracle (the reference's algorithm, numpy port) ──────────────────
 
 
@@ -517,6 +581,12 @@ def main():
         return
     out, wl, _, w = run_ours(args, world, rank, local)
     if rank == 0:
+        if not args.no_bf16 and "model" in w:
+            tps, ms = bf16_model_tokens_per_s(w, args.steps, args.warmup)
+            out["bf16_baseline"] = {"value": round(tps * world, 1), "unit": "tokens/s", "ms_per_step": round(ms, 4),
+                                    "what": "same model in torch BF16 autocast (cuBLAS, SDPA, exact GELU, "
+                                            "LayerNorm, fused AdamW), 1 GPU",
+                                    "int8_over_bf16": round(out["value"] / (tps * world), 3)}
         if not args.no_bf16 and "model" not in w:
             wb = dict(w)
             tps, ms = bf16_block_tokens_per_s(wb, args.steps, args.warmup)
