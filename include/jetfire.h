@@ -166,6 +166,18 @@ int jf_cross_entropy_bf16(const uint16_t *logits, int64_t n, int64_t v, int64_t 
                           const float *mask, const float *n_live, float *row_loss, uint16_t *dlogits,
                           jf_stream_t stream);
 
+/* AdamW step (trainer.py:247-262) in the reference's float32 operation order; lr, eps, wd,
+ * bc1 = 1 - b1^t, bc2 = 1 - b2^t are the float32 roundings of the Python floats, b1 and b2 the
+ * doubles themselves (the reference forms 1 - b1 in float64) (wd = 0: no decay).
+ * jf_adamw: flat update of count elements of p, m, v (in place).
+ * jf_adamw_quantize: same for a [n x c] matrix, then quantize_per_block(p) -> q, s
+ *   (the INT8 weight copy, qlayers.py:139-143) in the same pass. */
+int jf_adamw(float *p, const float *g, float *m, float *v, int64_t count, float lr, double b1, double b2,
+             float eps, float wd, float bc1, float bc2, jf_stream_t stream);
+int jf_adamw_quantize(float *p, const float *g, float *m, float *v, int64_t n, int64_t c, float lr, double b1,
+                      double b2, float eps, float wd, float bc1, float bc2, int8_t *q, float *s, int32_t *err,
+                      jf_stream_t stream);
+
 /* Dropout by scale folding  [qnonlinear.py:207-240]: codes zeroed where keep[i]==0,
  * scales snapped f16(s * keep_factor).  keep: [n x c] uint8 (the materialized mask). */
 int jf_dropout(const int8_t *q, const float *s, const uint8_t *keep, float keep_factor,

@@ -63,6 +63,10 @@ SIGNATURES = {
     "jf_colsum_workspace_bytes": (_SZ, [_I64, _I64]),
     "jf_dropout": (ctypes.c_int, [_P, _P, _P, _F32, _I64, _I64, _P, _P, _P, _P]),
     "jf_gemm_set_option": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int]),
+    "jf_adamw": (ctypes.c_int, [_P, _P, _P, _P, _I64, _F32, ctypes.c_double, ctypes.c_double, _F32, _F32, _F32,
+                                _F32, _P]),
+    "jf_adamw_quantize": (ctypes.c_int, [_P, _P, _P, _P, _I64, _I64, _F32, ctypes.c_double, ctypes.c_double, _F32,
+                                         _F32, _F32, _F32, _P, _P, _P, _P]),
     "jf_cross_entropy_bf16": (ctypes.c_int, [_P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P]),
     "jf_dequantize_qkv_heads": (ctypes.c_int, [_P, _P, _I64, _I64, _I64, _I64, _P, _P, _P, _P]),
     "jf_quantize_heads_bf16": (ctypes.c_int, [_P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _P, _I64, _P, _I64,
@@ -116,7 +120,7 @@ KERNELS_PER_CALL = {
     "quantize": 1, "dequantize": 1, "transpose": 1, "gemm_fwd": 1, "gemm_dgrad": 1, "gemm_wgrad": 1,
     "gemm_partials": 1, "add_stats": 1, "ln_fwd": 2, "ln_bwd": 4, "gelu_fwd": 1, "gelu_bwd": 1,
     "colsum": 2, "dropout": 1, "gelu_tables": 1, "dequant_qkv_heads": 1, "quantize_heads": 1,
-    "cross_entropy": 1,
+    "cross_entropy": 1, "adamw": 1, "adamw_quantize": 1,
 }
 launch_count = [0]
 

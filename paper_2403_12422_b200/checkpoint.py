@@ -60,31 +60,21 @@ def load_params(path) -> tuple[dict, dict]:
 def save_training_state(path, model, opt, step: int) -> None:
     """Parameters + AdamW moments in the reference trainer's layout."""
     state = {}
-    adam = opt.opt.state
     for k, p in model.params.items():
-        st = adam.get(p, {})
         state[f"param.{k}"] = p
-        state[f"m.{k}"] = st.get("exp_avg", torch.zeros_like(p))
-        state[f"v.{k}"] = st.get("exp_avg_sq", torch.zeros_like(p))
-    t = 0
-    for st in adam.values():
-        t = int(st["step"]) if "step" in st else t
-    save_params(path, state, {"step": int(step), "opt_t": t, "scheme": "per-block"})
+        state[f"m.{k}"] = opt.m[k]
+        state[f"v.{k}"] = opt.v[k]
+    save_params(path, state, {"step": int(step), "opt_t": int(opt.t), "scheme": "per-block"})
 
 
 def load_training_state(path, model, opt) -> int:
     """Restore parameters + moments (trainer.py:462-477); returns the checkpoint step."""
     state, meta = load_params(path)
-    t = int(meta["opt_t"])
     for k, p in model.params.items():
-        with torch.no_grad():
-            p.copy_(torch.from_numpy(state[f"param.{k}"]))
-        if t > 0:
-            opt.opt.state[p] = {
-                "step": torch.tensor(float(t), dtype=torch.float32, device=p.device),
-                "exp_avg": torch.from_numpy(state[f"m.{k}"]).to(p.device),
-                "exp_avg_sq": torch.from_numpy(state[f"v.{k}"]).to(p.device),
-            }
+        p.copy_(torch.from_numpy(state[f"param.{k}"]))
+        opt.m[k].copy_(torch.from_numpy(state[f"m.{k}"]))
+        opt.v[k].copy_(torch.from_numpy(state[f"v.{k}"]))
+    opt.t = int(meta["opt_t"])
     model.mark_updated()
     return int(meta["step"])
 

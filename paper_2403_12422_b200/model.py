@@ -194,26 +194,50 @@ class JetfireLM:
 
 
 class AdamW:
-    """Adam with decoupled weight decay and bias correction, FP32 state (trainer.py:225-262),
-    as torch's fused multi-tensor CUDA kernel; the INT8 weight copies are re-derived lazily."""
+    """AdamW exactly as the reference (trainer.py:225-262): FP32 moments, bias correction,
+    decoupled decay on ``model.decay_keys``, in the reference's float32 operation order
+    (libjetfire ``jf_adamw``; bit-identical updates).  Block weight matrices are updated by
+    ``jf_adamw_quantize``, which also writes their INT8 copy (qlayers.py:139-143) in the same
+    pass, so the next forward finds ``weight_q`` ready instead of re-quantizing the master."""
 
     def __init__(self, model: JetfireLM, lr: float, weight_decay: float = 0.0, betas=(0.9, 0.999),
                  eps: float = 1e-8):
         self.model = model
-        keys = sorted(model.params)
-        decay = [model.params[k] for k in keys if k in model.decay_keys]
-        rest = [model.params[k] for k in keys if k not in model.decay_keys]
-        self.keys = [k for k in keys if k in model.decay_keys] + [k for k in keys if k not in model.decay_keys]
-        groups = [{"params": decay, "weight_decay": weight_decay}, {"params": rest, "weight_decay": 0.0}]
-        self.opt = torch.optim.AdamW(groups, lr=lr, betas=betas, eps=eps, fused=True)
+        self.lr, self.weight_decay, self.betas, self.eps = lr, weight_decay, betas, eps
+        self.m = {k: torch.zeros_like(v) for k, v in model.params.items()}
+        self.v = {k: torch.zeros_like(v) for k, v in model.params.items()}
+        self.t = 0
+        self.qlin = {}
+        for i, blk in enumerate(model.blocks):
+            for name in ("qkv", "proj", "mlp1", "mlp2"):
+                self.qlin[f"block{i}.{name}.w"] = getattr(blk, name)
 
     def step(self, grads: dict) -> None:
-        for k in self.keys:
-            self.model.params[k].grad = grads[k]
-        self.opt.step()
-        for k in self.keys:
-            self.model.params[k].grad = None
-        self.model.mark_updated()
+        from .qtensor import empty_like_shape
+        from . import runtime as _rt
+
+        self.t += 1
+        b1, b2 = self.betas
+        bc1 = 1.0 - b1 ** self.t
+        bc2 = 1.0 - b2 ** self.t
+        L = _lib.lib()
+        st = _lib.stream_handle()
+        for key, p in self.model.params.items():
+            g = grads[key].contiguous()
+            wd = self.weight_decay if (key in self.model.decay_keys and self.weight_decay) else 0.0
+            lin = self.qlin.get(key)
+            if lin is not None:
+                n, c = p.shape
+                wq = empty_like_shape(n, c, p.device)
+                _lib.check(L.jf_adamw_quantize(p.data_ptr(), g.data_ptr(), self.m[key].data_ptr(),
+                                               self.v[key].data_ptr(), n, c, self.lr, b1, b2, self.eps, wd,
+                                               bc1, bc2, wq.values.data_ptr(), wq.scales.data_ptr(),
+                                               _rt.err_ptr(), st), "adamw_quantize")
+                lin._weight_q, lin._weight_qt = wq, None
+            else:
+                _lib.check(L.jf_adamw(p.data_ptr(), g.data_ptr(), self.m[key].data_ptr(), self.v[key].data_ptr(),
+                                      p.numel(), self.lr, b1, b2, self.eps, wd, bc1, bc2, st), "adamw")
+        _rt.maybe_check()
 
 
 __all__ = ["AdamW", "JetfireLM", "ModelConfig"]
