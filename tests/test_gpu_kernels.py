@@ -197,13 +197,15 @@ def test_gemm_random_exact_vs_oracle(jf, n, c, d):
 
 
 @pytest.mark.parametrize("promotion", ["exact", "fast"])
-def test_gemm_paths_bit_identical(jf, promotion):
+@pytest.mark.parametrize("shape", [(256, 384, 512), (2048, 256, 2304)])
+def test_gemm_paths_bit_identical(jf, promotion, shape):
     """Staged-scales kernel with MN-major operands (dgrad reads W, wgrad reads dY and X as
-    stored) vs the generic kernel on transposed copies: same bits, every output kind."""
+    stored) vs the generic kernel on transposed copies: same bits, every output kind.  The
+    second shape has more tiles than SMs (persistent loop)."""
     from paper_2403_12422_b200 import runtime
 
     rng = np.random.default_rng(5)
-    n, c, d = 256, 384, 512
+    n, c, d = shape
     X = bqt(jf, *_rand_q(rng, (n, c)))
     W = bqt(jf, *_rand_q(rng, (d, c), 1 / np.sqrt(c)))
     DY = bqt(jf, *_rand_q(rng, (n, d), 0.1))
@@ -219,11 +221,12 @@ def test_gemm_paths_bit_identical(jf, promotion):
         generic = run()
     finally:
         runtime.set_gemm_option("tma_scales", 1)
-    for a, b in ((staged[0], generic[0]), (staged[1], generic[1])):
-        assert torch.equal(a.values, b.values) and torch.equal(a.scales, b.scales)
-    assert torch.equal(staged[2][0].values, generic[2][0].values)
-    assert torch.equal(staged[2][1], generic[2][1])
-    assert torch.equal(staged[3], generic[3])
+    for other in (generic,):
+        for a, b in ((staged[0], other[0]), (staged[1], other[1])):
+            assert torch.equal(a.values, b.values) and torch.equal(a.scales, b.scales)
+        assert torch.equal(staged[2][0].values, other[2][0].values)
+        assert torch.equal(staged[2][1], other[2][1])
+        assert torch.equal(staged[3], other[3])
 
 
 def test_gemm_fast_mode_tolerance(jf):

@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--shape", default="mlp1")
     ap.add_argument("--mode", default="exact")
     ap.add_argument("--configs", nargs="+", required=True)
+    ap.add_argument("--base", default="", help="options applied before every config (reset keys)")
     ap.add_argument("--rounds", type=int, default=5)
     ap.add_argument("--iters", type=int, default=10)
     a = ap.parse_args()
@@ -42,6 +43,7 @@ def main():
     times = {cfg: [] for cfg in a.configs}
     for _ in range(a.rounds):
         for cfg in a.configs:
+            apply(a.base)
             apply(cfg)
             for _ in range(2):
                 jf.block_mm_forward(x, w, promotion=a.mode)
