@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--workload", default="block_h4096_s2048", choices=sorted(WORKLOADS))
     ap.add_argument("--batch", type=int, default=None, help="sequences per GPU")
     ap.add_argument("--promotion", default="exact", choices=["exact", "fast"])
+    ap.add_argument("--operands", default="f16", choices=["int8", "f16"],
+                    help="GEMM operand path (runtime.set_gemm_operands); both bit-identical")
     ap.add_argument("--attn-dtype", default="bf16", choices=["bf16", "fp32"])
     ap.add_argument("--no-bf16", action="store_true", help="skip the cuBLAS BF16 block baseline")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle baseline")
@@ -303,6 +305,7 @@ def run_ours(args, world, rank, local):
     jf.require_cuda()
     jf.set_error_check("deferred")
     jf.set_promotion(args.promotion)
+    jf.runtime.set_gemm_operands(args.operands)
     w = dict(WORKLOADS[args.workload])
     if args.batch:
         w["batch"] = args.batch
@@ -356,7 +359,7 @@ def run_ours(args, world, rank, local):
 
     cfg = {"workload": args.workload}
     cfg.update(wl.config())
-    cfg.update({"global_tokens": world * n, "block": 32, "promotion": args.promotion,
+    cfg.update({"global_tokens": world * n, "block": 32, "promotion": args.promotion, "operands": args.operands,
                 "attention": f"torch SDPA ({args.attn_dtype})",
                 "parallelism": f"dp{world}" if world > 1 else "single"})
     out = {
@@ -374,12 +377,14 @@ def run_ours(args, world, rank, local):
                  "share_of_step": round(gemm_ms_step / ms_step, 3)},
     }
     out["clocks"] = clocks.summary()
-    out["roofline"] = roofline(gemm_tops, args.promotion, clocks_mhz=out["clocks"].get("sm_mhz"))
+    out["roofline"] = roofline(gemm_tops, args.promotion, clocks_mhz=out["clocks"].get("sm_mhz"),
+                               operands=args.operands)
     return out, wl, None, w
 
 
-def roofline(gemm_tops: float, promotion: str, clocks_mhz=None) -> dict:
-    """Dominant kernel = gemm_i8s_kernel (87% of the step).
+def roofline(gemm_tops: float, promotion: str, clocks_mhz=None, operands: str = "f16") -> dict:
+    """Dominant kernel = the block GEMM (gemm_f16s_kernel on the default f16-widened
+    operand path, gemm_i8s_kernel with --operands int8; ~87% of the step).
 
     peak: B200 dense INT8 (datasheet 4.5 POPS; our raw kind::i8 microbenchmark
     measures 8178 MAC/clk/SM = 4.76 POPS at 1965 MHz).  The binding bound under
@@ -396,13 +401,16 @@ def roofline(gemm_tops: float, promotion: str, clocks_mhz=None) -> dict:
         why = "int32->fp32 conversion (I2FP, ALU pipe, half rate) per output element per chunk"
     traffic = None
     tr_src = None
+    key = "gemm_f16s_kernel" if operands == "f16" else "gemm_i8_kernel"
     try:
         with open(os.path.join(ROOT, "profiles", "roofline_traffic.json")) as f:
-            t = json.load(f)["gemm_i8_kernel"]
+            t = json.load(f)[key]
         traffic, tr_src = t["dram_bytes_per_launch"], t["launch"] + " (" + t["source"] + ")"
     except (OSError, KeyError, ValueError):
         pass
-    return {"kernel": "gemm_i8s_kernel (tcgen05 kind::i8)", "bound": "tensor", "achieved": round(gemm_tops, 1),
+    kname = ("gemm_f16s_kernel (tcgen05 kind::f16 on f16-widened int8 codes)" if operands == "f16"
+             else "gemm_i8s_kernel (tcgen05 kind::i8)")
+    return {"kernel": kname, "bound": "tensor", "achieved": round(gemm_tops, 1),
             "peak": INT8_PEAK_TOPS, "unit": "TFLOP/s", "frac": round(gemm_tops / INT8_PEAK_TOPS, 4),
             "traffic": traffic, "traffic_launch": tr_src,
             "peak_source": "B200 dense INT8 datasheet 4.5 POPS (int ops counted as FLOP); "

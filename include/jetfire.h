@@ -105,6 +105,24 @@ int jf_gemm_wgrad(const int8_t *dy, const float *dys, const int8_t *x, const flo
                   int64_t n, int64_t d, int64_t c, int32_t mode, int32_t out_kind, int8_t *dwq,
                   float *dws, float *dwf, void *scratch, int32_t *err, jf_stream_t stream);
 
+/* f16-widened operand path (same products as K3-K5, bit-identical; B200 design choice,
+ * no reference counterpart).  The int8 codes widened to f16 (exact) let the tcgen05
+ * kind::f16 MMA accumulate the per-chunk integer partials in f32 directly, so the
+ * promotion skips the int32->fp32 conversion that bounds the int8 kernels.
+ * jf_widen_codes: y = f16(x) [rows x cols], or f16(x)^T [cols x rows] when transpose != 0
+ * (rows, cols multiples of 64).  Used for the weights (cached per update) and activations. */
+int jf_widen_codes(const int8_t *x, int64_t rows, int64_t cols, uint16_t *y, int32_t transpose,
+                   jf_stream_t stream);
+
+/* Y[m x n] = A[m x k] . B[n x k]^T, A and B f16-widened codes, both K-major; sa / sb the
+ * per-32x32 scale grids of A [m/32 x k/32] and B [n/32 x k/32] with element strides
+ * (s0, s1) (contiguous along one axis).  m, n, k multiples of 128.  Output kinds,
+ * promotion and requantization as jf_gemm_fwd. */
+int jf_gemm_f16(const uint16_t *a, const float *sa, int64_t sa_s0, int64_t sa_s1, const uint16_t *b,
+                const float *sb, int64_t sb_s0, int64_t sb_s1, const float *bias, int64_t m, int64_t n,
+                int64_t k, int32_t mode, int32_t out_kind, int8_t *yq, float *ys, float *yf,
+                int32_t *err, jf_stream_t stream);
+
 /* Scratch bytes jf_gemm_dgrad / jf_gemm_wgrad need for the given shape. */
 size_t jf_gemm_scratch_bytes(int32_t which /*1=dgrad,2=wgrad*/, int64_t n, int64_t d, int64_t c);
 

@@ -50,6 +50,9 @@ SIGNATURES = {
     "jf_gemm_wgrad": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I32, _I32, _P, _P, _P,
                                      _P, _P, _P]),
     "jf_gemm_scratch_bytes": (_SZ, [_I32, _I64, _I64, _I64]),
+    "jf_widen_codes": (ctypes.c_int, [_P, _I64, _I64, _P, _I32, _P]),
+    "jf_gemm_f16": (ctypes.c_int, [_P, _P, _I64, _I64, _P, _P, _I64, _I64, _P, _I64, _I64, _I64, _I32, _I32,
+                                   _P, _P, _P, _P, _P]),
     "jf_gemm_partials": (ctypes.c_int, [_P, _P, _I64, _I64, _I64, _I64, _P, _P]),
     "jf_add_stats": (ctypes.c_int, [_P, _P, _P, _P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P]),
     "jf_ln_fwd": (ctypes.c_int, [_P, _P, _P, _P, _I64, _I64, _I64, _P, _P, _F32, _P, _P, _P, _P, _P, _P]),
@@ -120,7 +123,7 @@ KERNELS_PER_CALL = {
     "quantize": 1, "dequantize": 1, "transpose": 1, "gemm_fwd": 1, "gemm_dgrad": 1, "gemm_wgrad": 1,
     "gemm_partials": 1, "add_stats": 1, "ln_fwd": 2, "ln_bwd": 4, "gelu_fwd": 1, "gelu_bwd": 1,
     "colsum": 2, "dropout": 1, "gelu_tables": 1, "dequant_qkv_heads": 1, "quantize_heads": 1,
-    "cross_entropy": 1, "adamw": 1, "adamw_quantize": 1,
+    "cross_entropy": 1, "adamw": 1, "adamw_quantize": 1, "widen_codes": 1, "gemm_f16": 1,
 }
 launch_count = [0]
 

@@ -121,14 +121,15 @@ class Linear(torch.autograd.Function):
     def forward(ctx, xq, weight, bias, layer: QuantLinear):
         ctx.layer, ctx.xq = layer, xq.bq
         ctx.has_bias = bias is not None
-        return QTensor(block_mm_forward(xq.bq, layer.weight_q, bias=layer.bias))
+        return QTensor(block_mm_forward(xq.bq, layer.weight_q, bias=layer.bias, w16=layer.weight_f16(xq.bq.rows)))
 
     @staticmethod
     def backward(ctx, g):
         dyq = as_block_quant(g)
         lay = ctx.layer
         d, c = lay.master_weight.shape
-        dxq = block_mm_grad_input(dyq, lay.weight_q, wt=None if mn_major_ok(dyq.rows, d, c) else lay.weight_qt)
+        dxq = block_mm_grad_input(dyq, lay.weight_q, wt=None if mn_major_ok(dyq.rows, d, c) else lay.weight_qt,
+                                  w16t=lay.weight_f16(dyq.rows, transpose=True))
         _, dw = block_mm_grad_weight(dyq, ctx.xq, out="int8+deq")
         db = column_sum(dyq) if ctx.has_bias else None
         return QTensor(dxq), dw, db, None

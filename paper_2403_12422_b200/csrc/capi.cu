@@ -75,6 +75,29 @@ bool jf_make_tmap_i8(CUtensorMap *map, const void *ptr, int64_t rows, int64_t co
   return true;
 }
 
+// 2-D f16 tensor map: rows x cols, row stride ld elements, 128-byte swizzle.
+bool jf_make_tmap_f16(CUtensorMap *map, const void *ptr, int64_t rows, int64_t cols, int64_t ld,
+                      int box_cols, int box_rows) {
+  auto enc = get_encode();
+  if (!enc) {
+    jf_set_error("cuTensorMapEncodeTiled unavailable");
+    return false;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void *>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    snprintf(g_err, sizeof(g_err), "cuTensorMapEncodeTiled(f16) failed (%d) rows=%lld cols=%lld", (int)r,
+             (long long)rows, (long long)cols);
+    return false;
+  }
+  return true;
+}
+
 // 2-D fp32 tensor map (scale grids): rows x cols, row stride ld elements, no swizzle.
 bool jf_make_tmap_f32(CUtensorMap *map, const void *ptr, int64_t rows, int64_t cols, int64_t ld,
                       int box_cols, int box_rows) {

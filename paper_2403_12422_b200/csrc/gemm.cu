@@ -577,6 +577,228 @@ __global__ void __launch_bounds__((2 + 16) * 32, 1)
   if (warp == 1) tmem_dealloc(tmem, kTmemBufs * BN);
 }
 
+// ─────────────── gemm_f16s_kernel: f16-widened codes, kind::f16 MMA ───────────────
+// Same pipeline, scale staging and promotion as gemm_i8s_kernel (K-major A and
+// B), but the operands are the int8 codes widened to f16 in HBM
+// (jf_widen_codes): the f32 accumulator of the kind::f16 MMA holds the exact
+// integer partial (every product and partial sum is an integer below 2^20),
+// so the promotion skips the 32 I2F per chunk -- the kernel's issue-slot
+// bottleneck.  Bit-identical to the int8 kernels.  A stage (128 K) is two
+// 64-wide SW128 boxes per operand; a 32-deep chunk is two K=16 MMAs.
+constexpr int kStagesF = 3;
+constexpr uint32_t kBoxBytesF = 128 * 128;         // 128 rows x 64 f16
+constexpr uint32_t kStageBytesF = 2 * kBoxBytesF;  // per operand
+constexpr size_t kSmemBytesF = 1024 + kStagesF * 2 * kStageBytesF + kStagesF * kScaleBytes + sizeof(SmemS) + 64;
+
+template <bool kFast>
+__global__ void __launch_bounds__((2 + 16) * 32, 1)
+    gemm_f16s_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ CUtensorMap tmSA, const __grid_constant__ CUtensorMap tmSB,
+                     const Params p, const int saT, const int sbT) {
+  constexpr int kEpi = 16;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *base = reinterpret_cast<uint8_t *>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *sA = base;
+  uint8_t *sB = base + kStagesF * kStageBytesF;
+  uint8_t *sS = sB + kStagesF * kStageBytesF;
+  SmemS &S = *reinterpret_cast<SmemS *>(sS + kStagesF * kScaleBytes);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t mt = p.M / BM, nt = p.N / BN;
+  const int64_t ntiles = mt * nt;
+  const int nstages_k = (int)(p.K / BK);
+  const uint32_t bar_full = smem_u32(&S.full[0]), bar_empty = smem_u32(&S.empty[0]);
+  const uint32_t bar_tfull = smem_u32(&S.tfull[0]), bar_tempty = smem_u32(&S.tempty[0]);
+
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+    prefetch_tmap(&tmSA);
+    prefetch_tmap(&tmSB);
+    for (int s = 0; s < kStagesF; ++s) {
+      mbar_init(&S.full[s], 1);
+      mbar_init(&S.empty[s], 1 + kEpi);
+    }
+    for (int b = 0; b < kTmemBufs; ++b) {
+      mbar_init(&S.tfull[b], 1);
+      mbar_init(&S.tempty[b], kEpi);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(&S.tmem_base, kTmemBufs * BN);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = S.tmem_base;
+
+  if (warp == 0) {
+    // ───────────── TMA producer: f16 tiles (2 boxes each) + scale sub-grids ─────────────
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int m0 = (int)((tile % mt) * BM), n0 = (int)((tile / mt) * BN);
+        for (int ks = 0; ks < nstages_k; ++ks) {
+          ctl_wait(p, bar_empty + 8 * stage, phase ^ 1);
+          mbar_arrive_expect_tx(&S.full[stage], 2 * kStageBytesF + 128);
+          uint8_t *a = sA + stage * kStageBytesF, *b = sB + stage * kStageBytesF;
+          tma_load_2d(a, &tmA, &S.full[stage], ks * BK, m0);
+          tma_load_2d(a + kBoxBytesF, &tmA, &S.full[stage], ks * BK + 64, m0);
+          tma_load_2d(b, &tmB, &S.full[stage], ks * BK, n0);
+          tma_load_2d(b + kBoxBytesF, &tmB, &S.full[stage], ks * BK + 64, n0);
+          uint8_t *ss = sS + stage * kScaleBytes;
+          if (saT) tma_load_2d(ss, &tmSA, &S.full[stage], m0 / 32, ks * 4);
+          else tma_load_2d(ss, &tmSA, &S.full[stage], ks * 4, m0 / 32);
+          if (sbT) tma_load_2d(ss + 128, &tmSB, &S.full[stage], n0 / 32, ks * 4);
+          else tma_load_2d(ss + 128, &tmSB, &S.full[stage], ks * 4, n0 / 32);
+          if (++stage == kStagesF) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ───────────── MMA issuer: chunk c -> TMEM buffer c, two K=16 MMAs ─────────────
+    if (lane == 0) {
+      const uint64_t adesc0 = smem_desc_sw128(smem_u32(sA), 16, 1024);
+      const uint64_t bdesc0 = smem_desc_sw128(smem_u32(sB), 16, 1024);
+      constexpr uint32_t idesc = idesc_f16_f32(BM, BN);
+      int stage = 0;
+      uint32_t phase = 0, tphase = 0;
+      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        for (int ks = 0; ks < nstages_k; ++ks) {
+          ctl_wait(p, bar_full + 8 * stage, phase);
+          tc_fence_after();
+          const uint64_t ad = adesc0 + (uint64_t)((stage * kStageBytesF) >> 4);
+          const uint64_t bd = bdesc0 + (uint64_t)((stage * kStageBytesF) >> 4);
+#pragma unroll
+          for (int c = 0; c < kChunksPerStage; ++c) {
+            ctl_wait(p, bar_tempty + 8 * c, ((tphase >> c) & 1) ^ 1);
+            tphase ^= 1u << c;
+            tc_fence_after();
+            // chunk c: box c/2, byte offset (c%2)*64 in the 128-byte row; K=16 step = 32 bytes
+            const uint32_t off = ((c >> 1) * kBoxBytesF + (c & 1) * 64) >> 4;
+            mma_f16_ss(tmem + c * BN, ad + off, bd + off, idesc, 0u);
+            mma_f16_ss(tmem + c * BN, ad + off + 2, bd + off + 2, idesc, 1u);
+            mma_commit(&S.tfull[c]);
+          }
+          mma_commit(&S.empty[stage]);
+          if (++stage == kStagesF) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else {
+    // ───────────── promotion + epilogue (as gemm_i8s_kernel, f32 partials) ─────────────
+    const int lq = warp & 3;
+    const int cg = (warp - 2) >> 2;
+    const uint32_t tcol = tmem + ((uint32_t)(lq * 32) << 16) + cg * 32;
+    const uint32_t ssa0 = smem_u32(sS), ssb0 = ssa0 + 128;
+    const uint32_t oa = saT ? (uint32_t)lq * 4 : (uint32_t)lq * 16;
+    const uint32_t ob = sbT ? (uint32_t)cg * 4 : (uint32_t)cg * 16;
+    const uint32_t da = saT ? 16 : 4, db = sbT ? 16 : 4;
+    uint32_t tphase = 0;
+    int flags = 0;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const int64_t I = (tile % mt) * (BM / 32) + lq;
+      const int64_t J = (tile / mt) * (BN / 32) + cg;
+      float acc[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) acc[j] = 0.0f;
+      for (int ks = 0; ks < nstages_k; ++ks) {
+        mbar_wait_u32(bar_full + 8 * stage, phase);
+        const uint32_t sa_addr = ssa0 + stage * kScaleBytes + oa, sb_addr = ssb0 + stage * kScaleBytes + ob;
+        float sav[4], sbv[4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          sav[b] = lds_f32(sa_addr + b * da);
+          sbv[b] = lds_f32(sb_addr + b * db);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive_u32(bar_empty + 8 * stage);
+        if (++stage == kStagesF) {
+          stage = 0;
+          phase ^= 1;
+        }
+#pragma unroll
+        for (int b = 0; b < kTmemBufs; ++b) {
+          mbar_wait_u32(bar_tfull + 8 * b, (tphase >> b) & 1);
+          tphase ^= 1u << b;
+          tc_fence_after();
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tcol + b * BN, r);
+          tmem_wait_ld();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_u32(bar_tempty + 8 * b);
+          promote32f<kFast>(acc, r, sav[b], sbv[b], p.zero);
+        }
+      }
+      flags |= finish_block(p, acc, I, J, lane);
+    }
+    if (lane == 0) raise_flags(p.err, flags);
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, kTmemBufs * BN);
+}
+
+// int8 codes -> f16 (exact), 16 codes per thread.
+__global__ void widen_codes_kernel(const int8_t *__restrict__ x, __half *__restrict__ y, int64_t n16) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n16) return;
+  const int4 v = reinterpret_cast<const int4 *>(x)[i];
+  uint32_t o[8];
+  i8x4_to_f16x4((uint32_t)v.x, o[0], o[1]);
+  i8x4_to_f16x4((uint32_t)v.y, o[2], o[3]);
+  i8x4_to_f16x4((uint32_t)v.z, o[4], o[5]);
+  i8x4_to_f16x4((uint32_t)v.w, o[6], o[7]);
+  int4 *d = reinterpret_cast<int4 *>(y) + 2 * i;
+  d[0] = make_int4((int)o[0], (int)o[1], (int)o[2], (int)o[3]);
+  d[1] = make_int4((int)o[4], (int)o[5], (int)o[6], (int)o[7]);
+}
+
+// int8 codes [rows x cols] -> f16 transposed [cols x rows]; 64 x 64 tiles via shared memory.
+__global__ void __launch_bounds__(256) widen_codes_t_kernel(const int8_t *__restrict__ x, __half *__restrict__ y,
+                                                            int64_t rows, int64_t cols) {
+  __shared__ uint8_t t[64][64 + 4];
+  const int64_t r0 = (int64_t)blockIdx.y * 64, c0 = (int64_t)blockIdx.x * 64;
+  {
+    const int r = threadIdx.x >> 2, seg = threadIdx.x & 3;  // 64 rows x 4 segments of 16 bytes
+    const int4 v = *reinterpret_cast<const int4 *>(x + (r0 + r) * cols + c0 + seg * 16);
+    uint32_t *d = reinterpret_cast<uint32_t *>(&t[r][seg * 16]);
+    d[0] = (uint32_t)v.x;
+    d[1] = (uint32_t)v.y;
+    d[2] = (uint32_t)v.z;
+    d[3] = (uint32_t)v.w;
+  }
+  __syncthreads();
+  const int oc = threadIdx.x >> 2, seg = threadIdx.x & 3;  // output row oc (= input column), 16 codes
+  uint32_t w[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int rr = seg * 16 + q * 4;
+    w[q] = (uint32_t)t[rr][oc] | ((uint32_t)t[rr + 1][oc] << 8) | ((uint32_t)t[rr + 2][oc] << 16) |
+           ((uint32_t)t[rr + 3][oc] << 24);
+  }
+  uint32_t o[8];
+  i8x4_to_f16x4(w[0], o[0], o[1]);
+  i8x4_to_f16x4(w[1], o[2], o[3]);
+  i8x4_to_f16x4(w[2], o[4], o[5]);
+  i8x4_to_f16x4(w[3], o[6], o[7]);
+  int4 *d = reinterpret_cast<int4 *>(y + (c0 + oc) * rows + r0 + seg * 16);
+  d[0] = make_int4((int)o[0], (int)o[1], (int)o[2], (int)o[3]);
+  d[1] = make_int4((int)o[4], (int)o[5], (int)o[6], (int)o[7]);
+}
+
 #ifdef JF_GEMM_TRACE
 #define JF_TR(ev, i)                                                                        \
   do {                                                                                      \
@@ -855,6 +1077,8 @@ bool jf_make_tmap_i8(CUtensorMap *map, const void *ptr, int64_t rows, int64_t co
                      int box_cols, int box_rows, bool swizzle128);
 bool jf_make_tmap_f32(CUtensorMap *map, const void *ptr, int64_t rows, int64_t cols, int64_t ld,
                       int box_cols, int box_rows);
+bool jf_make_tmap_f16(CUtensorMap *map, const void *ptr, int64_t rows, int64_t cols, int64_t ld,
+                      int box_cols, int box_rows);
 
 #ifdef JF_GEMM_TRACE
 static long long *g_trace = nullptr;
@@ -1111,4 +1335,62 @@ extern "C" int jf_gemm_partials(const int8_t *a, const int8_t *bt, int64_t m, in
   return jf_gemm_launch(a + kblk * 32, k, bt + kblk * 32, k, m, n, 32, nullptr, 0, 0, nullptr, 0,
                         0, nullptr, JF_MODE_EXACT, jf::gemm::OUT_I32, nullptr, nullptr, out,
                         nullptr, (cudaStream_t)stream);
+}
+
+// ─────────────── f16-widened operand path (C ABI) ───────────────
+
+extern "C" int jf_widen_codes(const int8_t *x, int64_t rows, int64_t cols, uint16_t *y, int32_t transpose,
+                              jf_stream_t stream) {
+  using namespace jf::gemm;
+  if (rows <= 0 || cols <= 0 || rows % 64 || cols % 64 || (uintptr_t)x % 16 || (uintptr_t)y % 16) {
+    jf_set_error("widen_codes: rows/cols must be positive multiples of 64, pointers 16-byte aligned");
+    return JF_ERR_ARG;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  if (transpose) {
+    widen_codes_t_kernel<<<dim3((unsigned)(cols / 64), (unsigned)(rows / 64)), 256, 0, s>>>(
+        x, reinterpret_cast<__half *>(y), rows, cols);
+  } else {
+    const int64_t n16 = rows * cols / 16;
+    widen_codes_kernel<<<(unsigned)((n16 + 255) / 256), 256, 0, s>>>(x, reinterpret_cast<__half *>(y), n16);
+  }
+  return jf_launch_check("widen_codes");
+}
+
+extern "C" int jf_gemm_f16(const uint16_t *a, const float *sa, int64_t sa_s0, int64_t sa_s1, const uint16_t *b,
+                           const float *sb, int64_t sb_s0, int64_t sb_s1, const float *bias, int64_t m, int64_t n,
+                           int64_t k, int32_t mode, int32_t out_kind, int8_t *yq, float *ys, float *yf,
+                           int32_t *err, jf_stream_t stream) {
+  using namespace jf::gemm;
+  auto grid_ok = [](const float *s, int64_t s0, int64_t s1) {
+    return ((uintptr_t)s % 16 == 0) && ((s1 == 1 && s0 % 4 == 0) || (s0 == 1 && s1 % 4 == 0));
+  };
+  if (m <= 0 || n <= 0 || k <= 0 || m % 128 || n % 128 || k % 128 || (uintptr_t)a % 16 || (uintptr_t)b % 16 ||
+      !grid_ok(sa, sa_s0, sa_s1) || !grid_ok(sb, sb_s0, sb_s1) || out_kind == OUT_I32) {
+    jf_set_error("gemm_f16: dims must be multiples of 128, scale grids contiguous along one axis");
+    return JF_ERR_ARG;
+  }
+  const int64_t kb = k / 32;
+  const int saT = sa_s1 != 1, sbT = sb_s1 != 1;
+  CUtensorMap ta, tb, tsa, tsb;
+  const bool ok = jf_make_tmap_f16(&ta, a, m, k, k, 64, BM) && jf_make_tmap_f16(&tb, b, n, k, k, 64, BN) &&
+                  (saT ? jf_make_tmap_f32(&tsa, sa, kb, m / 32, sa_s1, 4, 4)
+                       : jf_make_tmap_f32(&tsa, sa, m / 32, kb, sa_s0, 4, 4)) &&
+                  (sbT ? jf_make_tmap_f32(&tsb, sb, kb, n / 32, sb_s1, 4, 4)
+                       : jf_make_tmap_f32(&tsb, sb, n / 32, kb, sb_s0, 4, 4));
+  if (!ok) return JF_ERR_LAUNCH;
+  Params p{m, n, k, sa, sa_s0, sa_s1, sb, sb_s0, sb_s1, bias, yq, ys, yf, err, out_kind, 0.0f, nullptr,
+           g_opt.ctl_kind, (uint32_t)g_opt.ctl_ns};
+  const bool fast = mode == JF_MODE_FAST;
+  auto kf = fast ? gemm_f16s_kernel<true> : gemm_f16s_kernel<false>;
+  static bool done[2] = {};
+  if (!done[fast]) {
+    if (cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytesF) != cudaSuccess)
+      return jf_launch_check("gemm_f16s attr");
+    done[fast] = true;
+  }
+  const int64_t tiles = (m / BM) * (n / BN);
+  const int grid = (int)(tiles < jf_num_sms() ? tiles : jf_num_sms());
+  kf<<<grid, 18 * 32, kSmemBytesF, (cudaStream_t)stream>>>(ta, tb, tsa, tsb, p, saT, sbT);
+  return jf_launch_check("gemm_f16s");
 }

@@ -233,7 +233,7 @@ class AdamW:
                                                self.v[key].data_ptr(), n, c, self.lr, b1, b2, self.eps, wd,
                                                bc1, bc2, wq.values.data_ptr(), wq.scales.data_ptr(),
                                                _rt.err_ptr(), st), "adamw_quantize")
-                lin._weight_q, lin._weight_qt = wq, None
+                lin.set_weight_q(wq)
             else:
                 _lib.check(L.jf_adamw(p.data_ptr(), g.data_ptr(), self.m[key].data_ptr(), self.v[key].data_ptr(),
                                       p.numel(), self.lr, b1, b2, self.eps, wd, bc1, bc2, st), "adamw")

@@ -217,8 +217,12 @@ def _prep(mode, quantize, out):
 def block_mm_forward(xq: BlockQuantTensor, wq: BlockQuantTensor, cfg: TileConfig | None = None,
                      mode: ExecMode = ExecMode.INT8_DATA_FLOW, counters: AccessCounters | None = None,
                      *, bias=None, threads: int = 1, quantize: bool = True,
-                     promotion: str | None = None, out: str | None = None):
-    """Y = X W^T (+bias) for X [N x C], W [D x C] — kernel K3 (qgemm.py:282-309)."""
+                     promotion: str | None = None, out: str | None = None,
+                     w16: torch.Tensor | None = None):
+    """Y = X W^T (+bias) for X [N x C], W [D x C] — kernel K3 (qgemm.py:282-309).
+
+    ``w16`` (optional): W's f16-widened codes, cached by QuantLinear for the f16 operand path.
+    """
     if xq.cols != wq.cols:
         raise ValueError(f"inner dims differ: X is {xq.shape}, W is {wq.shape}")
     if xq.block != wq.block:
@@ -232,12 +236,42 @@ def block_mm_forward(xq: BlockQuantTensor, wq: BlockQuantTensor, cfg: TileConfig
         bias = bias if isinstance(bias, torch.Tensor) else torch.as_tensor(np.asarray(bias))
         bias = bias.to(device=xq.device, dtype=torch.float32).contiguous()
     yq, yf = _outputs(xq.rows, wq.rows, xq.device, out)
+    n, c, d = xq.rows, xq.cols, wq.rows
+    if f16_ok(n, c, d):
+        b16 = w16 if w16 is not None else widen_codes(wq.values)
+        _lib.check(_gemm_f16("fwd", widen_codes(xq.values), xq.scales, (c // 32, 1), b16, wq.scales, (c // 32, 1),
+                             bias, n, d, c, promotion, out, yq, yf), "gemm_f16")
+        return _finish(yq, yf, mode, out)
     _lib.check(_timed("fwd", 2 * xq.rows * xq.cols * wq.rows, lambda: L.jf_gemm_fwd(
         xq.values.data_ptr(), xq.scales.data_ptr(), wq.values.data_ptr(), wq.scales.data_ptr(),
         _lib.ptr(bias), xq.rows, xq.cols, wq.rows, _rt.promotion_code(promotion), _OUT_KIND[out],
         _lib.ptr(yq and yq.values), _lib.ptr(yq and yq.scales), _lib.ptr(yf), _rt.err_ptr(),
         _lib.stream_handle())), "gemm_fwd")
     return _finish(yq, yf, mode, out)
+
+
+def f16_ok(*dims: int) -> bool:
+    """True when the f16-widened operand path applies (runtime.set_gemm_operands('f16') and
+    every dim a multiple of 128)."""
+    return _rt.gemm_operands() == "f16" and all(d % 128 == 0 for d in dims)
+
+
+def widen_codes(values: torch.Tensor, transpose: bool = False) -> torch.Tensor:
+    """f16 copy of int8 codes (exact), optionally transposed (libjetfire jf_widen_codes)."""
+    L = _lib.lib()
+    rows, cols = values.shape
+    out = torch.empty((cols, rows) if transpose else (rows, cols), dtype=torch.float16, device=values.device)
+    _lib.check(L.jf_widen_codes(values.data_ptr(), rows, cols, out.data_ptr(), int(transpose),
+                                _lib.stream_handle()), "widen_codes")
+    return out
+
+
+def _gemm_f16(kind, a16, sa, sa_st, b16, sb, sb_st, bias, m, n, k, promotion, out, yq, yf):
+    L = _lib.lib()
+    return _timed(kind, 2 * m * n * k, lambda: L.jf_gemm_f16(
+        a16.data_ptr(), sa.data_ptr(), sa_st[0], sa_st[1], b16.data_ptr(), sb.data_ptr(), sb_st[0], sb_st[1],
+        _lib.ptr(bias), m, n, k, _rt.promotion_code(promotion), _OUT_KIND[out], _lib.ptr(yq and yq.values),
+        _lib.ptr(yq and yq.scales), _lib.ptr(yf), _rt.err_ptr(), _lib.stream_handle()))
 
 
 def mn_major_ok(*dims: int) -> bool:
@@ -250,11 +284,13 @@ def block_mm_grad_input(dyq: BlockQuantTensor, wq: BlockQuantTensor, cfg: TileCo
                         mode: ExecMode = ExecMode.INT8_DATA_FLOW,
                         counters: AccessCounters | None = None, *, threads: int = 1,
                         quantize: bool = True, promotion: str | None = None,
-                        out: str | None = None, wt: BlockQuantTensor | None = None):
+                        out: str | None = None, wt: BlockQuantTensor | None = None,
+                        w16t: torch.Tensor | None = None):
     """dX = dY W for dY [N x D], W [D x C] — kernel K4 (qgemm.py:312-333).
 
     ``wt`` (optional) is W's transposed codes, cached by QuantLinear so the
-    kernel never re-transposes a weight between updates.
+    kernel never re-transposes a weight between updates; ``w16t`` the same
+    for the f16 operand path (W^T widened to f16).
     """
     if dyq.cols != wq.rows:
         raise ValueError(f"inner dims differ: dY is {dyq.shape}, W is {wq.shape}")
@@ -266,9 +302,15 @@ def block_mm_grad_input(dyq: BlockQuantTensor, wq: BlockQuantTensor, cfg: TileCo
         _count_call(counters, dyq.rows, dyq.cols, wq.cols, cfg, mode, quantize)
     L = _lib.lib()
     n, d, c = dyq.rows, dyq.cols, wq.cols
+    yq, yf = _outputs(n, c, dyq.device, out)
+    if f16_ok(n, d, c):
+        # A = dY [n x d] (K = d); B = W^T [c x d], grid element (J, ci) = W.scales[ci, J]
+        b16 = w16t if w16t is not None else widen_codes(wq.values, transpose=True)
+        _lib.check(_gemm_f16("dgrad", widen_codes(dyq.values), dyq.scales, (d // 32, 1), b16, wq.scales,
+                             (1, c // 32), None, n, c, d, promotion, out, yq, yf), "gemm_f16")
+        return _finish(yq, yf, mode, out)
     if wt is None and not mn_major_ok(n, d, c):
         wt = wq.transposed()
-    yq, yf = _outputs(n, c, dyq.device, out)
     _lib.check(_timed("dgrad", 2 * n * d * c, lambda: L.jf_gemm_dgrad(
         dyq.values.data_ptr(), dyq.scales.data_ptr(), wq.values.data_ptr(), wq.scales.data_ptr(),
         _lib.ptr(wt and wt.values), _lib.ptr(wt and wt.scales), n, d, c,
@@ -294,6 +336,13 @@ def block_mm_grad_weight(dyq: BlockQuantTensor, xq: BlockQuantTensor, cfg: TileC
         _count_call(counters, dyq.cols, dyq.rows, xq.cols, cfg, mode, quantize)
     L = _lib.lib()
     n, d, c = dyq.rows, dyq.cols, xq.cols
+    if f16_ok(n, d, c):
+        # A = dY^T [d x n] (K = n), grid (I, ci) = dY.scales[ci, I]; B = X^T [c x n] likewise
+        yq, yf = _outputs(d, c, dyq.device, out)
+        _lib.check(_gemm_f16("wgrad", widen_codes(dyq.values, transpose=True), dyq.scales, (1, d // 32),
+                             widen_codes(xq.values, transpose=True), xq.scales, (1, c // 32), None, d, c, n,
+                             promotion, out, yq, yf), "gemm_f16")
+        return _finish(yq, yf, mode, out)
     dyt = xt = None
     if not mn_major_ok(n, d, c):  # generic shapes: K(=tokens)-major transposed copies
         dyt = dyq.transposed()   # dY^T [d x n] (codes + grid)

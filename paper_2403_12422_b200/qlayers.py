@@ -23,7 +23,9 @@ from .qgemm import (
     block_mm_forward,
     block_mm_grad_input,
     block_mm_grad_weight,
+    f16_ok,
     mn_major_ok,
+    widen_codes,
 )
 from .qnonlinear import (
     DropoutState,
@@ -90,6 +92,7 @@ class QuantLinear:
         self.cfg = cfg
         self._weight_q: BlockQuantTensor | None = None
         self._weight_qt: BlockQuantTensor | None = None
+        self._weight_f16: list = [None, None]  # f16-widened W, W^T (f16 operand path)
         self.saved_input: BlockQuantTensor | None = None
 
     @classmethod
@@ -121,15 +124,31 @@ class QuantLinear:
             self._weight_qt = self.weight_q.transposed()
         return self._weight_qt
 
+    def weight_f16(self, n_tokens: int, transpose: bool = False):
+        """W (or W^T) widened to f16 for the f16 operand path, cached with weight_q; None
+        when that path does not apply to this shape."""
+        d, c = self.master_weight.shape
+        if not f16_ok(n_tokens, d, c):
+            return None
+        if self._weight_f16[transpose] is None:
+            self._weight_f16[transpose] = widen_codes(self.weight_q.values, transpose=transpose)
+        return self._weight_f16[transpose]
+
+    def set_weight_q(self, wq: BlockQuantTensor) -> None:
+        """Install freshly requantized codes (optimizer step); drops the derived copies."""
+        self.mark_updated()
+        self._weight_q = wq
+
     def mark_updated(self) -> None:
         self._weight_q = None
         self._weight_qt = None
+        self._weight_f16 = [None, None]
 
     def forward(self, xq: BlockQuantTensor, counters: AccessCounters | None = None,
                 threads: int = 1) -> BlockQuantTensor:
         self.saved_input = xq
         return block_mm_forward(xq, self.weight_q, cfg=self.cfg, counters=counters, bias=self.bias,
-                                threads=threads)
+                                threads=threads, w16=self.weight_f16(xq.rows))
 
     def backward(self, dyq: BlockQuantTensor, counters: AccessCounters | None = None,
                  threads: int = 1):
@@ -139,7 +158,7 @@ class QuantLinear:
         d, c = self.master_weight.shape
         wt = None if mn_major_ok(dyq.rows, d, c) else self.weight_qt  # W^T only for generic shapes
         dxq = block_mm_grad_input(dyq, self.weight_q, cfg=self.cfg, counters=counters,
-                                  threads=threads, wt=wt)
+                                  threads=threads, wt=wt, w16t=self.weight_f16(dyq.rows, transpose=True))
         _, dw = block_mm_grad_weight(dyq, self.saved_input, cfg=self.cfg, counters=counters,
                                      threads=threads, out="int8+deq")
         dbias = None if self.bias is None else column_sum(dyq)

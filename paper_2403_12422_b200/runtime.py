@@ -20,7 +20,7 @@ _MSG_NONFINITE = "input contains non-finite values"
 _MSG_OVERFLOW = "scale overflows the binary16 range; input magnitude too large"
 
 _state = threading.local()
-_config = {"error_check": "eager", "promotion": "exact"}
+_config = {"error_check": "eager", "promotion": "exact", "operands": "f16"}
 _gemm_options = {"tma_scales": 1}
 
 
@@ -58,6 +58,20 @@ def gemm_option(key: str) -> int | None:
 
 def get_promotion() -> str:
     return _config["promotion"]
+
+
+def set_gemm_operands(kind: str) -> None:
+    """GEMM operand path for shapes that are multiples of 128: 'int8' (tcgen05 kind::i8 on
+    the codes as stored) or 'f16' (codes widened to f16 -- exact -- and multiplied with
+    kind::f16, whose f32 partials need no int->float conversion in the promotion).  Both
+    are bit-identical; 'f16' (default) trades a widening pass per operand for a faster GEMM."""
+    if kind not in ("int8", "f16"):
+        raise ValueError(f"operands must be 'int8' or 'f16', got {kind!r}")
+    _config["operands"] = kind
+
+
+def gemm_operands() -> str:
+    return _config["operands"]
 
 
 def promotion_code(mode: str | None) -> int:

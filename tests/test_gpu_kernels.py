@@ -215,18 +215,92 @@ def test_gemm_paths_bit_identical(jf, promotion, shape):
                 jf.block_mm_grad_input(DY, W, promotion=promotion, wt=W.transposed()),
                 jf.block_mm_grad_weight(DY, X, promotion=promotion, out="int8+deq"),
                 jf.block_mm_grad_weight(DY, X, promotion=promotion, quantize=False))
+    prev = runtime.gemm_operands()
     try:
+        runtime.set_gemm_operands("int8")
         staged = run()
         runtime.set_gemm_option("tma_scales", 0)
         generic = run()
     finally:
         runtime.set_gemm_option("tma_scales", 1)
+        runtime.set_gemm_operands(prev)
     for other in (generic,):
         for a, b in ((staged[0], other[0]), (staged[1], other[1])):
             assert torch.equal(a.values, b.values) and torch.equal(a.scales, b.scales)
         assert torch.equal(staged[2][0].values, other[2][0].values)
         assert torch.equal(staged[2][1], other[2][1])
         assert torch.equal(staged[3], other[3])
+
+
+def test_widen_codes(jf):
+    from paper_2403_12422_b200.qgemm import widen_codes
+
+    rng = np.random.default_rng(3)
+    q = torch.from_numpy(rng.integers(-127, 128, size=(192, 320), dtype=np.int8)).cuda()
+    assert torch.equal(widen_codes(q), q.to(torch.float16))
+    assert torch.equal(widen_codes(q, transpose=True), q.t().contiguous().to(torch.float16))
+
+
+@pytest.mark.parametrize("promotion", ["exact", "fast"])
+@pytest.mark.parametrize("shape", [(256, 384, 512), (2048, 256, 2304)])
+def test_gemm_f16_operands_bit_identical(jf, promotion, shape):
+    """The f16-widened operand path (kind::f16 MMA, f32 partials) vs the int8 kernels: same
+    bits for fwd (+bias), dgrad and wgrad, every output kind."""
+    from paper_2403_12422_b200 import runtime
+
+    rng = np.random.default_rng(11)
+    n, c, d = shape
+    X = bqt(jf, *_rand_q(rng, (n, c)))
+    W = bqt(jf, *_rand_q(rng, (d, c), 1 / np.sqrt(c)))
+    DY = bqt(jf, *_rand_q(rng, (n, d), 0.1))
+    bias = cu((0.1 * rng.standard_normal(d)).astype(np.float32))
+
+    def run():
+        return (jf.block_mm_forward(X, W, bias=bias, promotion=promotion),
+                jf.block_mm_forward(X, W, promotion=promotion, quantize=False),
+                jf.block_mm_grad_input(DY, W, promotion=promotion),
+                jf.block_mm_grad_weight(DY, X, promotion=promotion, out="int8+deq"),
+                jf.block_mm_grad_weight(DY, X, promotion=promotion, quantize=False))
+    prev = runtime.gemm_operands()
+    try:
+        runtime.set_gemm_operands("int8")
+        ref = run()
+        runtime.set_gemm_operands("f16")
+        got = run()
+    finally:
+        runtime.set_gemm_operands(prev)
+    for a, b in ((ref[0], got[0]), (ref[2], got[2])):
+        assert torch.equal(a.values, b.values) and torch.equal(a.scales, b.scales)
+    assert torch.equal(ref[1], got[1])
+    assert torch.equal(ref[3][0].values, got[3][0].values) and torch.equal(ref[3][1], got[3][1])
+    assert torch.equal(ref[4], got[4])
+
+
+def test_quantlinear_f16_weight_cache(jf):
+    """QuantLinear caches the widened W / W^T and drops them on mark_updated / set_weight_q."""
+    from paper_2403_12422_b200 import runtime
+    from paper_2403_12422_b200.qlayers import QuantLinear
+
+    rng = np.random.default_rng(12)
+    lin = QuantLinear.initialize(rng, 256, 384)
+    x = jf.quantize_per_block(torch.from_numpy(rng.standard_normal((128, 384)).astype(np.float32)).cuda())
+    prev = runtime.gemm_operands()
+    try:
+        runtime.set_gemm_operands("int8")
+        ref = lin.forward(x)
+        runtime.set_gemm_operands("f16")
+        got = lin.forward(x)
+        assert lin._weight_f16[0] is not None
+        lin.master_weight.mul_(2.0)
+        lin.mark_updated()
+        assert lin._weight_f16 == [None, None]
+        got2 = lin.forward(x)
+        runtime.set_gemm_operands("int8")
+        ref2 = lin.forward(x)
+    finally:
+        runtime.set_gemm_operands(prev)
+    assert torch.equal(ref.values, got.values) and torch.equal(ref.scales, got.scales)
+    assert torch.equal(ref2.values, got2.values) and torch.equal(ref2.scales, got2.scales)
 
 
 def test_gemm_fast_mode_tolerance(jf):

@@ -23,7 +23,10 @@ SHAPES = {"qkv": (4096, 4096, 12288), "proj": (4096, 4096, 4096), "mlp1": (4096,
 def apply(cfg: str):
     for kv in filter(None, cfg.split(",")):
         k, v = kv.split("=")
-        jf.runtime.set_gemm_option(k, int(v))
+        if k == "operands":
+            jf.runtime.set_gemm_operands(v)
+        else:
+            jf.runtime.set_gemm_option(k, int(v))
 
 
 def main():

@@ -28,7 +28,7 @@ for s in $STEPS; do
         --log-file "$OUT/launches.csv" python bench.py --steps 1 --warmup 1 --no-bf16 --no-cpu \
         > "$OUT/launches.log" 2>&1 ;;
     ncu)
-      timeout 1200 ncu --set full --clock-control none --import-source on -k regex:gemm_i8 -s 4 -c 1 \
+      timeout 1200 ncu --set full --clock-control none --import-source on -k regex:gemm_ -s 4 -c 1 \
         -o "$OUT/gemm_full" -f python bench.py --steps 1 --warmup 1 --no-bf16 --no-cpu \
         > "$OUT/ncu_gemm.log" 2>&1
       timeout 900 ncu --set full --clock-control none --import-source on -k regex:gelu_bwd -s 1 -c 1 \
