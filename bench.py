@@ -58,7 +58,7 @@ def parse():
     ap.add_argument("--workload", default="block_h4096_s2048", choices=sorted(WORKLOADS))
     ap.add_argument("--batch", type=int, default=None, help="sequences per GPU")
     ap.add_argument("--promotion", default="exact", choices=["exact", "fast"])
-    ap.add_argument("--operands", default="f16", choices=["int8", "f16"],
+    ap.add_argument("--operands", default="auto", choices=["auto", "int8", "f16"],
                     help="GEMM operand path (runtime.set_gemm_operands); both bit-identical")
     ap.add_argument("--attn-dtype", default="bf16", choices=["bf16", "fp32"])
     ap.add_argument("--no-bf16", action="store_true", help="skip the cuBLAS BF16 block baseline")
@@ -401,14 +401,14 @@ def roofline(gemm_tops: float, promotion: str, clocks_mhz=None, operands: str = 
         why = "int32->fp32 conversion (I2FP, ALU pipe, half rate) per output element per chunk"
     traffic = None
     tr_src = None
-    key = "gemm_f16s_kernel" if operands == "f16" else "gemm_i8_kernel"
+    key = "gemm_f16s_kernel" if operands != "int8" else "gemm_i8_kernel"
     try:
         with open(os.path.join(ROOT, "profiles", "roofline_traffic.json")) as f:
             t = json.load(f)[key]
         traffic, tr_src = t["dram_bytes_per_launch"], t["launch"] + " (" + t["source"] + ")"
     except (OSError, KeyError, ValueError):
         pass
-    kname = ("gemm_f16s_kernel (tcgen05 kind::f16 on f16-widened int8 codes)" if operands == "f16"
+    kname = ("gemm_f16s_kernel (tcgen05 kind::f16 on f16-widened int8 codes)" if operands != "int8"
              else "gemm_i8s_kernel (tcgen05 kind::i8)")
     return {"kernel": kname, "bound": "tensor", "achieved": round(gemm_tops, 1),
             "peak": INT8_PEAK_TOPS, "unit": "TFLOP/s", "frac": round(gemm_tops / INT8_PEAK_TOPS, 4),

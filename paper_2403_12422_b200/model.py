@@ -153,7 +153,7 @@ class JetfireLM:
             loss = row_loss.sum()
             grads["head.w"] = (dl16.t() @ h16)[:v].float()
             dh = (dl16 @ w16).float()
-            grads["head.b"] = dl16[:, :v].float().sum(dim=0)
+            grads["head.b"] = dl16.sum(dim=0, dtype=torch.float32)[:v]  # fp32 accumulate, no fp32 copy
         else:
             logits = torch.addmm(self.params["head.b"], h, self.params["head.w"].t())
             logp = torch.log_softmax(logits, dim=1)

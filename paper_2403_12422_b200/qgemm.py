@@ -250,10 +250,14 @@ def block_mm_forward(xq: BlockQuantTensor, wq: BlockQuantTensor, cfg: TileConfig
     return _finish(yq, yf, mode, out)
 
 
-def f16_ok(*dims: int) -> bool:
-    """True when the f16-widened operand path applies (runtime.set_gemm_operands('f16') and
-    every dim a multiple of 128)."""
-    return _rt.gemm_operands() == "f16" and all(d % 128 == 0 for d in dims)
+def f16_ok(m: int, n: int, k: int) -> bool:
+    """True when the f16-widened operand path applies to an m x n x k GEMM
+    (runtime.set_gemm_operands: 'f16', or 'auto' and 2mnk >= runtime.F16_MIN_FLOP; every
+    dim a multiple of 128)."""
+    kind = _rt.gemm_operands()
+    if kind == "int8" or m % 128 or n % 128 or k % 128:
+        return False
+    return kind == "f16" or 2 * m * n * k >= _rt.F16_MIN_FLOP
 
 
 def widen_codes(values: torch.Tensor, transpose: bool = False) -> torch.Tensor:

@@ -20,7 +20,7 @@ _MSG_NONFINITE = "input contains non-finite values"
 _MSG_OVERFLOW = "scale overflows the binary16 range; input magnitude too large"
 
 _state = threading.local()
-_config = {"error_check": "eager", "promotion": "exact", "operands": "f16"}
+_config = {"error_check": "eager", "promotion": "exact", "operands": "auto"}
 _gemm_options = {"tma_scales": 1}
 
 
@@ -62,12 +62,18 @@ def get_promotion() -> str:
 
 def set_gemm_operands(kind: str) -> None:
     """GEMM operand path for shapes that are multiples of 128: 'int8' (tcgen05 kind::i8 on
-    the codes as stored) or 'f16' (codes widened to f16 -- exact -- and multiplied with
-    kind::f16, whose f32 partials need no int->float conversion in the promotion).  Both
-    are bit-identical; 'f16' (default) trades a widening pass per operand for a faster GEMM."""
-    if kind not in ("int8", "f16"):
-        raise ValueError(f"operands must be 'int8' or 'f16', got {kind!r}")
+    the codes as stored), 'f16' (codes widened to f16 -- exact -- and multiplied with
+    kind::f16, whose f32 partials need no int->float conversion in the promotion), or
+    'auto' (default: f16 for GEMMs of at least F16_MIN_FLOP, where the faster kernel
+    outweighs the widening passes; int8 below).  All are bit-identical."""
+    if kind not in ("int8", "f16", "auto"):
+        raise ValueError(f"operands must be 'int8', 'f16' or 'auto', got {kind!r}")
     _config["operands"] = kind
+
+
+# 'auto' threshold: measured on B200 -- 4096x12288x4096 and larger gain 7% with f16
+# operands, 4096^3 breaks even, the 8192x1024-wide GPT-2 GEMMs lose to the widening launches.
+F16_MIN_FLOP = 2 ** 38
 
 
 def gemm_operands() -> str:
