@@ -151,15 +151,33 @@ class QuantLinear:
                                 threads=threads, w16=self.weight_f16(xq.rows))
 
     def backward(self, dyq: BlockQuantTensor, counters: AccessCounters | None = None,
-                 threads: int = 1):
-        """(dX quantized, dW FP32 = deq(requant(dY^T X)), dbias FP32)."""
+                 threads: int = 1, defer_wgrad: bool = False):
+        """(dX quantized, dW FP32 = deq(requant(dY^T X)), dbias FP32).
+
+        ``defer_wgrad``: issue dW / dbias on the runtime side stream; the caller must
+        ``runtime.join_side_streams()`` before reading them (TransformerBlock does)."""
         if self.saved_input is None:
             raise RuntimeError("backward called before forward")
         d, c = self.master_weight.shape
         wt = None if mn_major_ok(dyq.rows, d, c) else self.weight_qt  # W^T only for generic shapes
         dxq = block_mm_grad_input(dyq, self.weight_q, cfg=self.cfg, counters=counters,
                                   threads=threads, wt=wt, w16t=self.weight_f16(dyq.rows, transpose=True))
-        _, dw = block_mm_grad_weight(dyq, self.saved_input, cfg=self.cfg, counters=counters,
+        x = self.saved_input
+        if defer_wgrad and counters is None:
+            # dW (+ dbias) on the side stream, joined by the caller (runtime.join_side_streams)
+            main = torch.cuda.current_stream()
+            side = _rt.side_stream(dyq.device)
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                _, dw = block_mm_grad_weight(dyq, x, cfg=self.cfg, threads=threads, out="int8+deq")
+                dbias = None if self.bias is None else column_sum(dyq)
+                ev = torch.cuda.Event()
+                ev.record(side)
+            for tsr in (dyq.values, dyq.scales, x.values, x.scales):
+                tsr.record_stream(side)
+            _rt.defer_join(ev, [dw, dbias])
+            return dxq, dw, dbias
+        _, dw = block_mm_grad_weight(dyq, x, cfg=self.cfg, counters=counters,
                                      threads=threads, out="int8+deq")
         dbias = None if self.bias is None else column_sum(dyq)
         return dxq, dw, dbias
@@ -373,26 +391,29 @@ class TransformerBlock:
         width = self.config.stats_width
 
         dm2 = dropout_backward(dyq, s.drop2, counters)
-        dg, dw_mlp2, db_mlp2 = self.mlp2.backward(dm2, counters, threads)
+        ov = _rt.overlap_wgrad()
+        dg, dw_mlp2, db_mlp2 = self.mlp2.backward(dm2, counters, threads, defer_wgrad=ov)
         dm1 = gelu_backward(s.m1, dg, counters)
-        dln2, dw_mlp1, db_mlp1 = self.mlp1.backward(dm1, counters, threads)
+        dln2, dw_mlp1, db_mlp1 = self.mlp1.backward(dm1, counters, threads, defer_wgrad=ov)
         dh_branch, dgamma2, dbeta2 = layernorm_backward(s.ctx2, dln2, self.ln2, counters)
         if grad_hook is not None:
+            _rt.join_side_streams()
             grad_hook({"mlp2.w": dw_mlp2, "mlp2.b": db_mlp2, "mlp1.w": dw_mlp1, "mlp1.b": db_mlp1,
                        "ln2.gamma": dgamma2, "ln2.beta": dbeta2},
                       ["mlp2.w", "mlp2.b", "mlp1.w", "mlp1.b", "ln2.gamma", "ln2.beta"])
         dh, _ = add_forward(dh_branch, dyq, width, counters)
 
         dproj = dropout_backward(dh, s.drop1, counters)
-        dattn_q, dw_proj, db_proj = self.proj.backward(dproj, counters, threads)
+        dattn_q, dw_proj, db_proj = self.proj.backward(dproj, counters, threads, defer_wgrad=ov)
         if self.attn.supports_q():
             dqkv_q = self.attn.backward_q(dattn_q, s.batch, s.seq)
         else:
             dqkv = self.attn.backward(dequantize(dattn_q, self.attn.dtype), s.batch, s.seq)
             dqkv_q = quantize_per_block(dqkv, self.config.block)
-        dln1, dw_qkv, db_qkv = self.qkv.backward(dqkv_q, counters, threads)
+        dln1, dw_qkv, db_qkv = self.qkv.backward(dqkv_q, counters, threads, defer_wgrad=ov)
         da1_branch, dgamma1, dbeta1 = layernorm_backward(s.ctx1, dln1, self.ln1, counters)
         dx, _ = add_forward(da1_branch, dh, width, counters)
+        _rt.join_side_streams()
 
         if grad_hook is not None:
             grad_hook({"proj.w": dw_proj, "proj.b": db_proj, "qkv.w": dw_qkv, "qkv.b": db_qkv,

@@ -80,6 +80,55 @@ def gemm_operands() -> str:
     return _config["operands"]
 
 
+# ── weight-gradient overlap ───────────────────────────────────────────────
+# dW = dY^T X does not feed the rest of backward, so TransformerBlock.backward
+# issues it on a side stream (QuantLinear.backward(defer_wgrad=True)): its tiles
+# fill the SMs the dgrad GEMM and the elementwise kernels leave idle (few-tile
+# GEMMs of 1024-wide models), and joins before publishing the gradients.
+# Bit-identical either way; on by default.
+_overlap = {"wgrad": True}
+_side_streams: dict = {}
+_pending: list = []
+
+
+def set_overlap_wgrad(flag: bool) -> None:
+    _overlap["wgrad"] = bool(flag)
+
+
+def overlap_wgrad() -> bool:
+    return _overlap["wgrad"]
+
+
+def side_stream(device) -> "torch.cuda.Stream":
+    import torch
+
+    key = torch.device(device).index
+    if key not in _side_streams:
+        _side_streams[key] = torch.cuda.Stream(device=device)
+    return _side_streams[key]
+
+
+def defer_join(event, outputs) -> None:
+    """Record side-stream work whose outputs the current stream must wait for."""
+    _pending.append((event, outputs))
+
+
+def join_side_streams() -> None:
+    """Make the current stream wait for all deferred side-stream work (and keep the
+    caching allocator from recycling its outputs while the current stream uses them)."""
+    if not _pending:
+        return
+    import torch
+
+    main = torch.cuda.current_stream()
+    for ev, outs in _pending:
+        main.wait_event(ev)
+        for t in outs:
+            if t is not None:
+                t.record_stream(main)
+    _pending.clear()
+
+
 def promotion_code(mode: str | None) -> int:
     m = mode or _config["promotion"]
     if m not in ("exact", "fast"):

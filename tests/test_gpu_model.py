@@ -66,6 +66,37 @@ def test_gpt2_shaped_step_runs(jf):
     assert losses[-1] < losses[0]  # same batch three times: the loss must drop
 
 
+@pytest.mark.parametrize("operands", ["int8", "f16"])
+def test_wgrad_overlap_bit_identical(jf, operands):
+    """Weight gradients on the side stream (runtime.set_overlap_wgrad) give the same bits as
+    the serial backward, for both GEMM operand paths, across two optimizer steps."""
+    from paper_2403_12422_b200 import runtime
+    from paper_2403_12422_b200.model import AdamW, JetfireLM, ModelConfig
+
+    cfg = ModelConfig(layers=2, c_model=256, heads=4, hidden=1024, vocab=512, max_seq=128, pos_emb=True,
+                      head_dtype="bf16", attn_dtype="bf16")
+    x = torch.randint(0, cfg.vocab, (2, 128), device="cuda")
+    y = torch.roll(x, -1, dims=1)
+    prev = runtime.gemm_operands()
+    runtime.set_gemm_operands(operands)
+    runs = []
+    try:
+        for overlap in (False, True):
+            runtime.set_overlap_wgrad(overlap)
+            model = JetfireLM(cfg, seed=3)
+            opt = AdamW(model, lr=1e-3, weight_decay=0.1)
+            for _ in range(2):
+                loss, grads = model.loss_and_grads(x, y)
+                opt.step(grads)
+            runs.append((float(loss), {k: g.clone() for k, g in grads.items()}))
+    finally:
+        runtime.set_overlap_wgrad(False)
+        runtime.set_gemm_operands(prev)
+    assert runs[0][0] == runs[1][0]
+    for k, g in runs[0][1].items():
+        assert torch.equal(g, runs[1][1][k]), k
+
+
 def test_training_state_roundtrip(jf, tmp_path):
     """save -> load into a fresh model resumes bit-identically (trainer.py:462-477, 526-536)."""
     from paper_2403_12422_b200.checkpoint import load_training_state, save_training_state
