@@ -52,7 +52,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 
 // 2-D int8 tensor map: rows x cols (cols contiguous, row stride ld bytes),
 // box box_rows x box_cols; 128-byte swizzle (box_cols must then be 128) or none.
-bool jf_make_tmap_i8(CUtensorMap *map, const void *ptr, int64_t rows, int64_t cols, int64_t ld,
+static bool jf_make_tmap_i8_encode(CUtensorMap *map, const void *ptr, int64_t rows, int64_t cols, int64_t ld,
                      int box_cols, int box_rows, bool swizzle128) {
   auto enc = get_encode();
   if (!enc) {
@@ -76,7 +76,7 @@ bool jf_make_tmap_i8(CUtensorMap *map, const void *ptr, int64_t rows, int64_t co
 }
 
 // 2-D f16 tensor map: rows x cols, row stride ld elements, 128-byte swizzle.
-bool jf_make_tmap_f16(CUtensorMap *map, const void *ptr, int64_t rows, int64_t cols, int64_t ld,
+static bool jf_make_tmap_f16_encode(CUtensorMap *map, const void *ptr, int64_t rows, int64_t cols, int64_t ld,
                       int box_cols, int box_rows) {
   auto enc = get_encode();
   if (!enc) {
@@ -99,7 +99,7 @@ bool jf_make_tmap_f16(CUtensorMap *map, const void *ptr, int64_t rows, int64_t c
 }
 
 // 2-D fp32 tensor map (scale grids): rows x cols, row stride ld elements, no swizzle.
-bool jf_make_tmap_f32(CUtensorMap *map, const void *ptr, int64_t rows, int64_t cols, int64_t ld,
+static bool jf_make_tmap_f32_encode(CUtensorMap *map, const void *ptr, int64_t rows, int64_t cols, int64_t ld,
                       int box_cols, int box_rows) {
   auto enc = get_encode();
   if (!enc) {
@@ -123,3 +123,72 @@ bool jf_make_tmap_f32(CUtensorMap *map, const void *ptr, int64_t rows, int64_t c
 extern "C" int jf_version(void) { return 1; }
 extern "C" const char *jf_last_error(void) { return g_err; }
 extern "C" int jf_sm_count(void) { return jf_num_sms(); }
+
+// ── tensor-map cache ───────────────────────────────────────────────────
+// cuTensorMapEncodeTiled costs microseconds of host time and every GEMM launch
+// needs four maps.  A map depends only on (address, dims, stride, box, kind),
+// so a reused allocation with the same shape gets a bit-identical map: cache
+// them (direct-mapped, 4096 entries).
+namespace {
+struct TmapKey {
+  const void *ptr;
+  int64_t rows, cols, ld;
+  int box_cols, box_rows, kind;
+  bool operator==(const TmapKey &o) const {
+    return ptr == o.ptr && rows == o.rows && cols == o.cols && ld == o.ld && box_cols == o.box_cols &&
+           box_rows == o.box_rows && kind == o.kind;
+  }
+};
+struct TmapEntry {
+  TmapKey key;
+  CUtensorMap map;
+  bool valid;
+};
+constexpr int kTmapCache = 4096;
+TmapEntry g_tmaps[kTmapCache];
+std::mutex g_tmap_mu;
+
+size_t tmap_slot(const TmapKey &k) {
+  uint64_t h = (uint64_t)(uintptr_t)k.ptr * 0x9E3779B97F4A7C15ull;
+  h ^= (uint64_t)k.rows * 0xC2B2AE3D27D4EB4Full + (uint64_t)k.cols * 0x165667B19E3779F9ull;
+  h ^= (uint64_t)k.ld * 0x27D4EB2F165667C5ull + (uint64_t)(k.box_cols * 131 + k.box_rows * 7 + k.kind);
+  return (size_t)((h ^ (h >> 29)) % kTmapCache);
+}
+
+template <typename F>
+bool cached_tmap(CUtensorMap *map, const TmapKey &k, F encode) {
+  const size_t s = tmap_slot(k);
+  {
+    std::lock_guard<std::mutex> lk(g_tmap_mu);
+    if (g_tmaps[s].valid && g_tmaps[s].key == k) {
+      *map = g_tmaps[s].map;
+      return true;
+    }
+  }
+  if (!encode(map)) return false;
+  std::lock_guard<std::mutex> lk(g_tmap_mu);
+  g_tmaps[s].key = k;
+  g_tmaps[s].map = *map;
+  g_tmaps[s].valid = true;
+  return true;
+}
+}  // namespace
+
+bool jf_make_tmap_i8(CUtensorMap *map, const void *ptr, int64_t rows, int64_t cols, int64_t ld, int box_cols,
+                     int box_rows, bool swizzle128) {
+  return cached_tmap(map, TmapKey{ptr, rows, cols, ld, box_cols, box_rows, swizzle128 ? 1 : 0}, [&](CUtensorMap *m) {
+    return jf_make_tmap_i8_encode(m, ptr, rows, cols, ld, box_cols, box_rows, swizzle128);
+  });
+}
+
+bool jf_make_tmap_f16(CUtensorMap *map, const void *ptr, int64_t rows, int64_t cols, int64_t ld, int box_cols,
+                      int box_rows) {
+  return cached_tmap(map, TmapKey{ptr, rows, cols, ld, box_cols, box_rows, 2},
+                     [&](CUtensorMap *m) { return jf_make_tmap_f16_encode(m, ptr, rows, cols, ld, box_cols, box_rows); });
+}
+
+bool jf_make_tmap_f32(CUtensorMap *map, const void *ptr, int64_t rows, int64_t cols, int64_t ld, int box_cols,
+                      int box_rows) {
+  return cached_tmap(map, TmapKey{ptr, rows, cols, ld, box_cols, box_rows, 3},
+                     [&](CUtensorMap *m) { return jf_make_tmap_f32_encode(m, ptr, rows, cols, ld, box_cols, box_rows); });
+}

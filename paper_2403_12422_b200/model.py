@@ -228,7 +228,11 @@ class AdamW:
             lin = self.qlin.get(key)
             if lin is not None:
                 n, c = p.shape
-                wq = empty_like_shape(n, c, p.device)
+                # the INT8 copy is rewritten in place (stable addresses: a captured CUDA graph
+                # of loss_and_grads keeps reading the live weights); derived copies go stale
+                wq = lin._weight_q
+                if wq is None:
+                    wq = empty_like_shape(n, c, p.device)
                 _lib.check(L.jf_adamw_quantize(p.data_ptr(), g.data_ptr(), self.m[key].data_ptr(),
                                                self.v[key].data_ptr(), n, c, self.lr, b1, b2, self.eps, wd,
                                                bc1, bc2, wq.values.data_ptr(), wq.scales.data_ptr(),
@@ -240,4 +244,48 @@ class AdamW:
         _rt.maybe_check()
 
 
-__all__ = ["AdamW", "JetfireLM", "ModelConfig"]
+class GraphedTrainStep:
+    """One training step with ``loss_and_grads`` replayed from a CUDA graph.
+
+    The model step issues ~900 small launches (GPT-2 medium: 24 blocks x ~37 kernels plus
+    embedding, head and loss); from Python that costs about as much host time as the GPU
+    needs to run them, so the step becomes launch-bound.  Captured once, the forward and
+    backward replay as one graph launch; AdamW stays eager (its step-dependent scalars are
+    kernel arguments).  Inputs are copied into static buffers; ``loss`` and the gradients
+    are the graph's static outputs.  AdamW rewrites the INT8 weight copies in place, so
+    the graph always reads the current weights.  Single process only (no grad hook).
+    """
+
+    def __init__(self, model: JetfireLM, opt: "AdamW", batch: int, seq: int, warmup: int = 2):
+        from . import runtime as _rt
+
+        dev = model.params["emb"].device
+        self.model, self.opt = model, opt
+        self.x = torch.zeros((batch, seq), dtype=torch.long, device=dev)
+        self.y = torch.zeros((batch, seq), dtype=torch.long, device=dev)
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):  # allocator / library warm-up outside the capture
+            for _ in range(warmup):
+                model.loss_and_grads(self.x, self.y)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        for blk in model.blocks:  # derived weight copies are then made inside the graph
+            blk.drop_derived_weights()
+        n0 = _lib.launch_count[0]
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.loss, self.grads = model.loss_and_grads(self.x, self.y)
+        self.kernels_per_replay = _lib.launch_count[0] - n0  # libjetfire kernels inside the graph
+        _rt.maybe_check()
+
+    def step(self, x: torch.Tensor, y: torch.Tensor) -> torch.Tensor:
+        self.x.copy_(x, non_blocking=True)
+        self.y.copy_(y, non_blocking=True)
+        self.graph.replay()
+        _lib.launch_count[0] += self.kernels_per_replay
+        self.opt.step(self.grads)
+        return self.loss
+
+
+__all__ = ["AdamW", "GraphedTrainStep", "JetfireLM", "ModelConfig"]

@@ -135,9 +135,15 @@ class QuantLinear:
         return self._weight_f16[transpose]
 
     def set_weight_q(self, wq: BlockQuantTensor) -> None:
-        """Install freshly requantized codes (optimizer step); drops the derived copies."""
-        self.mark_updated()
+        """Install freshly requantized codes (optimizer step; may be the same buffers,
+        rewritten in place); drops the derived copies."""
+        self.drop_derived()
         self._weight_q = wq
+
+    def drop_derived(self) -> None:
+        """Forget the copies derived from weight_q (W^T codes, f16-widened W / W^T)."""
+        self._weight_qt = None
+        self._weight_f16 = [None, None]
 
     def mark_updated(self) -> None:
         self._weight_q = None
@@ -173,8 +179,9 @@ class QuantLinear:
                 dbias = None if self.bias is None else column_sum(dyq)
                 ev = torch.cuda.Event()
                 ev.record(side)
-            for tsr in (dyq.values, dyq.scales, x.values, x.scales):
-                tsr.record_stream(side)
+            if not torch.cuda.is_current_stream_capturing():  # (graph capture: private pool)
+                for tsr in (dyq.values, dyq.scales, x.values, x.scales):
+                    tsr.record_stream(side)
             _rt.defer_join(ev, [dw, dbias])
             return dxq, dw, dbias
         _, dw = block_mm_grad_weight(dyq, x, cfg=self.cfg, counters=counters,
@@ -425,6 +432,10 @@ class TransformerBlock:
             "ln1.gamma": dgamma1, "ln1.beta": dbeta1, "ln2.gamma": dgamma2, "ln2.beta": dbeta2,
         }
         return dx, grads
+
+    def drop_derived_weights(self) -> None:
+        for lin in (self.qkv, self.proj, self.mlp1, self.mlp2):
+            lin.drop_derived()
 
     def saved_activation_bytes(self) -> int:
         if self._saved is None:

@@ -121,11 +121,13 @@ def join_side_streams() -> None:
     import torch
 
     main = torch.cuda.current_stream()
+    capturing = torch.cuda.is_current_stream_capturing()
     for ev, outs in _pending:
         main.wait_event(ev)
-        for t in outs:
-            if t is not None:
-                t.record_stream(main)
+        if not capturing:
+            for t in outs:
+                if t is not None:
+                    t.record_stream(main)
     _pending.clear()
 
 
@@ -147,8 +149,20 @@ def _word(device=None) -> torch.Tensor:
     return w
 
 
+_cur_dev = getattr(torch._C, "_cuda_getDevice", None) or torch.cuda.current_device
+
+
 def err_ptr() -> int:
-    return _word().data_ptr()
+    """Device address of this thread's error word on the current device (cached: this runs
+    once per kernel launch)."""
+    dev = _cur_dev()
+    ptrs = getattr(_state, "ptrs", None)
+    if ptrs is None:
+        ptrs = _state.ptrs = {}
+    p = ptrs.get(dev)
+    if p is None:
+        p = ptrs[dev] = _word(dev).data_ptr()
+    return p
 
 
 def check_errors() -> None:
@@ -163,5 +177,6 @@ def check_errors() -> None:
 
 
 def maybe_check() -> None:
-    if _config["error_check"] == "eager":
+    # (no host sync while a CUDA graph is being captured: the error word is read after replay)
+    if _config["error_check"] == "eager" and not torch.cuda.is_current_stream_capturing():
         check_errors()

@@ -97,6 +97,32 @@ def test_wgrad_overlap_bit_identical(jf, operands):
         assert torch.equal(g, runs[1][1][k]), k
 
 
+def test_graphed_train_step_bit_identical(jf):
+    """CUDA-graph replay of loss_and_grads + eager AdamW == the eager step, three steps,
+    fresh batches each step (loss, every gradient, every parameter)."""
+    from paper_2403_12422_b200.model import AdamW, GraphedTrainStep, JetfireLM, ModelConfig
+
+    cfg = ModelConfig(layers=2, c_model=256, heads=4, hidden=1024, vocab=512, max_seq=128, pos_emb=True,
+                      head_dtype="bf16", attn_dtype="bf16")
+    g = torch.Generator(device="cuda").manual_seed(7)
+    batches = [torch.randint(0, cfg.vocab, (2, 128), device="cuda", generator=g) for _ in range(3)]
+    eager = JetfireLM(cfg, seed=4)
+    oe = AdamW(eager, lr=1e-3, weight_decay=0.1)
+    graphed = JetfireLM(cfg, seed=4)
+    og = AdamW(graphed, lr=1e-3, weight_decay=0.1)
+    gs = GraphedTrainStep(graphed, og, 2, 128)
+    for x in batches:
+        y = torch.roll(x, -1, dims=1)
+        le, ge = eager.loss_and_grads(x, y)
+        oe.step(ge)
+        lg = gs.step(x, y)
+        assert float(le) == float(lg)
+        for k in ge:
+            assert torch.equal(ge[k], gs.grads[k]), k
+    for k, p in eager.params.items():
+        assert torch.equal(p, graphed.params[k]), k
+
+
 def test_training_state_roundtrip(jf, tmp_path):
     """save -> load into a fresh model resumes bit-identically (trainer.py:462-477, 526-536)."""
     from paper_2403_12422_b200.checkpoint import load_training_state, save_training_state
