@@ -17,6 +17,9 @@ from paper_2403_12422_b200.qgemm import transpose_codes  # noqa: E402
 SHAPES = {  # (N tokens, C in, D out) of the config-4 block at 4096 tokens
     "qkv": (4096, 4096, 12288), "proj": (4096, 4096, 4096), "mlp1": (4096, 4096, 16384),
     "mlp2": (4096, 16384, 4096),
+    # GPT-2 medium at 8192 tokens
+    "g2qkv": (8192, 1024, 3072), "g2proj": (8192, 1024, 1024), "g2mlp1": (8192, 1024, 4096),
+    "g2mlp2": (8192, 4096, 1024),
 }
 
 
@@ -31,12 +34,14 @@ def main():
     ap.add_argument("--modes", default="exact,fast")
     ap.add_argument("--shapes", default="mlp1,proj")
     ap.add_argument("--lib", default=None, help="alternative libjetfire build (A/B experiments)")
+    ap.add_argument("--operands", default="auto", choices=["auto", "int8", "f16"])
     a = ap.parse_args()
     if a.lib:
         from paper_2403_12422_b200 import _lib
         _lib.load_library(a.lib)
     jf.require_cuda()
     jf.set_error_check("deferred")
+    jf.runtime.set_gemm_operands(a.operands)
     for name in a.shapes.split(","):
         n, c, d = SHAPES[name]
         x, w, dy = rq((n, c)), rq((d, c), c ** -0.5), rq((n, d), 0.1)
