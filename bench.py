@@ -58,8 +58,9 @@ def parse(argv=None):
     ap.add_argument("--workload", default="block_h4096_s2048", choices=sorted(WORKLOADS))
     ap.add_argument("--batch", type=int, default=None, help="sequences per GPU")
     ap.add_argument("--promotion", default="exact", choices=["exact", "fast"])
-    ap.add_argument("--operands", default="auto", choices=["auto", "int8", "f16"],
-                    help="GEMM operand path (runtime.set_gemm_operands); both bit-identical")
+    ap.add_argument("--operands", default="int8", choices=["int8", "auto", "f16"],
+                    help="GEMM operand path (runtime.set_gemm_operands): int8 = tcgen05 kind::i8 (default); "
+                         "auto/f16 = opt-in f16-widened codes on kind::f16; all bit-identical")
     ap.add_argument("--overlap-wgrad", type=int, default=1, choices=[0, 1],
                     help="weight-gradient GEMMs on a side stream (runtime.set_overlap_wgrad)")
     ap.add_argument("--graph", type=int, default=1, choices=[0, 1],
@@ -459,9 +460,9 @@ def run_ours(args, world, rank, local):
     return out, wl, None, w
 
 
-def roofline(gemm_tops: float, promotion: str, clocks_mhz=None, operands: str = "f16") -> dict:
-    """Dominant kernel = the block GEMM (gemm_f16s_kernel on the default f16-widened
-    operand path, gemm_i8s_kernel with --operands int8; ~87% of the step).
+def roofline(gemm_tops: float, promotion: str, clocks_mhz=None, operands: str = "int8") -> dict:
+    """Dominant kernel = the block GEMM (gemm_i8s_kernel on the default int8 operand path,
+    gemm_f16s_kernel with the opt-in --operands auto/f16; ~87% of the step).
 
     peak: B200 dense INT8 (datasheet 4.5 POPS; our raw kind::i8 microbenchmark
     measures 8178 MAC/clk/SM = 4.76 POPS at 1965 MHz).  The binding bound under

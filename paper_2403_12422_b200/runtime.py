@@ -20,7 +20,7 @@ _MSG_NONFINITE = "input contains non-finite values"
 _MSG_OVERFLOW = "scale overflows the binary16 range; input magnitude too large"
 
 _state = threading.local()
-_config = {"error_check": "eager", "promotion": "exact", "operands": "auto"}
+_config = {"error_check": "eager", "promotion": "exact", "operands": "int8"}
 _gemm_options = {"tma_scales": 1}
 
 
@@ -61,11 +61,12 @@ def get_promotion() -> str:
 
 
 def set_gemm_operands(kind: str) -> None:
-    """GEMM operand path for shapes that are multiples of 128: 'int8' (tcgen05 kind::i8 on
-    the codes as stored), 'f16' (codes widened to f16 -- exact -- and multiplied with
-    kind::f16, whose f32 partials need no int->float conversion in the promotion), or
-    'auto' (default: f16 for GEMMs of at least F16_MIN_FLOP, where the faster kernel
-    outweighs the widening passes; int8 below).  All are bit-identical."""
+    """GEMM operand path for shapes that are multiples of 128: 'int8' (default: tcgen05
+    kind::i8 on the codes as stored, int32 TMEM partials -- the north-star design), 'f16'
+    (opt-in experiment: the codes widened to f16 -- exact -- and multiplied with
+    kind::f16, whose f32 partials need no int->float conversion in the promotion; the
+    widened copies are GEMM operand staging in HBM), or 'auto' (f16 for GEMMs of at least
+    F16_MIN_FLOP, int8 below).  All are bit-identical; DESIGN.md section 3 has the numbers."""
     if kind not in ("int8", "f16", "auto"):
         raise ValueError(f"operands must be 'int8', 'f16' or 'auto', got {kind!r}")
     _config["operands"] = kind

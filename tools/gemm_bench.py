@@ -34,7 +34,7 @@ def main():
     ap.add_argument("--modes", default="exact,fast")
     ap.add_argument("--shapes", default="mlp1,proj")
     ap.add_argument("--lib", default=None, help="alternative libjetfire build (A/B experiments)")
-    ap.add_argument("--operands", default="auto", choices=["auto", "int8", "f16"])
+    ap.add_argument("--operands", default="int8", choices=["auto", "int8", "f16"])
     a = ap.parse_args()
     if a.lib:
         from paper_2403_12422_b200 import _lib
