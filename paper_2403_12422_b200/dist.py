@@ -83,29 +83,47 @@ def _unpack(pending, grads, world):
 class OverlappedAllReduce:
     """All-reduce gradients group by group while backward continues.
 
-    Pass ``hook`` as ``JetfireLM.loss_and_grads(..., grad_hook=...)``: each call packs
-    the named FP32 gradients into one flat buffer and launches an async all-reduce (NCCL
-    runs on its own stream, so the transfer overlaps the next block's backward kernels);
-    ``finish(grads)`` waits, averages and unpacks.  Same sums as ``allreduce_mean``.
+    Pass ``hook`` as ``JetfireLM.loss_and_grads(..., grad_hook=...)``: each call launches
+    async all-reduces of the named FP32 gradients (NCCL runs on its own stream, so the
+    transfer overlaps the next block's backward kernels); ``finish(grads)`` waits and
+    averages.  Weight gradients (>= ``inplace_bytes``) are reduced in place -- no pack /
+    unpack copies of the hundreds of MB per block, and on NCCL the 1/world scaling rides
+    in the collective (ReduceOp.AVG); the small vectors (bias, gamma, beta) share one
+    packed buffer.  Same sums as ``allreduce_mean``.
     """
 
-    def __init__(self, group=None):
+    def __init__(self, group=None, inplace_bytes: int = 8 << 20):
         self.group = group
-        self.pending = []
+        self.inplace_bytes = inplace_bytes
+        self.avg = dist.get_backend(group) == "nccl"
+        self.pending = []   # packed buckets (work, names, flat)
+        self.inplace = []   # (work, tensor) reduced in place
 
     def hook(self, grads: dict, names) -> None:
         names = [k for k in names if grads.get(k) is not None]
-        if not names:
-            return
-        flat = torch.cat([grads[k].reshape(-1) for k in names])
-        work = dist.all_reduce(flat, group=self.group, async_op=True)
-        self.pending.append((work, names, flat))
+        small = []
+        for k in names:
+            g = grads[k]
+            if g.numel() * g.element_size() >= self.inplace_bytes and g.is_contiguous():
+                op = dist.ReduceOp.AVG if self.avg else dist.ReduceOp.SUM
+                self.inplace.append((dist.all_reduce(g, op=op, group=self.group, async_op=True), g))
+            else:
+                small.append(k)
+        if small:
+            flat = torch.cat([grads[k].reshape(-1) for k in small])
+            work = dist.all_reduce(flat, group=self.group, async_op=True)
+            self.pending.append((work, small, flat))
 
     def finish(self, grads: dict) -> None:
+        world = dist.get_world_size(self.group)
+        for work, g in self.inplace:
+            work.wait()
+            if not self.avg:
+                g.div_(world)
         for work, _, _ in self.pending:
             work.wait()
-        _unpack(self.pending, grads, dist.get_world_size(self.group))
-        self.pending = []
+        _unpack(self.pending, grads, world)
+        self.pending, self.inplace = [], []
 
 
 __all__ = ["OverlappedAllReduce", "allreduce_mean", "finish_allreduce", "shard_sequences"]

@@ -32,8 +32,8 @@ def _worker(rank, world, port, bucket_bytes, use_async, out):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         grads = _grads(rank)
-        if use_async == "overlap":  # groups as a model's backward releases them
-            ov = OverlappedAllReduce()
+        if use_async in ("overlap", "overlap_inplace"):  # groups as a model's backward releases them
+            ov = OverlappedAllReduce(inplace_bytes=1 if use_async == "overlap_inplace" else 8 << 20)
             ov.hook(grads, ["qkv.w", "qkv.b"])
             ov.hook(grads, ["proj.w", "proj.b"])
             ov.hook(grads, ["ln1.gamma", "ln1.beta"])
@@ -48,7 +48,7 @@ def _worker(rank, world, port, bucket_bytes, use_async, out):
 
 
 @pytest.mark.parametrize("bucket_bytes,use_async", [(64 << 20, False), (512, False), (512, True),
-                                                    (0, "overlap")])
+                                                    (0, "overlap"), (0, "overlap_inplace")])
 def test_allreduce_mean_world2(bucket_bytes, use_async):
     world = 2
     out = mp.Manager().dict()
