@@ -225,6 +225,108 @@ __global__ void __launch_bounds__(256) ln_bwd_rows_fast_kernel(LnRowArgs A, int 
   }
 }
 
+// Leaf-per-lane path (perfect tree, nleaf | 32, leaf_len % 16 == 0 -- every
+// hidden size used here).  The warp stages its rows' x and dY codes in shared
+// memory with coalesced 16-byte loads (leaf stride leaf_len + 16 bytes: the
+// leaf-per-lane 16-byte reads below are then bank-conflict free), then lane =
+// (row, leaf) keeps all 8 chains of its leaf in registers and walks the leaf
+// two chain elements per 16-byte read, in ascending order.  Leaf sum
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then an xor-butterfly over the row's
+// nleaf lanes: numpy's pairwise association exactly.
+__global__ void __launch_bounds__(256) ln_bwd_rows_leaf_kernel(LnRowArgs A, int nleaf, int leaf_len,
+                                                               float *m1, float *m2) {
+  extern __shared__ __align__(16) uint8_t lsm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rpw = 32 / nleaf;
+  const int stride = leaf_len + 16;                 // smem bytes per leaf
+  const int row_bytes = nleaf * stride;             // smem bytes per row and array
+  const int gstride = leaf_len + 4;                 // gamma: floats per leaf (padded)
+  float *gsm = reinterpret_cast<float *>(lsm);      // [nleaf][gstride]
+  uint8_t *wx = lsm + (size_t)nleaf * gstride * 4 + (size_t)warp * rpw * row_bytes * 2;
+  uint8_t *wd = wx + (size_t)rpw * row_bytes;
+  for (int q = threadIdx.x; q < (int)(A.c >> 2); q += blockDim.x) {  // gamma, once per CTA
+    const int e = q * 4, lf = e / leaf_len;
+    *reinterpret_cast<float4 *>(gsm + lf * gstride + (e - lf * leaf_len)) =
+        __ldg(reinterpret_cast<const float4 *>(A.gamma) + q);
+  }
+  const int64_t row0 = ((int64_t)blockIdx.x * 8 + warp) * rpw;
+  // stage: chunk q (16 bytes) of row r -> leaf (16q)/leaf_len, offset (16q)%leaf_len
+  const int chunks = (int)(A.c >> 4);
+  for (int r = 0; r < rpw; ++r) {
+    const int64_t row = row0 + r;
+    if (row >= A.n) break;
+    const uint4 *gx = reinterpret_cast<const uint4 *>(A.x + row * A.c);
+    const uint4 *gd = reinterpret_cast<const uint4 *>(A.dy + row * A.c);
+    for (int q = lane; q < chunks; q += 32) {
+      const int byte = q * 16, lf = byte / leaf_len;
+      const int off = r * row_bytes + lf * stride + (byte - lf * leaf_len);
+      *reinterpret_cast<uint4 *>(wx + off) = __ldg(gx + q);
+      *reinterpret_cast<uint4 *>(wd + off) = __ldg(gd + q);
+    }
+  }
+  __syncthreads();
+  const int lr = lane / nleaf, leaf = lane % nleaf;
+  const int64_t row = row0 + lr;
+  const bool valid = row < A.n;
+  float c1[8], c2[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) c1[j] = c2[j] = 0.f;
+  if (valid) {
+    const float mr = __ldg(A.mu + row), ir = __ldg(A.inv_std + row);
+    const int64_t cb = A.c >> 5;
+    const int64_t col0 = (int64_t)leaf * leaf_len;
+    const uint8_t *sx_ = wx + lr * row_bytes + leaf * stride;
+    const uint8_t *sd_ = wd + lr * row_bytes + leaf * stride;
+    const float *sxr = A.xs + (row >> 5) * cb;
+    const float *sdr = A.dys + (row >> 5) * cb;
+    for (int seg = 0; seg < leaf_len / 16; ++seg) {
+      const int64_t k0 = col0 + seg * 16;
+      const uint4 xq = *reinterpret_cast<const uint4 *>(sx_ + seg * 16);
+      const uint4 dq = *reinterpret_cast<const uint4 *>(sd_ + seg * 16);
+      const float sx = __ldg(sxr + (k0 >> 5)), sd = __ldg(sdr + (k0 >> 5));
+      float g[16];
+      const float *gl = gsm + leaf * gstride + seg * 16;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float4 g4 = *reinterpret_cast<const float4 *>(gl + 4 * q);
+        g[4 * q] = g4.x;
+        g[4 * q + 1] = g4.y;
+        g[4 * q + 2] = g4.z;
+        g[4 * q + 3] = g4.w;
+      }
+      const uint32_t xw[4] = {xq.x, xq.y, xq.z, xq.w}, dw[4] = {dq.x, dq.y, dq.z, dq.w};
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const float xv = __fmul_rn(code_at(xw[e >> 2], e & 3), sx);
+        const float dv = __fmul_rn(code_at(dw[e >> 2], e & 3), sd);
+        const float xh = __fmul_rn(__fsub_rn(xv, mr), ir);
+        const float dxh = __fmul_rn(dv, g[e]);
+        const float pr = __fmul_rn(dxh, xh);
+        const int j = e & 7;
+        if (seg == 0 && e < 8) {  // r[j] = a[j]: the chain starts at its first element
+          c1[j] = dxh;
+          c2[j] = pr;
+        } else {
+          c1[j] = __fadd_rn(c1[j], dxh);
+          c2[j] = __fadd_rn(c2[j], pr);
+        }
+      }
+    }
+  }
+  float s1 = __fadd_rn(__fadd_rn(__fadd_rn(c1[0], c1[1]), __fadd_rn(c1[2], c1[3])),
+                       __fadd_rn(__fadd_rn(c1[4], c1[5]), __fadd_rn(c1[6], c1[7])));
+  float s2 = __fadd_rn(__fadd_rn(__fadd_rn(c2[0], c2[1]), __fadd_rn(c2[2], c2[3])),
+                       __fadd_rn(__fadd_rn(c2[4], c2[5]), __fadd_rn(c2[6], c2[7])));
+  for (int o = 1; o < nleaf; o <<= 1) {
+    s1 = __fadd_rn(s1, __shfl_xor_sync(0xffffffffu, s1, o));
+    s2 = __fadd_rn(s2, __shfl_xor_sync(0xffffffffu, s2, o));
+  }
+  if (valid && leaf == 0) {
+    m1[row] = __fdiv_rn(s1, (float)A.c);
+    m2[row] = __fdiv_rn(s2, (float)A.c);
+  }
+}
+
 __global__ void __launch_bounds__(256) ln_bwd_rows_kernel(LnRowArgs A, int depth, int perfect,
                                                           float *m1, float *m2) {
   const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -644,6 +746,12 @@ static bool pw_equal_leaves(int64_t len, int depth) {
   return h == len - h && pw_equal_leaves(h, depth - 1);
 }
 
+// A/B switch for the leaf-per-lane row reduction (default on; JF_LN_LEAF=0 disables).
+static bool g_ln_leaf = [] {
+  const char *e = getenv("JF_LN_LEAF");
+  return !(e && e[0] == '0');
+}();
+
 extern "C" size_t jf_ln_bwd_workspace_bytes(int64_t n, int64_t c) {
   return (size_t)(2 * n + 2 * (n / 32) * c) * sizeof(float);
 }
@@ -663,7 +771,21 @@ extern "C" int jf_ln_bwd(const int8_t *x, const float *xs, const float *mu, cons
   const int64_t leaf_len = perfect ? (c >> depth) : 0;
   const bool fast = perfect && depth <= 7 && (leaf_len << depth) == c && leaf_len % 8 == 0 &&
                     pw_equal_leaves(c, depth) && ((1 << depth) <= 4 || true);
-  if (fast)
+  const int nleaf = 1 << depth;
+  const bool leafp = fast && nleaf <= 32 && leaf_len % 16 == 0 && ((uintptr_t)x % 16 == 0) &&
+                     ((uintptr_t)dy % 16 == 0) && ((uintptr_t)gamma % 16 == 0) && g_ln_leaf;
+  // staged rows: 8 warps x (32/nleaf) rows x 2 arrays x nleaf x (leaf_len + 16) bytes
+  const size_t leaf_smem = leafp ? (size_t)8 * 32 * 2 * (leaf_len + 16) + (size_t)nleaf * (leaf_len + 4) * 4 : 0;
+  if (leafp && leaf_smem <= 200 * 1024) {
+    static size_t attr = 0;
+    if (leaf_smem > 48 * 1024 && leaf_smem > attr) {
+      cudaFuncSetAttribute(ln_bwd_rows_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)leaf_smem);
+      attr = leaf_smem;
+    }
+    const int64_t rows_per_cta = 8 * (32 / nleaf);
+    ln_bwd_rows_leaf_kernel<<<(unsigned)((n + rows_per_cta - 1) / rows_per_cta), 256, leaf_smem, st>>>(
+        A, nleaf, (int)leaf_len, m1, m2);
+  } else if (fast)
     ln_bwd_rows_fast_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(A, 1 << depth, (int)leaf_len, m1, m2);
   else
     ln_bwd_rows_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(A, depth, perfect, m1, m2);
