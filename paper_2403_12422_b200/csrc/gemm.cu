@@ -548,6 +548,7 @@ __global__ void __launch_bounds__((2 + 16) * 32, 1)
       float acc[32];
 #pragma unroll
       for (int j = 0; j < 32; ++j) acc[j] = 0.0f;
+#pragma unroll 2
       for (int ks = 0; ks < nstages_k; ++ks) {
         // the stage's scales: acquire the TMA writes, read, release the stage
         mbar_wait_u32(bar_full + 8 * stage, phase);
