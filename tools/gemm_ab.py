@@ -1,9 +1,11 @@
 """Interleaved A/B timing of GEMM launch options in ONE process (diagnostics).
 
 python tools/gemm_ab.py --shape mlp1 --mode exact \
-    --configs "ctl_kind=0" "ctl_kind=1,ctl_ns=200" "issuers=3" --rounds 5
+    --configs "tma_scales=1" "tma_scales=0" "operands=f16" --rounds 5
 Each round times every config once (CUDA events, 10 launches after 2 warm-up);
-prints the median us/launch per config.  Options: jf_gemm_set_option keys.
+prints the median us/launch per config.  Options: jf_gemm_set_option keys (ctl_kind /
+ctl_ns only act in JF_CTL_RUNTIME builds), plus operands=int8|auto|f16.  --base is applied
+before every config so keys do not leak from one config into the next.
 """
 import argparse
 import json
