@@ -564,6 +564,22 @@ JF_DEV const float *gelu_row(const float *tab, float s) {
   return tab + ((int64_t)__half_as_ushort(__float2half_rn(s)) << 8) + 127;
 }
 
+// Copy the 8 table rows of this tile's 32x32 blocks (one per scale) into shared
+// memory with coalesced 16-byte loads; the per-element lookups then gather from
+// shared memory instead of L1 (a gather over up to 32 lines per warp load).
+JF_DEV void stage_gelu_rows(const TilePos &t, const float *__restrict__ gtab,
+                            const float *__restrict__ xs, float (*tab)[256]) {
+  const int b = threadIdx.x >> 5, q0 = (threadIdx.x & 31) * 8;
+  if (t.c0 + 32 * b < t.c) {
+    const float *row = gelu_row(gtab, __ldg(xs + t.scale_idx(t.r0, t.c0 + 32 * b))) - 127;
+    const float4 lo = __ldg(reinterpret_cast<const float4 *>(row + q0));
+    const float4 hi = __ldg(reinterpret_cast<const float4 *>(row + q0) + 1);
+    *reinterpret_cast<float4 *>(&tab[b][q0]) = lo;
+    *reinterpret_cast<float4 *>(&tab[b][q0 + 4]) = hi;
+  }
+  __syncthreads();
+}
+
 __global__ void __launch_bounds__(kTileThreads) gelu_fwd_kernel(const int8_t *__restrict__ x,
                                                                 const float *__restrict__ xs,
                                                                 int64_t n, int64_t c, int8_t *yq,
@@ -576,12 +592,13 @@ __global__ void __launch_bounds__(kTileThreads) gelu_fwd_kernel(const int8_t *__
     int k[4][8];
     float v[4][8];
     load_codes(t, x, k);
+    stage_gelu_rows(t, gtab, xs, tab);
     if (t.active) {
-      const float *tb = gelu_row(gtab, __ldg(xs + t.scale_idx(t.r0, t.col())));
+      const float *tb = tab[t.lane >> 2] + 127;
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) v[i][j] = __ldg(tb + k[i][j]);
+        for (int j = 0; j < 8; ++j) v[i][j] = tb[k[i][j]];
     }
     quant_store(t, v, yq, ys, red, err);
     return;
