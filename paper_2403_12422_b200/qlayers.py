@@ -179,10 +179,9 @@ class QuantLinear:
                 dbias = None if self.bias is None else column_sum(dyq)
                 ev = torch.cuda.Event()
                 ev.record(side)
-            if not torch.cuda.is_current_stream_capturing():  # (graph capture: private pool)
-                for tsr in (dyq.values, dyq.scales, x.values, x.scales):
-                    tsr.record_stream(side)
-            _rt.defer_join(ev, [dw, dbias])
+            # dY and X stay referenced until the join (no record_stream: the caching
+            # allocator's per-free event bookkeeping stalled the host)
+            _rt.defer_join(ev, [dw, dbias], keepalive=(dyq, x))
             return dxq, dw, dbias
         _, dw = block_mm_grad_weight(dyq, x, cfg=self.cfg, counters=counters,
                                      threads=threads, out="int8+deq")

@@ -109,26 +109,24 @@ def side_stream(device) -> "torch.cuda.Stream":
     return _side_streams[key]
 
 
-def defer_join(event, outputs) -> None:
-    """Record side-stream work whose outputs the current stream must wait for."""
-    _pending.append((event, outputs))
+def defer_join(event, outputs, keepalive=()) -> None:
+    """Record side-stream work the current stream must wait for.  ``keepalive``: inputs
+    the side stream reads -- referenced until the join, so the caching allocator cannot
+    hand their memory to new work before the side stream is done with it.  Outputs need
+    no bookkeeping: the side stream waits on the current stream before every new batch
+    of work, so a block the current stream freed is never still in use there."""
+    _pending.append((event, outputs, keepalive))
 
 
 def join_side_streams() -> None:
-    """Make the current stream wait for all deferred side-stream work (and keep the
-    caching allocator from recycling its outputs while the current stream uses them)."""
+    """Make the current stream wait for all deferred side-stream work."""
     if not _pending:
         return
     import torch
 
     main = torch.cuda.current_stream()
-    capturing = torch.cuda.is_current_stream_capturing()
-    for ev, outs in _pending:
+    for ev, _, _ in _pending:
         main.wait_event(ev)
-        if not capturing:
-            for t in outs:
-                if t is not None:
-                    t.record_stream(main)
     _pending.clear()
 
 
