@@ -263,6 +263,7 @@ class BlockWorkload:
                 ready[i % 2].record(cs)
 
         upload(0)
+        keep = []  # results referenced until the copy stream is joined (no record_stream)
         for i in range(steps):
             if i + 1 < steps:
                 upload(i + 1)
@@ -279,9 +280,9 @@ class BlockWorkload:
                 cs.wait_event(done)
                 self.hq.copy_(gx.values, non_blocking=True)
                 self.hs.copy_(gx.scales, non_blocking=True)
-            gx.values.record_stream(cs)
-            gx.scales.record_stream(cs)
+            keep.append(gx)
         main.wait_stream(cs)
+        del keep
 
     def config(self):
         w = self.w
