@@ -38,6 +38,8 @@ METRIC = "transformer-block fwd+bwd tokens/s; per-block INT8 GEMM TOPS vs INT8 p
 INT8_PEAK_TOPS = 4500.0  # B200 dense INT8 datasheet (no measured INT8 figure in MEASURED_PEAKS.json)
 
 WORKLOADS = {
+    # BASELINE.json configs[0]: one QuantLinear fwd+bwd, the reference's own CPU-runnable case
+    "linear_n4096": dict(linear=True, n=4096, c=1024, d=4096),
     # BASELINE.json configs[3]: the paper's speed-up setting, north-star target
     "block_h4096_s2048": dict(c=4096, heads=32, hidden=16384, seq=2048, batch=2),
     # BASELINE.json configs[1]
@@ -291,6 +293,61 @@ class BlockWorkload:
                 "l2": "working set (201 MB INT8 weights + activations) larger than the 126 MB L2"}
 
 
+class LinearWorkload:
+    """One QuantLinear fwd + bwd (dgrad, wgrad -> FP32 dW, dbias) per step (BASELINE config 1)."""
+
+    def __init__(self, jf, w, args, world, rank):
+        from paper_2403_12422_b200.qlayers import QuantLinear
+
+        self.jf, self.w, self.world = jf, w, world
+        self.n, self.c, self.d = w["n"], w["c"], w["d"]
+        g = torch.Generator(device="cuda").manual_seed(1000 + rank)
+        wm = torch.randn((self.d, self.c), generator=g, device="cuda") * self.c ** -0.5
+        self.lin = QuantLinear(wm, torch.zeros(self.d, device="cuda"))
+        self.x = torch.randn((self.n, self.c), generator=g, device="cuda")
+        self.dy = 0.1 * torch.randn((self.n, self.d), generator=g, device="cuda")
+        self.xq = jf.quantize_per_block(self.x)
+        self.dyq = jf.quantize_per_block(self.dy)
+        self._flush = torch.zeros(64 << 20, dtype=torch.float32, device="cuda")  # 256 MiB > 126 MB L2
+
+    def step(self):
+        self._flush.add_(1)  # operands fit in L2: write 256 MiB first so every step starts cold
+        self.lin.forward(self.xq)
+        _, dw, db = self.lin.backward(self.dyq)
+        if self.world > 1:
+            allreduce_grads({"w": dw, "b": db}, self.world)
+
+    def e2e_setup(self):
+        n, c, d = self.n, self.c, self.d
+        self.hx, self.hdy = self.x.cpu().pin_memory(), self.dy.cpu().pin_memory()
+        self.hq = torch.empty((n, c), dtype=torch.int8).pin_memory()
+        self.hs = torch.empty((n // 32, c // 32), dtype=torch.float32).pin_memory()
+        return int(n * c * 4 + n * d * 4), int(n * c + (n * c // 1024) * 4)
+
+    def e2e_step(self):
+        """Host pinned FP32 x, dY in; dX codes + scales out."""
+        jf = self.jf
+        dx_ = torch.empty_like(self.x)
+        dd_ = torch.empty_like(self.dy)
+        dx_.copy_(self.hx, non_blocking=True)
+        dd_.copy_(self.hdy, non_blocking=True)
+        self.lin.forward(jf.quantize_per_block(dx_))
+        gx, dw, db = self.lin.backward(jf.quantize_per_block(dd_))
+        if self.world > 1:
+            allreduce_grads({"w": dw, "b": db}, self.world)
+        self.hq.copy_(gx.values, non_blocking=True)
+        self.hs.copy_(gx.scales, non_blocking=True)
+
+    def e2e_run(self, steps):
+        for _ in range(steps):
+            self.e2e_step()
+
+    def config(self):
+        return {"linear": f"QuantLinear {self.c}->{self.d}", "tokens_per_gpu": self.n,
+                "l2": "operands fit in the 126 MB L2: every step first writes a 256 MiB buffer (flush, "
+                      "inside the timed step)"}
+
+
 class ModelWorkload:
     """GPT-2-style pretraining step: embedding, INT8 blocks, BF16 head + FP32 loss,
     backward, DP all-reduce, fused AdamW (paper_2403_12422_b200.model)."""
@@ -372,7 +429,8 @@ def run_ours(args, world, rank, local):
     w = dict(WORKLOADS[args.workload])
     if args.batch:
         w["batch"] = args.batch
-    wl = (ModelWorkload if "model" in w else BlockWorkload)(jf, w, args, world, rank)
+    wl = (ModelWorkload if "model" in w else LinearWorkload if "linear" in w else BlockWorkload)(
+        jf, w, args, world, rank)
     n = wl.n
     stream = torch.cuda.current_stream()
 
@@ -499,6 +557,29 @@ def roofline(gemm_tops: float, promotion: str, clocks_mhz=None, operands: str = 
 
 
 # ── cuBLAS BF16 block of the same wiring (context baseline) ─────────────
+
+
+def bf16_linear_tokens_per_s(w, steps, warmup):
+    n, c, d = w["n"], w["c"], w["d"]
+    g = torch.Generator(device="cuda").manual_seed(0)
+    lin = torch.nn.Linear(c, d, device="cuda", dtype=torch.bfloat16)
+    x = torch.randn((n, c), generator=g, device="cuda").to(torch.bfloat16).requires_grad_(True)
+    dy = (0.1 * torch.randn((n, d), generator=g, device="cuda")).to(torch.bfloat16)
+
+    def step():
+        lin(x).backward(dy)
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(steps):
+        step()
+    e.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(e) / steps
+    return n / (ms / 1e3), ms
 
 
 def bf16_block_tokens_per_s(w, steps, warmup):
@@ -638,16 +719,46 @@ def cpu_block_sample(w, tokens, reps=1):
             "seconds": round(t, 3)}
 
 
+def cpu_linear_sample(w, tokens, reps=1):
+    """Time the oracle QuantLinear fwd+bwd (qlayers.py:149-181) on `tokens` tokens."""
+    from oracle import int8flow_oracle as O
+
+    rng = np.random.default_rng(0)
+    c, d = w["c"], w["d"]
+    wm = (rng.standard_normal((d, c)) / np.sqrt(c)).astype(np.float32)
+    wc = O.quantize(wm)
+    bias = np.zeros(d, dtype=np.float32)
+    xq, xs = O.quantize(rng.standard_normal((tokens, c)).astype(np.float32))
+    dq, ds = O.quantize((0.1 * rng.standard_normal((tokens, d))).astype(np.float32))
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        O.linear_forward(xq, xs, wc, bias)
+        O.linear_backward(xq, xs, wc, dq, ds)
+        times.append(time.perf_counter() - t0)
+    t = min(times)
+    return {"value": round(tokens / t, 2), "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
+            "sample": f"oracle (numpy port of int8flow) QuantLinear {c}->{d} fwd+bwd, {tokens} tokens, "
+                      f"OpenBLAS threads = all host cores, best of {reps}",
+            "seconds": round(t, 3)}
+
+
+def cpu_sample(w, tokens):
+    if "linear" in w:  # the CPU finishes this case quickly: a 1024-token sample (of 4096)
+        return cpu_linear_sample(w, max(tokens, 1024))
+    return cpu_block_sample(w, tokens)
+
+
 def run_reference(args, world, rank):
     if rank != 0:
         return None
     w = dict(WORKLOADS[args.workload])
-    tokens = args.cpu_tokens
+    tokens = max(args.cpu_tokens, 1024) if "linear" in w else args.cpu_tokens
     for _ in range(args.warmup):
-        cpu_block_sample(w, tokens)
-    vals = [cpu_block_sample(w, tokens)["value"] for _ in range(args.steps)]
+        cpu_sample(w, tokens)
+    vals = [cpu_sample(w, tokens)["value"] for _ in range(args.steps)]
     v = statistics.median(vals)
-    cb = cpu_block_sample(w, tokens)
+    cb = cpu_sample(w, tokens)
     cb["value"] = v
     return {"metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(1e3 * tokens / v, 2), "higher_is_better": True,
@@ -674,15 +785,20 @@ def main():
                                     "what": "same model in torch BF16 autocast (cuBLAS, SDPA, exact GELU, "
                                             "LayerNorm, fused AdamW), 1 GPU",
                                     "int8_over_bf16": round(out["value"] / (tps * world), 3)}
-        if not args.no_bf16 and "model" not in w:
+        if not args.no_bf16 and "model" not in w and "linear" not in w:
             wb = dict(w)
             tps, ms = bf16_block_tokens_per_s(wb, args.steps, args.warmup)
             out["bf16_baseline"] = {"value": round(tps * world, 1), "unit": "tokens/s", "ms_per_step": round(ms, 4),
                                     "what": "same block wiring in torch BF16 (cuBLAS linear, F.layer_norm, "
                                             "exact-erf GELU, SDPA), fwd+bwd autograd, 1 GPU",
                                     "int8_over_bf16": round(out["value"] / (tps * world), 3)}
+        if not args.no_bf16 and "linear" in w:
+            tps, ms = bf16_linear_tokens_per_s(w, args.steps, args.warmup)
+            out["bf16_baseline"] = {"value": round(tps * world, 1), "unit": "tokens/s", "ms_per_step": round(ms, 4),
+                                    "what": "torch BF16 nn.Linear fwd+bwd (cuBLAS), same shapes, 1 GPU",
+                                    "int8_over_bf16": round(out["value"] / (tps * world), 3)}
         if world == 1 and not args.no_cpu and "model" not in w:
-            out["cpu_baseline"] = cpu_block_sample(w, args.cpu_tokens)
+            out["cpu_baseline"] = cpu_sample(w, args.cpu_tokens)
         print(json.dumps(out), flush=True)
     if world > 1:
         import torch.distributed as dist
