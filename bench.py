@@ -108,6 +108,51 @@ def max_over_ranks(x: float, world: int) -> float:
     return float(t.item())
 
 
+def grad_shapes(wl) -> dict:
+    """Name -> shape of the FP32 parameter gradients one step all-reduces."""
+    if hasattr(wl, "model"):
+        return {k: tuple(p.shape) for k, p in wl.model.params.items()}
+    if hasattr(wl, "lin"):
+        lin = wl.lin
+        return {"w": tuple(lin.master_weight.shape), "b": tuple(lin.bias.shape)}
+    blk, out = wl.blk, {}
+    for name in ("qkv", "proj", "mlp1", "mlp2"):
+        lin = getattr(blk, name)
+        out[f"{name}.w"] = tuple(lin.master_weight.shape)
+        if lin.bias is not None:
+            out[f"{name}.b"] = tuple(lin.bias.shape)
+    for name in ("ln1", "ln2"):
+        ln = getattr(blk, name)
+        out[f"{name}.gamma"] = tuple(ln.gamma.shape)
+        out[f"{name}.beta"] = tuple(ln.beta.shape)
+    return out
+
+
+def measure_allreduce(wl, world: int, reps: int = 5) -> dict:
+    """Time the step's gradient all-reduce alone (same payload and bucketing as the step:
+    paper_2403_12422_b200.dist.allreduce_mean), max over ranks; bus bandwidth = algbw *
+    2(n-1)/n (ring all-reduce accounting)."""
+    from paper_2403_12422_b200.dist import allreduce_mean
+
+    grads = {k: torch.ones(s, device="cuda") for k, s in grad_shapes(wl).items()}
+    nbytes = sum(g.numel() * g.element_size() for g in grads.values())
+    allreduce_mean(grads)
+    torch.cuda.synchronize()
+    barrier(world)
+    a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        allreduce_mean(grads)
+    e.record()
+    torch.cuda.synchronize()
+    ms = max_over_ranks(a.elapsed_time(e) / reps, world)
+    algbw = nbytes / (ms / 1e3) / 1e9
+    return {"bytes_per_step": nbytes, "ms": round(ms, 4), "algbw_GBps": round(algbw, 1),
+            "busbw_GBps": round(algbw * 2 * (world - 1) / world, 1), "world": world,
+            "how": "FP32 parameter-gradient all-reduce of one step timed alone (NCCL, 64 MiB buckets), "
+                   f"CUDA events, mean of {reps}, max over ranks; in the step it overlaps backward"}
+
+
 # ── clocks sampling during the timed region ─────────────────────────────
 
 
@@ -516,6 +561,8 @@ def run_ours(args, world, rank, local):
     out["clocks"] = clocks.summary()
     out["roofline"] = roofline(gemm_tops, args.promotion, clocks_mhz=out["clocks"].get("sm_mhz"),
                                operands=args.operands)
+    if world > 1:
+        out["allreduce"] = measure_allreduce(wl, world)
     return out, wl, None, w
 
 

@@ -196,6 +196,46 @@ def test_overlapped_allreduce_hook_nccl_world1(jf):
         dist.destroy_process_group()
 
 
+def test_bench_allreduce_measurement_nccl_world1(jf):
+    """bench.measure_allreduce (the N>1 'allreduce' line) on every workload kind's
+    gradient payload, over a world-size-1 NCCL group."""
+    import os
+    import socket
+    import sys
+    import types
+
+    import torch.distributed as dist
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    from paper_2403_12422_b200.model import JetfireLM, ModelConfig
+    from paper_2403_12422_b200.qlayers import BlockConfig, QuantLinear, TransformerBlock
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        rng = np.random.default_rng(0)
+        lin = [QuantLinear.initialize(rng, d, c) for d, c in ((192, 64), (64, 64), (256, 64), (64, 256))]
+        blk = TransformerBlock(BlockConfig(c_model=64, heads=2, hidden=256), *lin,
+                               jf.NormParams(torch.ones(64, device="cuda"), torch.zeros(64, device="cuda")),
+                               jf.NormParams(torch.ones(64, device="cuda"), torch.zeros(64, device="cuda")))
+        cfg = ModelConfig(layers=1, c_model=64, heads=2, hidden=128, vocab=64, max_seq=32)
+        for wl, nbytes in ((types.SimpleNamespace(blk=blk), 4 * (192 * 64 + 192 + 64 * 64 + 64 + 256 * 64 + 256
+                                                                + 64 * 256 + 64 + 4 * 64)),
+                           (types.SimpleNamespace(lin=lin[0]), 4 * (192 * 64 + 192)),
+                           (types.SimpleNamespace(model=JetfireLM(cfg, seed=1)), None)):
+            r = bench.measure_allreduce(wl, 1, reps=2)
+            assert r["ms"] > 0 and r["world"] == 1
+            if nbytes is not None:
+                assert r["bytes_per_step"] == nbytes
+    finally:
+        dist.destroy_process_group()
+
+
 def test_fused_cross_entropy(jf):
     """jf_cross_entropy_bf16 == FP32 log_softmax / softmax-minus-onehot of the same bf16 logits."""
     from paper_2403_12422_b200 import _lib
