@@ -13,7 +13,8 @@ import threading
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libjetfire.so")
+# JF_LIBJETFIRE: an alternative in-tree build (diagnostics / A-B of kernel variants)
+LIB_PATH = os.environ.get("JF_LIBJETFIRE") or os.path.join(_HERE, "libjetfire.so")
 
 JF_EFLAG_NONFINITE = 1
 JF_EFLAG_OVERFLOW = 2
