@@ -196,6 +196,14 @@ int jf_adamw_quantize(float *p, const float *g, float *m, float *v, int64_t n, i
                       double b2, float eps, float wd, float bc1, float bc2, int8_t *q, float *s, int32_t *err,
                       jf_stream_t stream);
 
+/* AdamW over many small FP32 tensors in one launch (same per-element arithmetic as
+ * jf_adamw).  `tensors`: device array of {float *p; const float *g; float *m; float *v;
+ * int64 count; float wd; int32 pad} (48 bytes each); chunk c covers elements
+ * [chunk_start[c], chunk_start[c] + chunk_len) of tensor chunk_tensor[c]. */
+int jf_adamw_multi(const void *tensors, const int32_t *chunk_tensor, const int64_t *chunk_start,
+                   int32_t nchunks, int64_t chunk_len, float lr, double b1, double b2, float eps,
+                   float bc1, float bc2, jf_stream_t stream);
+
 /* Dropout by scale folding  [qnonlinear.py:207-240]: codes zeroed where keep[i]==0,
  * scales snapped f16(s * keep_factor).  keep: [n x c] uint8 (the materialized mask). */
 int jf_dropout(const int8_t *q, const float *s, const uint8_t *keep, float keep_factor,

@@ -73,6 +73,38 @@ __global__ void __launch_bounds__(kTileThreads) adamw_quant_kernel(float *p, con
   quant_store(t, w, q, s, red, err);
 }
 
+// Many small tensors (biases, LayerNorm γ/β) in one launch: a table of tensors
+// and a table of fixed-length chunks (tensor index, first element); one CTA
+// per chunk.  Per-element arithmetic identical to adamw_kernel.
+struct AdamTensor {
+  float *p;
+  const float *g;
+  float *m;
+  float *v;
+  int64_t count;
+  float wd;
+  int32_t pad;
+};
+static_assert(sizeof(AdamTensor) == 48, "AdamTensor layout (mirrored in model.py)");
+
+__global__ void __launch_bounds__(256) adamw_multi_kernel(const AdamTensor *__restrict__ tab,
+                                                          const int32_t *__restrict__ chunk_tensor,
+                                                          const int64_t *__restrict__ chunk_start,
+                                                          int64_t chunk_len, AdamArgs a) {
+  const AdamTensor T = tab[chunk_tensor[blockIdx.x]];
+  const int64_t s = chunk_start[blockIdx.x];
+  const int64_t e = min(s + chunk_len, T.count);
+  AdamArgs aa = a;
+  aa.wd = T.wd;
+  for (int64_t i = s + threadIdx.x; i < e; i += blockDim.x) {
+    float pp = T.p[i], mm = T.m[i], vv = T.v[i];
+    adam_elem(aa, pp, __ldg(T.g + i), mm, vv);
+    T.p[i] = pp;
+    T.m[i] = mm;
+    T.v[i] = vv;
+  }
+}
+
 }  // namespace jf
 
 using namespace jf;
@@ -111,4 +143,14 @@ extern "C" int jf_adamw_quantize(float *p, const float *g, float *m, float *v, i
   adamw_quant_kernel<<<tile_grid(n, c), kTileThreads, 0, (cudaStream_t)stream>>>(
       p, g, m, v, n, c, adam_args(lr, b1, b2, eps, wd, bc1, bc2), q, s, err);
   return jf_launch_check("adamw_quantize");
+}
+
+extern "C" int jf_adamw_multi(const void *tensors, const int32_t *chunk_tensor, const int64_t *chunk_start,
+                              int32_t nchunks, int64_t chunk_len, float lr, double b1, double b2, float eps,
+                              float bc1, float bc2, jf_stream_t stream) {
+  if (nchunks <= 0 || chunk_len <= 0) return JF_ERR_ARG;
+  adamw_multi_kernel<<<(unsigned)nchunks, 256, 0, (cudaStream_t)stream>>>(
+      static_cast<const AdamTensor *>(tensors), chunk_tensor, chunk_start, chunk_len,
+      adam_args(lr, b1, b2, eps, 0.0f, bc1, bc2));
+  return jf_launch_check("adamw_multi");
 }

@@ -211,6 +211,32 @@ class AdamW:
         for i, blk in enumerate(model.blocks):
             for name in ("qkv", "proj", "mlp1", "mlp2"):
                 self.qlin[f"block{i}.{name}.w"] = getattr(blk, name)
+        # small tensors (biases, LayerNorm gamma/beta) share one jf_adamw_multi launch
+        self.small = [k for k, p in model.params.items() if k not in self.qlin and p.numel() < self.SMALL]
+        self._multi = None
+
+    SMALL = 1 << 20      # elements: tensors below this go through the multi-tensor launch
+    CHUNK = 4096         # elements per CTA of jf_adamw_multi
+
+    def _multi_tables(self, device):
+        """Device chunk tables (static) and a pinned/device pair for the per-step tensor table."""
+        if self._multi is None:
+            import numpy as np
+
+            ct, cs = [], []
+            for ti, k in enumerate(self.small):
+                n = self.model.params[k].numel()
+                for s in range(0, n, self.CHUNK):
+                    ct.append(ti)
+                    cs.append(s)
+            chunk_t = torch.tensor(np.asarray(ct, np.int32), device=device)
+            chunk_s = torch.tensor(np.asarray(cs, np.int64), device=device)
+            host = torch.empty((len(self.small), 6), dtype=torch.int64).pin_memory()
+            dev = torch.empty((len(self.small), 6), dtype=torch.int64, device=device)
+            ev = torch.cuda.Event()
+            ev.record()
+            self._multi = (chunk_t, chunk_s, host, dev, ev)
+        return self._multi
 
     def step(self, grads: dict) -> None:
         from .qtensor import empty_like_shape
@@ -222,7 +248,27 @@ class AdamW:
         bc2 = 1.0 - b2 ** self.t
         L = _lib.lib()
         st = _lib.stream_handle()
+        small = set(self.small)
+        if self.small:
+            import struct
+
+            chunk_t, chunk_s, host, dev, ev = self._multi_tables(self.model.params[self.small[0]].device)
+            ev.synchronize()  # the previous step's upload of the pinned table has finished
+            tab = host.numpy()
+            for i, key in enumerate(self.small):
+                p, g = self.model.params[key], grads[key]
+                if not g.is_contiguous():
+                    g = grads[key] = g.contiguous()
+                wd = self.weight_decay if (key in self.model.decay_keys and self.weight_decay) else 0.0
+                tab[i] = (p.data_ptr(), g.data_ptr(), self.m[key].data_ptr(), self.v[key].data_ptr(), p.numel(),
+                          struct.unpack("<I", struct.pack("<f", wd))[0])
+            dev.copy_(host, non_blocking=True)
+            ev.record()
+            _lib.check(L.jf_adamw_multi(dev.data_ptr(), chunk_t.data_ptr(), chunk_s.data_ptr(), chunk_t.numel(),
+                                        self.CHUNK, self.lr, b1, b2, self.eps, bc1, bc2, st), "adamw_multi")
         for key, p in self.model.params.items():
+            if key in small:
+                continue
             g = grads[key].contiguous()
             wd = self.weight_decay if (key in self.model.decay_keys and self.weight_decay) else 0.0
             lin = self.qlin.get(key)
