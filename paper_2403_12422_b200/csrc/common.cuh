@@ -68,6 +68,19 @@ JF_DEV int quant_code_fast(float x, float s, float r) {
   return q;
 }
 
+// quant_code_fast's common path only: the code of fl(x * r), and `tie` raised when
+// y is within 3e-5 of a half-integer (the caller then redoes the element with
+// quant_code_fast).  Straight-line code: no per-element branch / reconvergence.
+JF_DEV int quant_code_try(float x, float r, bool &tie) {
+  const float y = __fmul_rn(x, r);
+  const float d = fabsf(__fsub_rn(__fsub_rn(y, floorf(y)), 0.5f));
+  tie = tie || !(d > 3.0e-5f);
+  int q = __float2int_rn(y);
+  q = q > kQmax ? kQmax : q;
+  q = q < -kQmax ? -kQmax : q;
+  return q;
+}
+
 JF_DEV uint32_t abs_bits(float x) { return __float_as_uint(x) & 0x7fffffffu; }
 
 // pack 4 codes into one 32-bit word (little-endian byte order = column order)

@@ -82,10 +82,17 @@ JF_DEV void quant_store(const TilePos &t, const float (&v)[4][8], int8_t *__rest
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       uint2 w;
-      w.x = pack4(quant_code_fast(v[i][0], sc, rc), quant_code_fast(v[i][1], sc, rc),
-                  quant_code_fast(v[i][2], sc, rc), quant_code_fast(v[i][3], sc, rc));
-      w.y = pack4(quant_code_fast(v[i][4], sc, rc), quant_code_fast(v[i][5], sc, rc),
-                  quant_code_fast(v[i][6], sc, rc), quant_code_fast(v[i][7], sc, rc));
+      bool tie = false;
+      w.x = pack4(quant_code_try(v[i][0], rc, tie), quant_code_try(v[i][1], rc, tie),
+                  quant_code_try(v[i][2], rc, tie), quant_code_try(v[i][3], rc, tie));
+      w.y = pack4(quant_code_try(v[i][4], rc, tie), quant_code_try(v[i][5], rc, tie),
+                  quant_code_try(v[i][6], rc, tie), quant_code_try(v[i][7], rc, tie));
+      if (tie) {  // rare: a code near a rounding tie takes the exact division
+        w.x = pack4(quant_code_fast(v[i][0], sc, rc), quant_code_fast(v[i][1], sc, rc),
+                    quant_code_fast(v[i][2], sc, rc), quant_code_fast(v[i][3], sc, rc));
+        w.y = pack4(quant_code_fast(v[i][4], sc, rc), quant_code_fast(v[i][5], sc, rc),
+                    quant_code_fast(v[i][6], sc, rc), quant_code_fast(v[i][7], sc, rc));
+      }
       *reinterpret_cast<uint2 *>(q + t.row(i) * t.c + t.col()) = w;
     }
     if (t.warp == 0 && (t.lane & 3) == 0) {
@@ -122,10 +129,17 @@ JF_DEV void quant_store_ld(const TilePos &t, const float (&v)[4][8], int8_t *__r
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       uint2 w;
-      w.x = pack4(quant_code_fast(v[i][0], sc, rc), quant_code_fast(v[i][1], sc, rc),
-                  quant_code_fast(v[i][2], sc, rc), quant_code_fast(v[i][3], sc, rc));
-      w.y = pack4(quant_code_fast(v[i][4], sc, rc), quant_code_fast(v[i][5], sc, rc),
-                  quant_code_fast(v[i][6], sc, rc), quant_code_fast(v[i][7], sc, rc));
+      bool tie = false;
+      w.x = pack4(quant_code_try(v[i][0], rc, tie), quant_code_try(v[i][1], rc, tie),
+                  quant_code_try(v[i][2], rc, tie), quant_code_try(v[i][3], rc, tie));
+      w.y = pack4(quant_code_try(v[i][4], rc, tie), quant_code_try(v[i][5], rc, tie),
+                  quant_code_try(v[i][6], rc, tie), quant_code_try(v[i][7], rc, tie));
+      if (tie) {  // rare: a code near a rounding tie takes the exact division
+        w.x = pack4(quant_code_fast(v[i][0], sc, rc), quant_code_fast(v[i][1], sc, rc),
+                    quant_code_fast(v[i][2], sc, rc), quant_code_fast(v[i][3], sc, rc));
+        w.y = pack4(quant_code_fast(v[i][4], sc, rc), quant_code_fast(v[i][5], sc, rc),
+                    quant_code_fast(v[i][6], sc, rc), quant_code_fast(v[i][7], sc, rc));
+      }
       *reinterpret_cast<uint2 *>(q + t.row(i) * ldq + t.col()) = w;
     }
     if (t.warp == 0 && (t.lane & 3) == 0) {
