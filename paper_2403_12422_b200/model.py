@@ -9,8 +9,11 @@ Data flow per step (as the reference):
   logits = deq(h) @ head_w^T + head_b                   FP32 (reference) or BF16 head
   loss = masked mean of -log_softmax(logits)[y]         FP32
   dh = dlogits @ head_w -> quantize -> blocks backward -> deq -> scatter-add into emb
-Parameters, gradients and AdamW moments are FP32; the INT8 weight copies are
-re-derived lazily after ``step()`` (``QuantLinear.mark_updated``, qlayers.py:139-147).
+Parameters, gradients and AdamW moments are FP32.  ``AdamW.step`` (``optim.cu``,
+``jf_adamw_quantize``) writes the updated FP32 master AND its INT8 codes + scales in one
+pass, in place, so the INT8 weight copies never go stale (the reference re-derives them
+lazily after ``mark_updated``, qlayers.py:139-147; ``mark_updated`` here requantizes in
+place too).
 """
 
 from __future__ import annotations
@@ -328,8 +331,13 @@ class GraphedTrainStep:
     def step(self, x: torch.Tensor, y: torch.Tensor) -> torch.Tensor:
         self.x.copy_(x, non_blocking=True)
         self.y.copy_(y, non_blocking=True)
+        from . import runtime as _rt
+
         self.graph.replay()
         _lib.launch_count[0] += self.kernels_per_replay
+        # eager error mode: a non-finite / overflowing forward or backward raises the
+        # reference's ValueError BEFORE AdamW touches params, m and v (trainer.py:482-505)
+        _rt.maybe_check()
         self.opt.step(self.grads)
         return self.loss
 

@@ -146,9 +146,12 @@ class QuantLinear:
         self._weight_f16 = [None, None]
 
     def mark_updated(self) -> None:
-        self._weight_q = None
-        self._weight_qt = None
-        self._weight_f16 = [None, None]
+        """The master weight changed (qlayers.py:145-147).  An existing INT8 copy is
+        requantized IN PLACE (same buffers), so a captured CUDA graph that reads it keeps
+        reading live weights; derived copies are dropped."""
+        if self._weight_q is not None:
+            quantize_per_block(self.master_weight, self.block, out=self._weight_q)
+        self.drop_derived()
 
     def forward(self, xq: BlockQuantTensor, counters: AccessCounters | None = None,
                 threads: int = 1) -> BlockQuantTensor:

@@ -179,12 +179,13 @@ def _check_block(block: int) -> None:
         raise ValueError(f"the B200 path supports block size {BLOCK} only, got {block}")
 
 
-def quantize_per_block(x, block: int = BLOCK) -> BlockQuantTensor:
+def quantize_per_block(x, block: int = BLOCK, *, out: BlockQuantTensor | None = None) -> BlockQuantTensor:
     """Per-block absmax INT8 quantizer (qtensor.py:219-246) — kernel K1.
 
     ``x``: float32 or bfloat16 2-D tensor (CUDA; numpy arrays are uploaded).
     Raises the reference's ValueErrors (2-D, block, multiple, non-finite,
-    binary16 overflow).
+    binary16 overflow).  ``out`` (extension): write the codes and scales into
+    an existing tensor of the same shape (stable addresses for captured graphs).
     """
     if not isinstance(x, torch.Tensor):
         x = np.asarray(x)
@@ -205,7 +206,10 @@ def quantize_per_block(x, block: int = BLOCK) -> BlockQuantTensor:
         x = x.to(torch.float32)
     if x.stride(1) != 1 or x.stride(0) < c or (x.data_ptr() % 16):
         x = x.contiguous()
-    out = empty_like_shape(n, c, x.device)
+    if out is None:
+        out = empty_like_shape(n, c, x.device)
+    elif out.shape != (n, c) or out.device != x.device:
+        raise ValueError(f"out has shape {out.shape}, expected {(n, c)}")
     fn = L.jf_quantize_f32 if x.dtype == torch.float32 else L.jf_quantize_bf16
     if x.dtype == torch.bfloat16 and x.stride(0) % 8:
         x = x.contiguous()

@@ -13,8 +13,18 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,temperature.gpu --format=csv
 for s in $STEPS; do
   case $s in
     tests)
-      timeout 900 python -m pytest tests -m gpu -x -q > "$OUT/pytest_gpu.log" 2>&1
+      JF_REPORT_DIR="$OUT" timeout 2400 python -m pytest tests -m gpu -q -rf > "$OUT/pytest_gpu.log" 2>&1
       echo "pytest exit $?" >> "$OUT/pytest_gpu.log" ;;
+    parity)
+      JF_REPORT_DIR="$OUT" timeout 1800 python -m pytest tests/test_gpu_parity_configs.py tests/test_gpu_ref_suite.py \
+        -m gpu -q -rA > "$OUT/pytest_parity.log" 2>&1
+      echo "pytest exit $?" >> "$OUT/pytest_parity.log" ;;
+    sanitize)
+      for tool in memcheck racecheck synccheck; do
+        timeout 900 compute-sanitizer --tool $tool --print-limit 20 python tools/sanitize_driver.py \
+          > "$OUT/sanitize_$tool.txt" 2>&1
+        echo "exit $?" >> "$OUT/sanitize_$tool.txt"
+      done ;;
     micro)
       timeout 300 ./paper_2403_12422_b200/microbench > "$OUT/microbench.jsonl" 2>&1 ;;
     gemm)

@@ -1,0 +1,51 @@
+"""Small-shape driver for compute-sanitizer (memcheck / racecheck / synccheck):
+one launch of each hand-written pipeline -- the tcgen05 GEMM kernels (TMA-staged
+scales, MN-major operands, generic-shape kernel with partial tiles, int32
+partials, f16-widened operands), Add+stats, LayerNorm fwd/bwd, GELU fwd/bwd,
+the quantizer and the column sum.  Usage:
+  compute-sanitizer --tool racecheck python tools/sanitize_driver.py
+"""
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2403_12422_b200 as jf  # noqa: E402
+from paper_2403_12422_b200 import runtime  # noqa: E402
+
+
+def q(shape, scale=1.0, seed=0):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    return jf.quantize_per_block(torch.randn(shape, generator=g, device="cuda") * scale)
+
+
+def main():
+    jf.require_cuda()
+    x, w, dy = q((256, 384), seed=1), q((256, 384), 0.05, seed=2), q((256, 256), 0.1, seed=3)
+    for prom in ("exact", "fast"):
+        runtime.set_promotion(prom)
+        jf.block_mm_forward(x, w, bias=torch.zeros(256, device="cuda"))   # i8s, K-major
+        jf.block_mm_grad_input(dy, w)                                      # i8s, MN-major B
+        jf.block_mm_grad_weight(dy, x, quantize=False)                     # i8s, MN-major A and B
+    runtime.set_promotion("exact")
+    xg, wg = q((160, 96), seed=4), q((224, 96), seed=5)                    # generic kernel, partial tiles
+    jf.block_mm_forward(xg, wg)
+    jf.block_partials(xg.values, wg.values, 1)                            # int32 partials
+    runtime.set_gemm_operands("f16")
+    jf.block_mm_forward(x, w)                                              # f16-widened operands
+    runtime.set_gemm_operands("int8")
+    a, st = jf.add_forward(x, q((256, 384), seed=6), 64)
+    ln = jf.NormParams(torch.ones(384, device="cuda"), torch.zeros(384, device="cuda"))
+    y, ctx = jf.layernorm_forward(a, st, ln)
+    jf.layernorm_backward(ctx, q((256, 384), 0.1, seed=7), ln)
+    g = jf.gelu_forward(x)
+    jf.gelu_backward(x, g)
+    jf.column_sum(dy)
+    torch.cuda.synchronize()
+    jf.check_errors()
+    print("sanitize driver ok")
+
+
+if __name__ == "__main__":
+    main()
