@@ -6,6 +6,8 @@
 #include <string.h>
 
 #include <mutex>
+#include <set>
+#include <utility>
 
 #include "common.cuh"
 
@@ -26,14 +28,34 @@ int jf_launch_check(const char *what) {
 }
 
 int jf_num_sms() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
+  static int n[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int &v = n[dev & 63];
+  if (v == 0) {
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    if (v <= 0) v = 148;
   }
-  return n;
+  return v;
+}
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is a per-DEVICE setting: remember
+// the (kernel, device) pairs already raised, so a process driving several GPUs sets
+// it once on each.
+int jf_set_smem_attr(const void *func, int bytes, const char *what) {
+  static std::mutex mu;
+  static std::set<std::pair<const void *, int>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.count({func, dev})) return JF_OK;
+  }
+  if (cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess)
+    return jf_launch_check(what);
+  std::lock_guard<std::mutex> lk(mu);
+  done.insert({func, dev});
+  return JF_OK;
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {

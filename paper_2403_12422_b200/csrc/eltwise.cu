@@ -705,6 +705,7 @@ __global__ void __launch_bounds__(256) dropout_kernel(const int8_t *__restrict__
 
 using namespace jf;
 int jf_launch_check(const char *what);
+int jf_set_smem_attr(const void *func, int bytes, const char *what);
 
 static bool ok_shape(int64_t n, int64_t c) { return n > 0 && c > 0 && n % 32 == 0 && c % 32 == 0; }
 
@@ -720,11 +721,7 @@ extern "C" int jf_add_stats(const int8_t *a, const float *as, const int8_t *b, c
   const int tile_w = (kTileCols / l) * l;
   dim3 grid((unsigned)((c + tile_w - 1) / tile_w), (unsigned)(n / 32));
   const size_t smem = 32 * 257 * sizeof(float);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(add_stats_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  if (int rc = jf_set_smem_attr((const void *)add_stats_kernel, (int)smem, "add_stats attr")) return rc;
   add_stats_kernel<<<grid, kTileThreads, smem, (cudaStream_t)stream>>>(
       a, as, b, bs, n, c, w, tile_w, yq, ys, mean, sumsq, err);
   return jf_launch_check("add_stats");
@@ -794,11 +791,8 @@ extern "C" int jf_ln_bwd(const int8_t *x, const float *xs, const float *mu, cons
   // staged rows: 8 warps x (32/nleaf) rows x 2 arrays x nleaf x (leaf_len + 16) bytes
   const size_t leaf_smem = leafp ? (size_t)8 * 32 * 2 * (leaf_len + 16) + (size_t)nleaf * (leaf_len + 4) * 4 : 0;
   if (leafp && leaf_smem <= 200 * 1024) {
-    static size_t attr = 0;
-    if (leaf_smem > 48 * 1024 && leaf_smem > attr) {
-      cudaFuncSetAttribute(ln_bwd_rows_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)leaf_smem);
-      attr = leaf_smem;
-    }
+    if (leaf_smem > 48 * 1024)
+      if (int rc = jf_set_smem_attr((const void *)ln_bwd_rows_leaf_kernel, 200 * 1024, "ln_bwd attr")) return rc;
     const int64_t rows_per_cta = 8 * (32 / nleaf);
     ln_bwd_rows_leaf_kernel<<<(unsigned)((n + rows_per_cta - 1) / rows_per_cta), 256, leaf_smem, st>>>(
         A, nleaf, (int)leaf_len, m1, m2);

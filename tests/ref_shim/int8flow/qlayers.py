@@ -84,6 +84,14 @@ class QuantLinear:
         return wrap(dxq), host(dw), host(db)
 
 
+def _drop_host(st):
+    """GPU DropoutState (mask None = keep all at p = 0) -> the reference's numpy form."""
+    from .qnonlinear import DropoutState
+
+    mask = None if st.mask is None else st.mask.cpu().numpy().astype(bool)
+    return DropoutState(st.p, st.seed, mask)
+
+
 def _norm_gpu(p) -> _gn.NormParams:
     return _gn.NormParams(np.asarray(p.gamma, np.float32), np.asarray(p.beta, np.float32), p.eps)
 
@@ -135,7 +143,9 @@ class TransformerBlock:
                                           _norm_gpu(self.ln2), attn_dtype=torch.float32)
         out = self._inner.forward(gpu(xq), batch, seq, dropout_seed=dropout_seed, train=train,
                                   counters=counters, threads=threads)
-        self._saved = SimpleNamespace(quant_saves=[wrap(t) for t in self._inner._saved.quant_saves])
+        sv = self._inner._saved
+        self._saved = SimpleNamespace(quant_saves=[wrap(t) for t in sv.quant_saves],
+                                      drop1=_drop_host(sv.drop1), drop2=_drop_host(sv.drop2))
         return wrap(out)
 
     def backward(self, dyq, counters=None, threads: int = 1):

@@ -11,6 +11,10 @@ from ._ref import qtensor as _r
 
 INT8_MAX = _r.INT8_MAX
 snap_to_f16 = _r.snap_to_f16  # host helper (qtensor.py:26-28), not a kernel
+# ablation-only quantization schemes (qtensor.py:31-70, 267-310; out of scope)
+PER_TENSOR, PER_TOKEN, PER_CHANNEL = _r.PER_TENSOR, _r.PER_TOKEN, _r.PER_CHANNEL
+QuantScheme, SchemeKind = _r.QuantScheme, _r.SchemeKind
+quantize_with_scheme, quantization_error = _r.quantize_with_scheme, _r.quantization_error
 
 
 def _frozen(a: np.ndarray) -> np.ndarray:
