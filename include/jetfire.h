@@ -43,7 +43,7 @@ typedef struct CUstream_st *jf_stream_t; /* == cudaStream_t */
 
 /* GEMM promotion modes (qgemm.py:183-229). */
 #define JF_MODE_EXACT 0 /* acc = fl(acc + fl(fl(P*sa)*sb)): bit-exact with the reference */
-#define JF_MODE_FAST 1  /* acc = fl(acc + fl(P*(sa*sb))): one rounding less, |err| <= 1e-6 rel */
+#define JF_MODE_FAST 1  /* acc = fma(P, sa*sb, acc) (sa*sb exact): one rounding per chunk instead of three */
 
 /* GEMM output kinds (qgemm.py:266-279). */
 #define JF_OUT_INT8 0     /* requantized codes + scales (quantize=True) */
@@ -132,8 +132,8 @@ size_t jf_gemm_scratch_bytes(int32_t which /*1=dgrad,2=wgrad*/, int64_t n, int64
 int jf_gemm_partials(const int8_t *a, const int8_t *bt, int64_t m, int64_t n, int64_t k,
                      int64_t kblk, int32_t *p, jf_stream_t stream);
 
-/* Diagnostics: GEMM launch options for A/B experiments ("impl" 0 = kind::i8, 1 = kind::f16;
- * "epi" 16|8 promotion warps; "issuers" 1|3; "ctl_kind"/"ctl_ns" control-thread wait flavour).
+/* Diagnostics: GEMM launch options for A/B experiments ("cols" 32|64 columns per promotion
+ * warp; "pipe" 0|1 software-pipelined TMEM loads; "tma_scales" 0 forces the generic kernel).
  * Defaults are the measured best; results are bit-identical across options. */
 int jf_gemm_set_option(const char *key, int value);
 

@@ -5,33 +5,30 @@
 // exactly as qgemm.py:193-229 (_mm_core / _scaled_accumulate), then +bias and
 // a 32x32 block requantization (qgemm.py:266-279).
 //
-// Design (one persistent CTA per SM, warp-specialized, 128x128 output tiles):
-//   warp 0        TMA producer: 128x128-byte K-major SW128 tiles of A and B
-//                 into a 6-stage smem ring (4 K chunks per stage).
-//   warp 1        MMA issuer: one tcgen05.mma.kind::i8 (M=128, N=128, K=32)
-//                 per K chunk into TMEM buffer (chunk % 4), accumulate = 0:
-//                 every chunk is a fresh int32 partial because the reference
-//                 promotes each 32-deep product separately.
-//   warps 2..17   promotion/epilogue (16 warps, 32 columns each; TMEM lane
-//                 quarter = warp % 4).  Per chunk a thread tcgen05.ld's its 32
-//                 int32 partials, frees the buffer, and promotes in packed
-//                 f32x2 ops:
+// Main kernel (gemm_tc_kernel; every transformer shape: M, N, K multiples of 128):
+// one persistent CTA per SM, warp-specialized, 128x128 output tiles.
+//   warp 0        TMA producer: each stage = 4 K chunks of A and B (SW128 tiles)
+//                 plus the stage's 4x4 sub-grids of both scale grids.
+//   warp 1        MMA issuer: per 32-deep chunk one tcgen05.mma.kind::i8
+//                 (M=128 N=128 K=32; or two kind::f16 K=16 on f16-widened
+//                 codes), accumulate = 0 -- every chunk is a fresh partial
+//                 because the reference promotes each 32-deep product
+//                 separately -- into TMEM buffer (chunk % 4).
+//   warps 2..17   promotion/epilogue: 32 columns x 32 TMEM lanes per warp
+//                 (lane quarter = warp % 4).  Per chunk: tcgen05.ld the
+//                 partials, release the buffer, promote in packed f32x2 ops:
 //                   EXACT: acc = fl(acc + fl(fl(P*sa)*sb))   (bit-exact)
 //                   FAST : acc = fma(P, sa*sb, acc)          (sa*sb exact)
-//                 After the last chunk: +bias, 32x32 absmax (warp = 32 rows),
-//                 binary16 scale, RNE codes, INT8 + scale stores.
-// Bound: per output element per 32 MACs the promotion
-// costs one I2F (ALU pipe, half rate) and 3 (exact) / 1 (fast) FP32 ops; at
-// 128 FP32 ops/clk/SM exact mode cannot beat 384 clk per 128x128x32 chunk
-// (16.7% of the 64-clk tensor rate), fast mode is held to 256 clk by I2F.
-// Variants measured A/B in one session (mlp1 fwd, 4096x16384x4096, exact):
-// this per-chunk hand-off 1294 us; chunk pairs per barrier 1345 us; MMA issue
-// folded into a promotion warp 1842 us; 8 promotion warps x 64 columns 1406
-// us; 3 MMA issuers 1318 us; "phase" issue (4 MMAs after all 4 buffers
-// drain) 1356 us.  The remaining gap to the 403-clk/chunk standalone
-// promotion loop (profiles/r1e_microbench.jsonl) is sub-partition skew: the
-// four sub-partitions each serve one TMEM lane quarter, the buffer release
-// waits for the slowest, and the one hosting the MMA issuer lags.
+//                 After the last chunk: +bias, 32x32 absmax, binary16
+//                 scale, RNE codes.  FP32 never reaches HBM (except the FP32
+//                 output kinds).
+// Bounds per 128x128x32 chunk and SM: MMA 64 clk (i8) / 128
+// (f16); TMEM read 64 KB at ~480 B/clk = 136 clk; exact promotion 3 rounded
+// FP32 ops x 16384 / 128 lanes = 384 clk; fast 128 clk FMA + (i8 only) one
+// I2F per element on the half-rate ALU pipe = 256 clk.
+//
+// Generic kernel (gemm_i8_kernel): any multiple-of-32 shape (partial tiles,
+// scale grids read from global memory), and the int32 partials debug output.
 #include <stdio.h>
 #include <string.h>
 
@@ -42,17 +39,12 @@ namespace gemm {
 
 constexpr int BM = 128;
 constexpr int BN = 128;
-constexpr int BK = 128;  // bytes of K per stage (4 chunks)
-constexpr int kStages = 6;
+constexpr int BK = 128;  // K per stage (4 chunks)
 constexpr int kChunksPerStage = BK / 32;
 constexpr int kTmemBufs = 4;  // == kChunksPerStage: chunk c of a stage uses buffer c
-constexpr int kEpiWarps = 16;  // promotion warps (kind::f16 path)
-constexpr int kPairSlots = 2;  // kind::f16 path: 2 slots x 2 chunk buffers x 128 f32 columns
-constexpr int kTmemCols = kPairSlots * 2 * BN;
-constexpr uint32_t kStageBytesA = BM * BK;
-constexpr uint32_t kStageBytesB = BN * BK;
 
 enum OutKind { OUT_INT8 = 0, OUT_F32 = 1, OUT_INT8_DEQ = 2, OUT_I32 = 3 };
+enum OpKind { OP_I8 = 0, OP_F16 = 1 };
 
 struct Params {
   int64_t M, N, K;
@@ -67,48 +59,64 @@ struct Params {
   int32_t *err;
   int out_kind;
   float zero;  // always 0.0f; opaque to ptxas (blocks FMUL2+FADD2 contraction)
-  long long *trace;  // JF_GEMM_TRACE builds only (f16 path): CTA 0 event clocks [8][512]
-  int ctl_kind;      // control-thread waits: 0 spin, 1 try_wait with suspend hint, 2 test + nanosleep
-  uint32_t ctl_ns;
+  long long *trace;  // JF_GEMM_TRACE builds only: CTA-0 event clocks [8][512]
 };
 
-// mbarrier wait used by the single-thread TMA producer and MMA issuer.
-JF_DEV void ctl_wait(const Params &p, uint32_t addr, uint32_t parity) {
-#ifdef JF_CTL_RUNTIME
-  if (p.ctl_kind == 1) {
-    mbar_wait_u32_sleep(addr, parity, p.ctl_ns);
-  } else if (p.ctl_kind == 2) {
-    while (!mbar_test_u32(addr, parity)) __nanosleep(p.ctl_ns);
-  } else {
-    mbar_wait_u32(addr, parity);
-  }
+// Diagnostics (JF_GEMM_TRACE builds, `make trace`): clock64 of pipeline events of
+// CTA 0's first 256 chunks (tools/gemm_trace.py): [0..2] MMA issuer (tempty wait
+// start, buffer free, commit issued), [3..5] warp 2 (tfull wait start, full, data),
+// [8 + w] promotion warp w's promotion end.
+#ifdef JF_GEMM_TRACE
+constexpr int kTrEv = 32, kTrChunks = 256;
+#define JF_TR(ev, g)                                                                               \
+  do {                                                                                             \
+    if (blockIdx.x == 0 && (g) < kTrChunks && p.trace) p.trace[(ev) * kTrChunks + (g)] = clock64(); \
+  } while (0)
 #else
-  // One flavour, compiled in: the control loops stay small enough to share the
-  // sub-partition's L0 instruction cache with the promotion loop (a runtime
-  // switch between three wait loops at every call site measured 9% slower).
-  mbar_wait_u32_sleep(addr, parity, 200);
+#define JF_TR(ev, g) \
+  do {               \
+  } while (0)
 #endif
+
+// Single-thread control roles (TMA producer, MMA issuer) wait with a suspend
+// hint: they share SM sub-partitions with promotion warps and would otherwise
+// steal their issue slots spinning.
+JF_DEV void ctl_wait(uint32_t addr, uint32_t parity) { mbar_wait_u32_sleep(addr, parity, 200); }
+
+// One lane of a converged warp (the control roles run their loops on all 32 lanes so
+// the loop state stays warp-uniform -- uniform datapath, no per-chunk R2UR -- and
+// issue each TMA / MMA / commit from the elected lane).
+JF_DEV bool elect_one() {
+  uint32_t p;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "elect.sync _|P, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, P;\n\t}"
+      : "=r"(p));
+  return p != 0;
 }
 
-struct Smem {
-  uint64_t full[kStages];
-  uint64_t empty[kStages];
-  uint64_t tfull[kTmemBufs];
-  uint64_t tempty[kTmemBufs];
-  uint32_t tmem_base;
-};
+// The partials a tcgen05.ld wrote are only valid after tcgen05.wait::ld; make
+// every consumer depend on the wait (the "+r" operands) so the compiler cannot
+// hoist any use of them above it.
+template <int N>
+JF_DEV void tmem_wait_ld_dep(uint32_t (&r)[N]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < N; i += 8)
+    asm volatile("" : "+r"(r[i]), "+r"(r[i + 1]), "+r"(r[i + 2]), "+r"(r[i + 3]), "+r"(r[i + 4]),
+                 "+r"(r[i + 5]), "+r"(r[i + 6]), "+r"(r[i + 7]));
+}
 
-constexpr size_t kSmemBytes = 1024 /*align slack*/ + kStages * (kStageBytesA + kStageBytesB) + 256;
-
-// Promote one 32-column block of int32 partials into the FP32 accumulator.
-template <bool kFast>
+// Promote one 32-column block of partials into the FP32 accumulator.
+// kF32: the partials are f32 bit patterns holding exact integers (kind::f16 path).
+template <bool kFast, bool kF32>
 JF_DEV void promote32(float *acc, const uint32_t *r, float sa, float sb, float zero) {
+  auto val = [&](int j) { return kF32 ? __uint_as_float(r[j]) : __int2float_rn((int)r[j]); };
   if (kFast) {
     const float s = __fmul_rn(sa, sb);  // exact: 11 x 11 significant bits
 #pragma unroll
-    for (int j = 0; j < 32; j += 2)
-      ffma2_rn(acc[j], acc[j + 1], __int2float_rn((int)r[j]), __int2float_rn((int)r[j + 1]), s, s, acc[j],
-               acc[j + 1]);
+    for (int j = 0; j < 32; j += 2) ffma2_rn(acc[j], acc[j + 1], val(j), val(j + 1), s, s, acc[j], acc[j + 1]);
   } else {
     // packed f32x2, every op an IEEE-rounded fp32 op in the reference order.
     // ptxas contracts mul.rn.f32x2 + add.rn.f32x2 into FFMA2 (not equivalent);
@@ -116,26 +124,7 @@ JF_DEV void promote32(float *acc, const uint32_t *r, float sa, float sb, float z
 #pragma unroll
     for (int j = 0; j < 32; j += 2) {
       float t0, t1;
-      fmul2_rn(t0, t1, __int2float_rn((int)r[j]), __int2float_rn((int)r[j + 1]), sa, sa);
-      ffma2_rn(t0, t1, t0, t1, sb, sb, zero, zero);
-      fadd2_rn(acc[j], acc[j + 1], acc[j], acc[j + 1], t0, t1);
-    }
-  }
-}
-
-// Same, for f32 partials that hold exact integers (kind::f16 path: no I2F).
-template <bool kFast>
-JF_DEV void promote32f(float *acc, const uint32_t *r, float sa, float sb, float zero) {
-  if (kFast) {
-    const float s = __fmul_rn(sa, sb);
-#pragma unroll
-    for (int j = 0; j < 32; j += 2)
-      ffma2_rn(acc[j], acc[j + 1], __uint_as_float(r[j]), __uint_as_float(r[j + 1]), s, s, acc[j], acc[j + 1]);
-  } else {
-#pragma unroll
-    for (int j = 0; j < 32; j += 2) {
-      float t0, t1;
-      fmul2_rn(t0, t1, __uint_as_float(r[j]), __uint_as_float(r[j + 1]), sa, sa);
+      fmul2_rn(t0, t1, val(j), val(j + 1), sa, sa);
       ffma2_rn(t0, t1, t0, t1, sb, sb, zero, zero);
       fadd2_rn(acc[j], acc[j + 1], acc[j], acc[j + 1], t0, t1);
     }
@@ -185,255 +174,59 @@ JF_DEV int finish_block(const Params &p, float *acc, int64_t I, int64_t J, int l
   return lane == 0 ? f : 0;
 }
 
-// kEpi promotion warps (8 or 16) in (kEpi/4) column groups of kCols = BN*4/kEpi;
-// kIss MMA issuer warps (1, or 3 when nchunks % 4 == 0).
-template <bool kFast, bool kPartials, int kEpi, int kIss>
-__global__ void __launch_bounds__((1 + kIss + kEpi) * 32, 1)
-    gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const Params p) {
-  constexpr int kCtrl = 1 + kIss;  // warp 0: TMA, warps 1..kIss: MMA issuers
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t *base = reinterpret_cast<uint8_t *>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t *sA = base;
-  uint8_t *sB = base + kStages * kStageBytesA;
-  Smem &S = *reinterpret_cast<Smem *>(sB + kStages * kStageBytesB);
-
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const int64_t mt = (p.M + BM - 1) / BM, nt = (p.N + BN - 1) / BN;
-  const int64_t ntiles = mt * nt;
-  const int nchunks = (int)(p.K / 32);
-  const int nstages_k = (nchunks + kChunksPerStage - 1) / kChunksPerStage;
-  const int my_tiles = (int)((ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x);
-  const uint32_t bar_full = smem_u32(&S.full[0]), bar_empty = smem_u32(&S.empty[0]);
-  const uint32_t bar_tfull = smem_u32(&S.tfull[0]), bar_tempty = smem_u32(&S.tempty[0]);
-
-  if (threadIdx.x == 0) {
-    prefetch_tmap(&tmA);
-    prefetch_tmap(&tmB);
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&S.full[s], 1);
-      mbar_init(&S.empty[s], kIss > 1 ? kChunksPerStage : 1);  // multi-issuer: one commit per chunk
-    }
-    for (int b = 0; b < kTmemBufs; ++b) {
-      mbar_init(&S.tfull[b], 1);
-      mbar_init(&S.tempty[b], kEpi);
-    }
-    fence_barrier_init();
-  }
-  if (warp == 1) tmem_alloc(&S.tmem_base, kTmemBufs * BN);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = S.tmem_base;
-
-  if (warp == 0) {
-    // ───────────── TMA producer ─────────────
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int m0 = (int)((tile % mt) * BM), n0 = (int)((tile / mt) * BN);
-        for (int ks = 0; ks < nstages_k; ++ks) {
-          ctl_wait(p, bar_empty + 8 * stage, phase ^ 1);
-          mbar_arrive_expect_tx(&S.full[stage], kStageBytesA + kStageBytesB);
-          tma_load_2d(sA + stage * kStageBytesA, &tmA, &S.full[stage], ks * BK, m0);
-          tma_load_2d(sB + stage * kStageBytesB, &tmB, &S.full[stage], ks * BK, n0);
-          if (++stage == kStages) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
-      }
-    }
-  } else if (warp < kCtrl) {
-    // ───────────── MMA issuers ─────────────
-    // Descriptors are precomputed: the per-chunk path is wait -> fence -> MMA -> commit.
-    const uint64_t adesc0 = smem_desc_sw128(smem_u32(sA), 16, 1024);
-    const uint64_t bdesc0 = smem_desc_sw128(smem_u32(sB), 16, 1024);
-    constexpr uint32_t idesc = idesc_i8(BM, BN, 0, 0);
-    if (kIss > 1) {
-      // issuer j takes global chunks g = j, j+kIss, ...: stage seq g/4, buffer (and
-      // K slice within the stage) g%4, and this is buffer g%4's (g/4)-th use.
-      if (lane == 0) {
-        const int total = my_tiles * nchunks;
-        for (int g = warp - 1; g < total; g += kIss) {
-          const int G = g >> 2, c = g & 3, slot = G % kStages;
-          mbar_wait_u32(bar_full + 8 * slot, (uint32_t)(G / kStages) & 1);
-          mbar_wait_u32(bar_tempty + 8 * c, ((uint32_t)G & 1) ^ 1);
-          tc_fence_after();
-          mma_i8_ss(tmem + c * BN, adesc0 + (uint64_t)((slot * kStageBytesA + c * 32) >> 4),
-                    bdesc0 + (uint64_t)((slot * kStageBytesB + c * 32) >> 4), idesc, 0u);
-          mma_commit(&S.tfull[c]);
-          mma_commit(&S.empty[slot]);
-        }
-      }
-    } else if (lane == 0) {
-      // single issuer (generic K): chunk ci of every tile lands in TMEM buffer ci % 4
-      int stage = 0, gk = 0;
-      uint32_t phase = 0, tphase = 0;
-      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        for (int ks = 0; ks < nstages_k; ++ks) {
-          ctl_wait(p, bar_full + 8 * stage, phase);
-          tc_fence_after();
-          const uint64_t ad = adesc0 + (uint64_t)((stage * kStageBytesA) >> 4);
-          const uint64_t bd = bdesc0 + (uint64_t)((stage * kStageBytesB) >> 4);
-          const int nch = min(kChunksPerStage, nchunks - ks * kChunksPerStage);
-#pragma unroll
-          for (int c = 0; c < kChunksPerStage; ++c) {
-            if (c < nch) {
-              ctl_wait(p, bar_tempty + 8 * c, ((tphase >> c) & 1) ^ 1);
-              tphase ^= 1u << c;
-              tc_fence_after();
-              mma_i8_ss(tmem + c * BN, ad + 2 * c, bd + 2 * c, idesc, 0u);
-              mma_commit(&S.tfull[c]);
-            }
-          }
-          mma_commit(&S.empty[stage]);
-          gk += nch;
-          if (++stage == kStages) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
-      }
-    }
-  } else {
-    // ───────────── promotion + epilogue ─────────────
-    constexpr int kCols = BN * 4 / kEpi;        // columns per warp: 64 (8 warps) or 32 (16 warps)
-    constexpr int kBlk = kCols / 32;            // 32-column blocks per warp
-    const int lq = warp & 3;                    // TMEM lane quarter == 32-row block of the tile
-    const int cgp = (warp - kCtrl) >> 2;        // column group
-    const uint32_t tcol = tmem + ((uint32_t)(lq * 32) << 16) + cgp * kCols;
-    const bool vec_scales = (p.sa_s1 == 1) && (p.sb_s1 == 1) && (nchunks % 4 == 0);
-    uint32_t tphase = 0;
-    int flags = 0;
-    int lt = 0;  // this CTA's local tile index
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {
-      const int64_t I = (tile % mt) * (BM / 32) + lq;              // 32-row block index
-      const int64_t J0 = (tile / mt) * (BN / 32) + kBlk * cgp;     // first 32-col block
-      const bool vrow = I * 32 < p.M;
-      bool vb[kBlk];
-#pragma unroll
-      for (int q = 0; q < kBlk; ++q) vb[q] = vrow && ((J0 + q) * 32 < p.N);
-      float acc[kBlk][32];
-#pragma unroll
-      for (int q = 0; q < kBlk; ++q)
-#pragma unroll
-        for (int j = 0; j < 32; ++j) acc[q][j] = 0.0f;
-      const float *pa = p.sa + (kPartials || !vrow ? 0 : I * p.sa_s0);
-      const float *pb[kBlk];
-#pragma unroll
-      for (int q = 0; q < kBlk; ++q) pb[q] = p.sb + (kPartials || !vb[q] ? 0 : (J0 + q) * p.sb_s0);
-      for (int cb = 0; cb < nchunks; cb += kTmemBufs) {
-        float sav[4] = {0.f, 0.f, 0.f, 0.f}, sbv[kBlk][4];
-#pragma unroll
-        for (int q = 0; q < kBlk; ++q) sbv[q][0] = sbv[q][1] = sbv[q][2] = sbv[q][3] = 0.f;
-        if (!kPartials) {
-          if (vec_scales) {  // K-contiguous scale grids: 4 chunks per 16-byte load
-            if (vrow) {
-              const float4 t = __ldg(reinterpret_cast<const float4 *>(pa + cb));
-              sav[0] = t.x; sav[1] = t.y; sav[2] = t.z; sav[3] = t.w;
-            }
-#pragma unroll
-            for (int q = 0; q < kBlk; ++q)
-              if (vb[q]) {
-                const float4 t = __ldg(reinterpret_cast<const float4 *>(pb[q] + cb));
-                sbv[q][0] = t.x; sbv[q][1] = t.y; sbv[q][2] = t.z; sbv[q][3] = t.w;
-              }
-          } else {
-#pragma unroll
-            for (int b = 0; b < kTmemBufs; ++b)
-              if (cb + b < nchunks) {
-                if (vrow) sav[b] = __ldg(pa + (cb + b) * p.sa_s1);
-#pragma unroll
-                for (int q = 0; q < kBlk; ++q)
-                  if (vb[q]) sbv[q][b] = __ldg(pb[q] + (cb + b) * p.sb_s1);
-              }
-          }
-        }
-#pragma unroll
-        for (int b = 0; b < kTmemBufs; ++b) {
-          if (cb + b >= nchunks) break;
-          mbar_wait_u32(bar_tfull + 8 * b, (tphase >> b) & 1);
-          tphase ^= 1u << b;
-          tc_fence_after();
-          uint32_t r[kBlk][32];
-#pragma unroll
-          for (int q = 0; q < kBlk; ++q) tmem_ld_32x32b_x32(tcol + b * BN + 32 * q, r[q]);
-          tmem_wait_ld();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive_u32(bar_tempty + 8 * b);
-          if (kPartials) {
-            // debug: raw int32 partials of the (single) chunk
-#pragma unroll
-            for (int q = 0; q < kBlk; ++q)
-              if (vb[q]) {
-                int32_t *dst = reinterpret_cast<int32_t *>(p.yf) + (I * 32 + lane) * p.N + (J0 + q) * 32;
-#pragma unroll
-                for (int j = 0; j < 32; j += 4)
-                  *reinterpret_cast<int4 *>(dst + j) =
-                      make_int4((int)r[q][j], (int)r[q][j + 1], (int)r[q][j + 2], (int)r[q][j + 3]);
-              }
-          } else {
-#pragma unroll
-            for (int q = 0; q < kBlk; ++q) promote32<kFast>(acc[q], r[q], sav[b], sbv[q][b], p.zero);
-          }
-        }
-      }
-      if (kPartials) continue;
-#pragma unroll
-      for (int q = 0; q < kBlk; ++q)
-        if (vb[q]) flags |= finish_block(p, acc[q], I, J0 + q, lane);
-    }
-    if (lane == 0) raise_flags(p.err, flags);
-  }
-
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, kTmemBufs * BN);
-}
-
-
-// ─────────────── gemm_i8s_kernel: the same pipeline, scales staged by TMA ───────────────
-// Used when M, N, K are multiples of 128 (every transformer-block shape).  The
-// TMA producer also brings each stage's 4x4 sub-grids of sA and sB (64 B each)
-// into shared memory, so the promotion warps read their scale factors with
-// one LDS per 4 chunks instead of two L2-latency LDGs (hand-off microbenchmark:
-// 471 clk/chunk floor, +66 with global scale loads).  A stage is released only
-// when the MMAs consumed its tiles AND all promotion warps read its scales
-// (empty barrier count 1 + 16).  No partial tiles, so no validity predicates.
-struct SmemS {
-  uint64_t full[kStages];
-  uint64_t empty[kStages];
+struct Bars {
+  uint64_t full[8];
+  uint64_t empty[8];
   uint64_t tfull[kTmemBufs];
   uint64_t tempty[kTmemBufs];
   uint32_t tmem_base;
 };
-constexpr uint32_t kScaleBytes = 256;  // per stage: A box at +0, B box at +128 (16 floats each)
-constexpr size_t kSmemBytesS =
-    1024 + kStages * (kStageBytesA + kStageBytesB) + kStages * kScaleBytes + sizeof(SmemS) + 64;
 
-// kAmn / kBmn: the operand is MN-major in memory (the UMMA reads int8
-// MN-major tiles directly, so dgrad consumes W [d x c] and wgrad consumes
-// dY [n x d] and X [n x c] as stored -- no transposed copies).  An MN-major
-// stage is a TMA box of 128 K-rows x 128 MN-bytes (SW128); chunk c starts
-// 32 rows = 4096 bytes further, versus 32 bytes for a K-major stage.
-template <bool kFast, bool kAmn, bool kBmn>
-__global__ void __launch_bounds__((2 + 16) * 32, 1)
-    gemm_i8s_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    const __grid_constant__ CUtensorMap tmSA, const __grid_constant__ CUtensorMap tmSB,
-                    const Params p, const int saT, const int sbT) {
-  constexpr int kEpi = 16;
+// ───────────────────────── gemm_tc_kernel (main) ─────────────────────────
+// Operand staging per stage (4 chunks):
+//   OP_I8 : A, B each one 128-row x 128-byte SW128 box (16 KB); K-major (row =
+//           M/N index, 128 K bytes) or MN-major (row = K index, 128 M/N bytes;
+//           the UMMA reads int8 MN-major tiles directly, so dgrad consumes W
+//           [d x c] and wgrad dY [n x d], X [n x c] as stored).  6 stages.
+//   OP_F16: A, B each two 128-row x 64-f16 SW128 boxes (32 KB), K-major.  3 stages.
+// Scales: per stage the 4x4 sub-grids of sA (row blocks x chunks) and sB, 64 B
+// each, by TMA into the stage's 256-byte scale slot.
+constexpr int kEpiTC = 16;  // promotion warps of gemm_tc_kernel
+
+template <int kOp>
+struct Cfg {
+  static constexpr int kStages = kOp == OP_I8 ? 6 : 3;
+  static constexpr uint32_t kStageBytes = kOp == OP_I8 ? BM * BK : 2 * BM * BK;  // per operand
+  static constexpr uint32_t kScaleBytes = 256;
+  static constexpr size_t kSmem = 1024 + (size_t)kStages * 2 * kStageBytes + kStages * kScaleBytes + sizeof(Bars) + 64;
+};
+
+// Warp layout: warp 0 TMA producer (sub-partition 0), warp 1 MMA issuer
+// (sub-partition 1), warps 2.. promotion.  Both control roles run their loops on
+// the whole warp (uniform loop state) and issue from one elected lane: the MMA
+// issuer shares sub-partition 1 with four promotion warps, and every instruction
+// it needs per chunk is an issue slot they lose (tools/gemm_trace.py: with a
+// lane-0-only issuer, sub-partition 1's warps trail the others by ~2 chunks and
+// gate every TMEM buffer release).  Measured and NOT kept (profiles/r2_gemm_ab.md):
+// one issuer per sub-partition (4 issuers, 20 warps) -- no skew, but slower;
+// software-pipelined TMEM loads (spills at the 96-register cap of 18 warps);
+// 64 columns per promotion warp (2 warps per sub-partition hide less latency).
+template <int kOp, bool kFast, bool kAmn, bool kBmn>
+__global__ void __launch_bounds__((2 + kEpiTC) * 32, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmSA, const __grid_constant__ CUtensorMap tmSB,
+                   const Params p, const int saT, const int sbT) {
+  using C = Cfg<kOp>;
+  constexpr int kStages = C::kStages;
+  constexpr int kEpi = kEpiTC;  // promotion warps
+  constexpr int kCols = 32;     // columns per promotion warp
+  constexpr int kBlk = 1;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t *base = reinterpret_cast<uint8_t *>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *sA = base;
-  uint8_t *sB = base + kStages * kStageBytesA;
-  uint8_t *sS = sB + kStages * kStageBytesB;  // scale boxes, 128-byte aligned
-  SmemS &S = *reinterpret_cast<SmemS *>(sS + kStages * kScaleBytes);
+  uint8_t *sB = base + kStages * C::kStageBytes;
+  uint8_t *sS = sB + kStages * C::kStageBytes;  // scale slots, 128-byte aligned
+  Bars &S = *reinterpret_cast<Bars *>(sS + kStages * C::kScaleBytes);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -442,6 +235,11 @@ __global__ void __launch_bounds__((2 + 16) * 32, 1)
   const int nstages_k = (int)(p.K / BK);
   const uint32_t bar_full = smem_u32(&S.full[0]), bar_empty = smem_u32(&S.empty[0]);
   const uint32_t bar_tfull = smem_u32(&S.tfull[0]), bar_tempty = smem_u32(&S.tempty[0]);
+  // warp roles
+  const int epi_w = warp - 2;  // promotion warp index
+  const bool is_tma = warp == 0;
+  const bool is_iss = warp == 1;
+  const int alloc_warp = 1;
 
   if (threadIdx.x == 0) {
     prefetch_tmap(&tmA);
@@ -450,7 +248,7 @@ __global__ void __launch_bounds__((2 + 16) * 32, 1)
     prefetch_tmap(&tmSB);
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&S.full[s], 1);
-      mbar_init(&S.empty[s], 1 + kEpi);
+      mbar_init(&S.empty[s], 1 + kEpi);  // the MMAs consumed the tiles AND every warp read the scales
     }
     for (int b = 0; b < kTmemBufs; ++b) {
       mbar_init(&S.tfull[b], 1);
@@ -458,35 +256,68 @@ __global__ void __launch_bounds__((2 + 16) * 32, 1)
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(&S.tmem_base, kTmemBufs * BN);
+  if (warp == alloc_warp) tmem_alloc(&S.tmem_base, kTmemBufs * BN);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = S.tmem_base;
 
-  if (warp == 0) {
-    // ───────────── TMA producer: int8 tiles + scale sub-grids ─────────────
-    if (lane == 0) {
+  // TMA loads of one stage (operand tiles + the 4x4 scale sub-grids)
+  auto tma_stage = [&](int stage, int64_t tile, int ks) {
+    const int m0 = (int)((tile % mt) * BM), n0 = (int)((tile / mt) * BN);
+    mbar_arrive_expect_tx(&S.full[stage], 2 * C::kStageBytes + 128);
+    uint8_t *a = sA + stage * C::kStageBytes, *b = sB + stage * C::kStageBytes;
+    // tensor-map coordinates are {inner, outer}
+    if constexpr (kOp == OP_F16) {
+      tma_load_2d(a, &tmA, &S.full[stage], ks * BK, m0);
+      tma_load_2d(a + C::kStageBytes / 2, &tmA, &S.full[stage], ks * BK + 64, m0);
+      tma_load_2d(b, &tmB, &S.full[stage], ks * BK, n0);
+      tma_load_2d(b + C::kStageBytes / 2, &tmB, &S.full[stage], ks * BK + 64, n0);
+    } else {
+      if (kAmn) tma_load_2d(a, &tmA, &S.full[stage], m0, ks * BK);
+      else tma_load_2d(a, &tmA, &S.full[stage], ks * BK, m0);
+      if (kBmn) tma_load_2d(b, &tmB, &S.full[stage], n0, ks * BK);
+      else tma_load_2d(b, &tmB, &S.full[stage], ks * BK, n0);
+    }
+    uint8_t *ss = sS + stage * C::kScaleBytes;
+    // box {4, 4}: K-contiguous grids -> [row block][chunk], else [chunk][row block]
+    if (saT) tma_load_2d(ss, &tmSA, &S.full[stage], m0 / 32, ks * 4);
+    else tma_load_2d(ss, &tmSA, &S.full[stage], ks * 4, m0 / 32);
+    if (sbT) tma_load_2d(ss + 128, &tmSB, &S.full[stage], n0 / 32, ks * 4);
+    else tma_load_2d(ss + 128, &tmSB, &S.full[stage], ks * 4, n0 / 32);
+  };
+  // one chunk's MMA(s): chunk c of stage `stage` -> TMEM buffer c
+  const uint64_t adesc0 = smem_desc_sw128(smem_u32(sA), 16, 1024);
+  const uint64_t bdesc0 = smem_desc_sw128(smem_u32(sB), 16, 1024);
+  auto mma_chunk = [&](int stage, int c) {
+    const uint64_t ad = adesc0 + (uint64_t)((stage * C::kStageBytes) >> 4);
+    const uint64_t bd = bdesc0 + (uint64_t)((stage * C::kStageBytes) >> 4);
+    if constexpr (kOp == OP_F16) {
+      constexpr uint32_t idesc = idesc_f16_f32(BM, BN);
+      // chunk c: box c/2, byte offset (c%2)*64 in the 128-byte row; K=16 step = 32 bytes
+      const uint32_t off = ((c >> 1) * (C::kStageBytes / 2) + (c & 1) * 64) >> 4;
+      mma_f16_ss(tmem + c * BN, ad + off, bd + off, idesc, 0u);
+      mma_f16_ss(tmem + c * BN, ad + off + 2, bd + off + 2, idesc, 1u);
+    } else {
+      constexpr uint32_t idesc = idesc_i8(BM, BN, kAmn ? 1 : 0, kBmn ? 1 : 0);
+      constexpr uint32_t kStepA = kAmn ? (32 * 128) >> 4 : 2;  // descriptor units (16 B) per chunk
+      constexpr uint32_t kStepB = kBmn ? (32 * 128) >> 4 : 2;
+      mma_i8_ss(tmem + c * BN, ad + kStepA * c, bd + kStepB * c, idesc, 0u);
+    }
+  };
+
+  if (is_tma) {
+    // ───────────── TMA producer (basic layout; whole warp, one elected lane issues) ─────────────
+    {
       int stage = 0;
       uint32_t phase = 0;
 #pragma unroll 1
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int m0 = (int)((tile % mt) * BM), n0 = (int)((tile / mt) * BN);
-#pragma unroll 1  // (control loops stay compact: they share the L0 I-cache with the promotion loop)
+#pragma unroll 1
         for (int ks = 0; ks < nstages_k; ++ks) {
-          ctl_wait(p, bar_empty + 8 * stage, phase ^ 1);
-          mbar_arrive_expect_tx(&S.full[stage], kStageBytesA + kStageBytesB + 128);
-          // tensor-map coordinates are {inner, outer}
-          if (kAmn) tma_load_2d(sA + stage * kStageBytesA, &tmA, &S.full[stage], m0, ks * BK);
-          else tma_load_2d(sA + stage * kStageBytesA, &tmA, &S.full[stage], ks * BK, m0);
-          if (kBmn) tma_load_2d(sB + stage * kStageBytesB, &tmB, &S.full[stage], n0, ks * BK);
-          else tma_load_2d(sB + stage * kStageBytesB, &tmB, &S.full[stage], ks * BK, n0);
-          uint8_t *ss = sS + stage * kScaleBytes;
-          // box {4, 4}: K-contiguous grids -> [row block][chunk], else [chunk][row block]
-          if (saT) tma_load_2d(ss, &tmSA, &S.full[stage], m0 / 32, ks * 4);
-          else tma_load_2d(ss, &tmSA, &S.full[stage], ks * 4, m0 / 32);
-          if (sbT) tma_load_2d(ss + 128, &tmSB, &S.full[stage], n0 / 32, ks * 4);
-          else tma_load_2d(ss + 128, &tmSB, &S.full[stage], ks * 4, n0 / 32);
+          ctl_wait(bar_empty + 8 * stage, phase ^ 1);
+          if (elect_one()) tma_stage(stage, tile, ks);
+          __syncwarp();
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
@@ -494,33 +325,35 @@ __global__ void __launch_bounds__((2 + 16) * 32, 1)
         }
       }
     }
-  } else if (warp == 1) {
-    // ───────────── MMA issuer: chunk c of every stage -> TMEM buffer c ─────────────
-    if (lane == 0) {
-      const uint64_t adesc0 = smem_desc_sw128(smem_u32(sA), 16, 1024);
-      const uint64_t bdesc0 = smem_desc_sw128(smem_u32(sB), 16, 1024);
-      constexpr uint32_t idesc = idesc_i8(BM, BN, kAmn ? 1 : 0, kBmn ? 1 : 0);
-      constexpr uint32_t kStepA = kAmn ? (32 * 128) >> 4 : 2;  // descriptor units (16 B) per chunk
-      constexpr uint32_t kStepB = kBmn ? (32 * 128) >> 4 : 2;
-      int stage = 0;
+  } else if (is_iss) {
+    // ───────────── single MMA issuer (whole warp): chunk c of every stage -> TMEM buffer c ─────────────
+    {
+      int stage = 0, gch = 0;
       uint32_t phase = 0, tphase = 0;
 #pragma unroll 1
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
 #pragma unroll 1
         for (int ks = 0; ks < nstages_k; ++ks) {
-          ctl_wait(p, bar_full + 8 * stage, phase);
+          ctl_wait(bar_full + 8 * stage, phase);
           tc_fence_after();
-          const uint64_t ad = adesc0 + (uint64_t)((stage * kStageBytesA) >> 4);
-          const uint64_t bd = bdesc0 + (uint64_t)((stage * kStageBytesB) >> 4);
 #pragma unroll
           for (int c = 0; c < kChunksPerStage; ++c) {
-            ctl_wait(p, bar_tempty + 8 * c, ((tphase >> c) & 1) ^ 1);
+            if (lane == 0) JF_TR(0, gch + c);
+            ctl_wait(bar_tempty + 8 * c, ((tphase >> c) & 1) ^ 1);
+            if (lane == 0) JF_TR(1, gch + c);
             tphase ^= 1u << c;
             tc_fence_after();
-            mma_i8_ss(tmem + c * BN, ad + kStepA * c, bd + kStepB * c, idesc, 0u);
-            mma_commit(&S.tfull[c]);
+            if (lane == 0) JF_TR(6, gch + c);
+            if (elect_one()) {
+              mma_chunk(stage, c);
+              mma_commit(&S.tfull[c]);
+            }
+            __syncwarp();
+            if (lane == 0) JF_TR(2, gch + c);
           }
-          mma_commit(&S.empty[stage]);
+          if (elect_one()) mma_commit(&S.empty[stage]);
+          __syncwarp();
+          gch += kChunksPerStage;
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
@@ -530,34 +363,44 @@ __global__ void __launch_bounds__((2 + 16) * 32, 1)
     }
   } else {
     // ───────────── promotion + epilogue ─────────────
-    const int lq = warp & 3;          // TMEM lane quarter == 32-row block of the tile
-    const int cg = (warp - 2) >> 2;   // 32-column group of the tile
-    const uint32_t tcol = tmem + ((uint32_t)(lq * 32) << 16) + cg * 32;
+    const int lq = warp & 3;              // TMEM lane quarter == 32-row block of the tile
+    const int cg = epi_w >> 2;            // column group: columns [cg*kCols, +kCols)
+    const uint32_t tcol = tmem + ((uint32_t)(lq * 32) << 16) + cg * kCols;
     const uint32_t ssa0 = smem_u32(sS), ssb0 = ssa0 + 128;
-    // float offsets of this warp's 4 scale factors inside the 4x4 boxes
+    // float offsets of this warp's scale factors inside the 4x4 boxes
     const uint32_t oa = saT ? (uint32_t)lq * 4 : (uint32_t)lq * 16;
-    const uint32_t ob = sbT ? (uint32_t)cg * 4 : (uint32_t)cg * 16;
-    const uint32_t da = saT ? 16 : 4, db = sbT ? 16 : 4;  // byte step between chunks
+    const uint32_t da = saT ? 16 : 4;  // byte step between chunks
+    const uint32_t db = sbT ? 16 : 4;
     uint32_t tphase = 0;
     int flags = 0;
     int stage = 0;
     uint32_t phase = 0;
+    constexpr bool kF32 = kOp == OP_F16;
+    const bool trw = epi_w == 0 && lane == 0;
+    int gch = 0;
+#pragma unroll 1
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       const int64_t I = (tile % mt) * (BM / 32) + lq;
-      const int64_t J = (tile / mt) * (BN / 32) + cg;
-      float acc[32];
+      const int64_t J0 = (tile / mt) * (BN / 32) + cg * kBlk;
+      float acc[kBlk][32];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) acc[j] = 0.0f;
-#pragma unroll 2
+      for (int q = 0; q < kBlk; ++q)
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[q][j] = 0.0f;
+#pragma unroll 1
       for (int ks = 0; ks < nstages_k; ++ks) {
         // the stage's scales: acquire the TMA writes, read, release the stage
         mbar_wait_u32(bar_full + 8 * stage, phase);
-        const uint32_t sa_addr = ssa0 + stage * kScaleBytes + oa, sb_addr = ssb0 + stage * kScaleBytes + ob;
-        float sav[4], sbv[4];
+        const uint32_t sa_addr = ssa0 + stage * C::kScaleBytes + oa;
+        const uint32_t sb_addr = ssb0 + stage * C::kScaleBytes;
+        float sav[4], sbv[kBlk][4];
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
           sav[b] = lds_f32(sa_addr + b * da);
-          sbv[b] = lds_f32(sb_addr + b * db);
+#pragma unroll
+          for (int q = 0; q < kBlk; ++q)
+            sbv[q][b] = lds_f32(sb_addr + (sbT ? (uint32_t)(cg * kBlk + q) * 4 : (uint32_t)(cg * kBlk + q) * 16) +
+                                b * db);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive_u32(bar_empty + 8 * stage);
@@ -567,75 +410,75 @@ __global__ void __launch_bounds__((2 + 16) * 32, 1)
         }
 #pragma unroll
         for (int b = 0; b < kTmemBufs; ++b) {
+          uint32_t r[kCols];
+          if (trw) JF_TR(3, gch + b);
           mbar_wait_u32(bar_tfull + 8 * b, (tphase >> b) & 1);
+          if (trw) JF_TR(4, gch + b);
           tphase ^= 1u << b;
           tc_fence_after();
-          uint32_t r[32];
           tmem_ld_32x32b_x32(tcol + b * BN, r);
-          tmem_wait_ld();
+          tmem_wait_ld_dep(r);
+          if (trw) JF_TR(5, gch + b);
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive_u32(bar_tempty + 8 * b);
-          promote32<kFast>(acc, r, sav[b], sbv[b], p.zero);
+#pragma unroll
+          for (int q = 0; q < kBlk; ++q) promote32<kFast, kF32>(acc[q], r + 32 * q, sav[b], sbv[q][b], p.zero);
+#ifdef JF_GEMM_TRACE
+          if (lane == 0 && epi_w < 16) JF_TR(8 + epi_w, gch + b + (int)(acc[0][0] == 1.2345f));  // (after the math)
+#endif
         }
+        gch += kTmemBufs;
       }
-      flags |= finish_block(p, acc, I, J, lane);
+#pragma unroll
+      for (int q = 0; q < kBlk; ++q) flags |= finish_block(p, acc[q], I, J0 + q, lane);
     }
     if (lane == 0) raise_flags(p.err, flags);
   }
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, kTmemBufs * BN);
+  if (warp == alloc_warp) tmem_dealloc(tmem, kTmemBufs * BN);
 }
 
-// ─────────────── gemm_f16s_kernel: f16-widened codes, kind::f16 MMA ───────────────
-// Same pipeline, scale staging and promotion as gemm_i8s_kernel (K-major A and
-// B), but the operands are the int8 codes widened to f16 in HBM
-// (jf_widen_codes): the f32 accumulator of the kind::f16 MMA holds the exact
-// integer partial (every product and partial sum is an integer below 2^20),
-// so the promotion skips the 32 I2F per chunk -- the kernel's issue-slot
-// bottleneck.  Bit-identical to the int8 kernels.  A stage (128 K) is two
-// 64-wide SW128 boxes per operand; a 32-deep chunk is two K=16 MMAs.
-constexpr int kStagesF = 3;
-constexpr uint32_t kBoxBytesF = 128 * 128;         // 128 rows x 64 f16
-constexpr uint32_t kStageBytesF = 2 * kBoxBytesF;  // per operand
-constexpr size_t kSmemBytesF = 1024 + kStagesF * 2 * kStageBytesF + kStagesF * kScaleBytes + sizeof(SmemS) + 64;
+// ───────────────────────── gemm_i8_kernel (generic shapes) ─────────────────────────
+// Same pipeline, K-major A and B ([rows x K] codes, row stride a multiple of 16),
+// scale grids read from global memory, partial tiles predicated.  kPartials:
+// the raw int32 partials of a single chunk (jf_gemm_partials, micro_mm_16).
+constexpr int kStagesG = 6;
+constexpr int kEpiG = 16;
+constexpr uint32_t kStageBytesG = BM * BK;
+constexpr size_t kSmemG = 1024 + kStagesG * 2 * kStageBytesG + sizeof(Bars) + 64;
 
-template <bool kFast>
-__global__ void __launch_bounds__((2 + 16) * 32, 1)
-    gemm_f16s_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const __grid_constant__ CUtensorMap tmSA, const __grid_constant__ CUtensorMap tmSB,
-                     const Params p, const int saT, const int sbT) {
-  constexpr int kEpi = 16;
+template <bool kFast, bool kPartials>
+__global__ void __launch_bounds__((2 + kEpiG) * 32, 1)
+    gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const Params p) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t *base = reinterpret_cast<uint8_t *>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *sA = base;
-  uint8_t *sB = base + kStagesF * kStageBytesF;
-  uint8_t *sS = sB + kStagesF * kStageBytesF;
-  SmemS &S = *reinterpret_cast<SmemS *>(sS + kStagesF * kScaleBytes);
+  uint8_t *sB = base + kStagesG * kStageBytesG;
+  Bars &S = *reinterpret_cast<Bars *>(sB + kStagesG * kStageBytesG);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int64_t mt = p.M / BM, nt = p.N / BN;
+  const int64_t mt = (p.M + BM - 1) / BM, nt = (p.N + BN - 1) / BN;
   const int64_t ntiles = mt * nt;
-  const int nstages_k = (int)(p.K / BK);
+  const int nchunks = (int)(p.K / 32);
+  const int nstages_k = (nchunks + kChunksPerStage - 1) / kChunksPerStage;
   const uint32_t bar_full = smem_u32(&S.full[0]), bar_empty = smem_u32(&S.empty[0]);
   const uint32_t bar_tfull = smem_u32(&S.tfull[0]), bar_tempty = smem_u32(&S.tempty[0]);
 
   if (threadIdx.x == 0) {
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
-    prefetch_tmap(&tmSA);
-    prefetch_tmap(&tmSB);
-    for (int s = 0; s < kStagesF; ++s) {
+    for (int s = 0; s < kStagesG; ++s) {
       mbar_init(&S.full[s], 1);
-      mbar_init(&S.empty[s], 1 + kEpi);
+      mbar_init(&S.empty[s], 1);
     }
     for (int b = 0; b < kTmemBufs; ++b) {
       mbar_init(&S.tfull[b], 1);
-      mbar_init(&S.tempty[b], kEpi);
+      mbar_init(&S.tempty[b], kEpiG);
     }
     fence_barrier_init();
   }
@@ -646,26 +489,17 @@ __global__ void __launch_bounds__((2 + 16) * 32, 1)
   const uint32_t tmem = S.tmem_base;
 
   if (warp == 0) {
-    // ───────────── TMA producer: f16 tiles (2 boxes each) + scale sub-grids ─────────────
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int m0 = (int)((tile % mt) * BM), n0 = (int)((tile / mt) * BN);
         for (int ks = 0; ks < nstages_k; ++ks) {
-          ctl_wait(p, bar_empty + 8 * stage, phase ^ 1);
-          mbar_arrive_expect_tx(&S.full[stage], 2 * kStageBytesF + 128);
-          uint8_t *a = sA + stage * kStageBytesF, *b = sB + stage * kStageBytesF;
-          tma_load_2d(a, &tmA, &S.full[stage], ks * BK, m0);
-          tma_load_2d(a + kBoxBytesF, &tmA, &S.full[stage], ks * BK + 64, m0);
-          tma_load_2d(b, &tmB, &S.full[stage], ks * BK, n0);
-          tma_load_2d(b + kBoxBytesF, &tmB, &S.full[stage], ks * BK + 64, n0);
-          uint8_t *ss = sS + stage * kScaleBytes;
-          if (saT) tma_load_2d(ss, &tmSA, &S.full[stage], m0 / 32, ks * 4);
-          else tma_load_2d(ss, &tmSA, &S.full[stage], ks * 4, m0 / 32);
-          if (sbT) tma_load_2d(ss + 128, &tmSB, &S.full[stage], n0 / 32, ks * 4);
-          else tma_load_2d(ss + 128, &tmSB, &S.full[stage], ks * 4, n0 / 32);
-          if (++stage == kStagesF) {
+          ctl_wait(bar_empty + 8 * stage, phase ^ 1);
+          mbar_arrive_expect_tx(&S.full[stage], 2 * kStageBytesG);
+          tma_load_2d(sA + stage * kStageBytesG, &tmA, &S.full[stage], ks * BK, m0);
+          tma_load_2d(sB + stage * kStageBytesG, &tmB, &S.full[stage], ks * BK, n0);
+          if (++stage == kStagesG) {
             stage = 0;
             phase ^= 1;
           }
@@ -673,32 +507,31 @@ __global__ void __launch_bounds__((2 + 16) * 32, 1)
       }
     }
   } else if (warp == 1) {
-    // ───────────── MMA issuer: chunk c -> TMEM buffer c, two K=16 MMAs ─────────────
     if (lane == 0) {
       const uint64_t adesc0 = smem_desc_sw128(smem_u32(sA), 16, 1024);
       const uint64_t bdesc0 = smem_desc_sw128(smem_u32(sB), 16, 1024);
-      constexpr uint32_t idesc = idesc_f16_f32(BM, BN);
+      constexpr uint32_t idesc = idesc_i8(BM, BN, 0, 0);
       int stage = 0;
       uint32_t phase = 0, tphase = 0;
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         for (int ks = 0; ks < nstages_k; ++ks) {
-          ctl_wait(p, bar_full + 8 * stage, phase);
+          ctl_wait(bar_full + 8 * stage, phase);
           tc_fence_after();
-          const uint64_t ad = adesc0 + (uint64_t)((stage * kStageBytesF) >> 4);
-          const uint64_t bd = bdesc0 + (uint64_t)((stage * kStageBytesF) >> 4);
+          const uint64_t ad = adesc0 + (uint64_t)((stage * kStageBytesG) >> 4);
+          const uint64_t bd = bdesc0 + (uint64_t)((stage * kStageBytesG) >> 4);
+          const int nch = min(kChunksPerStage, nchunks - ks * kChunksPerStage);
 #pragma unroll
           for (int c = 0; c < kChunksPerStage; ++c) {
-            ctl_wait(p, bar_tempty + 8 * c, ((tphase >> c) & 1) ^ 1);
-            tphase ^= 1u << c;
-            tc_fence_after();
-            // chunk c: box c/2, byte offset (c%2)*64 in the 128-byte row; K=16 step = 32 bytes
-            const uint32_t off = ((c >> 1) * kBoxBytesF + (c & 1) * 64) >> 4;
-            mma_f16_ss(tmem + c * BN, ad + off, bd + off, idesc, 0u);
-            mma_f16_ss(tmem + c * BN, ad + off + 2, bd + off + 2, idesc, 1u);
-            mma_commit(&S.tfull[c]);
+            if (c < nch) {
+              ctl_wait(bar_tempty + 8 * c, ((tphase >> c) & 1) ^ 1);
+              tphase ^= 1u << c;
+              tc_fence_after();
+              mma_i8_ss(tmem + c * BN, ad + 2 * c, bd + 2 * c, idesc, 0u);
+              mma_commit(&S.tfull[c]);
+            }
           }
           mma_commit(&S.empty[stage]);
-          if (++stage == kStagesF) {
+          if (++stage == kStagesG) {
             stage = 0;
             phase ^= 1;
           }
@@ -706,54 +539,55 @@ __global__ void __launch_bounds__((2 + 16) * 32, 1)
       }
     }
   } else {
-    // ───────────── promotion + epilogue (as gemm_i8s_kernel, f32 partials) ─────────────
     const int lq = warp & 3;
     const int cg = (warp - 2) >> 2;
     const uint32_t tcol = tmem + ((uint32_t)(lq * 32) << 16) + cg * 32;
-    const uint32_t ssa0 = smem_u32(sS), ssb0 = ssa0 + 128;
-    const uint32_t oa = saT ? (uint32_t)lq * 4 : (uint32_t)lq * 16;
-    const uint32_t ob = sbT ? (uint32_t)cg * 4 : (uint32_t)cg * 16;
-    const uint32_t da = saT ? 16 : 4, db = sbT ? 16 : 4;
     uint32_t tphase = 0;
     int flags = 0;
-    int stage = 0;
-    uint32_t phase = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       const int64_t I = (tile % mt) * (BM / 32) + lq;
       const int64_t J = (tile / mt) * (BN / 32) + cg;
+      const bool valid = I * 32 < p.M && J * 32 < p.N;
       float acc[32];
 #pragma unroll
       for (int j = 0; j < 32; ++j) acc[j] = 0.0f;
-      for (int ks = 0; ks < nstages_k; ++ks) {
-        mbar_wait_u32(bar_full + 8 * stage, phase);
-        const uint32_t sa_addr = ssa0 + stage * kScaleBytes + oa, sb_addr = ssb0 + stage * kScaleBytes + ob;
-        float sav[4], sbv[4];
+      const float *pa = p.sa + (kPartials || !valid ? 0 : I * p.sa_s0);
+      const float *pb = p.sb + (kPartials || !valid ? 0 : J * p.sb_s0);
+      for (int cb = 0; cb < nchunks; cb += kTmemBufs) {
+        float sav[4] = {0.f, 0.f, 0.f, 0.f}, sbv[4] = {0.f, 0.f, 0.f, 0.f};
+        if (!kPartials && valid) {
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          sav[b] = lds_f32(sa_addr + b * da);
-          sbv[b] = lds_f32(sb_addr + b * db);
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive_u32(bar_empty + 8 * stage);
-        if (++stage == kStagesF) {
-          stage = 0;
-          phase ^= 1;
+          for (int b = 0; b < kTmemBufs; ++b)
+            if (cb + b < nchunks) {
+              sav[b] = __ldg(pa + (cb + b) * p.sa_s1);
+              sbv[b] = __ldg(pb + (cb + b) * p.sb_s1);
+            }
         }
 #pragma unroll
         for (int b = 0; b < kTmemBufs; ++b) {
+          if (cb + b >= nchunks) break;
           mbar_wait_u32(bar_tfull + 8 * b, (tphase >> b) & 1);
           tphase ^= 1u << b;
           tc_fence_after();
           uint32_t r[32];
           tmem_ld_32x32b_x32(tcol + b * BN, r);
-          tmem_wait_ld();
+          tmem_wait_ld_dep(r);
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive_u32(bar_tempty + 8 * b);
-          promote32f<kFast>(acc, r, sav[b], sbv[b], p.zero);
+          if (kPartials) {
+            if (valid) {
+              int32_t *dst = reinterpret_cast<int32_t *>(p.yf) + (I * 32 + lane) * p.N + J * 32;
+#pragma unroll
+              for (int j = 0; j < 32; j += 4)
+                *reinterpret_cast<int4 *>(dst + j) = make_int4((int)r[j], (int)r[j + 1], (int)r[j + 2], (int)r[j + 3]);
+            }
+          } else {
+            promote32<kFast, false>(acc, r, sav[b], sbv[b], p.zero);
+          }
         }
       }
-      flags |= finish_block(p, acc, I, J, lane);
+      if (!kPartials && valid) flags |= finish_block(p, acc, I, J, lane);
     }
     if (lane == 0) raise_flags(p.err, flags);
   }
@@ -811,271 +645,6 @@ __global__ void __launch_bounds__(256) widen_codes_t_kernel(const int8_t *__rest
   d[1] = make_int4((int)o[4], (int)o[5], (int)o[6], (int)o[7]);
 }
 
-#ifdef JF_GEMM_TRACE
-#define JF_TR(ev, i)                                                                        \
-  do {                                                                                      \
-    if (blockIdx.x == 0 && (i) < 512 && p.trace) p.trace[(ev) * 512 + (i)] = clock64();     \
-  } while (0)
-#else
-#define JF_TR(ev, i) \
-  do {               \
-  } while (0)
-#endif
-
-// ─────────────── kind::f16 variant: int8 codes in HBM, f16 tiles in smem ───────────────
-// The tensor core's int32 output forces one I2F per output element per chunk
-// (ALU pipe, half rate): on B200 that, not the MMA, bounds the kind::i8
-// kernel (ncu: ALU 65% / issue 68% busy in fast mode, tensor 12%).  Here the
-// int8 codes are widened to f16 in shared memory (every code is exact in
-// binary16) and tcgen05.mma.kind::f16 accumulates in f32: each 32-deep chunk's
-// partial is an integer of magnitude <= 32*127^2 < 2^24, so the f32 partial
-// IS the int32 partial, exactly, and the promotion reads it without any
-// conversion.  The widening costs ~1.5 instructions per OPERAND element
-// (8192 per 128x128x32 chunk) instead of one I2F per OUTPUT element (16384).
-//   warps 0..15  promotion/epilogue (as in gemm_i8_kernel); warp 0 lane 0
-//                also issues the MMAs right after its TMEM slot is released
-//   warps 16..19 converters; warp 16 lane 0 is also the TMA producer
-namespace h16 {
-constexpr int BKH = 64;                       // K per stage (2 chunks)
-constexpr int kHStages = 3;                   // f16 ring depth (tensor-core operands)
-constexpr int kQStages = 8;                   // int8 ring depth (TMA lookahead)
-constexpr int kConvWarps = 4;
-constexpr int kWarps = kConvWarps + kEpiWarps;
-constexpr uint32_t kI8Bytes = BM * BKH;       // per operand per stage: 8 KB
-constexpr uint32_t kF16Bytes = BM * BKH * 2;  // 16 KB (128 rows x 128 B, SW128)
-struct Bars {
-  uint64_t full8[kQStages], empty8[kQStages], hfull[kHStages], hempty[kHStages];
-  uint64_t tfull[kPairSlots], tempty[kPairSlots];
-  uint32_t tmem_base;
-};
-constexpr size_t kSmemBytes = 1024 + kHStages * 2 * kF16Bytes + kQStages * 2 * kI8Bytes + 256;
-}  // namespace h16
-
-template <bool kFast, int kProbe = 0>  // diagnostics: kProbe 1 = converters skip the widening, 2 = no TMEM loads
-__global__ void __launch_bounds__(h16::kWarps * 32, 1)
-    gemm_h16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    const Params p) {
-  using namespace h16;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t *base = reinterpret_cast<uint8_t *>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t *hA = base;                              // f16 ring (1024-aligned for SW128)
-  uint8_t *hB = hA + kHStages * kF16Bytes;
-  uint8_t *qA = hB + kHStages * kF16Bytes;          // int8 ring (TMA, no swizzle)
-  uint8_t *qB = qA + kQStages * kI8Bytes;
-  Bars &S = *reinterpret_cast<Bars *>(qB + kQStages * kI8Bytes);
-
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const int64_t mt = (p.M + BM - 1) / BM, nt = (p.N + BN - 1) / BN;
-  const int64_t ntiles = mt * nt;
-  const int nchunks = (int)(p.K / 32);
-  const int nh = (nchunks + 1) / 2;  // stages (chunk pairs) per tile
-  const int my_tiles = (int)((ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x);
-  const int total = my_tiles * nh;   // stages this CTA streams
-  const uint32_t bar_full8 = smem_u32(&S.full8[0]), bar_empty8 = smem_u32(&S.empty8[0]);
-  const uint32_t bar_hfull = smem_u32(&S.hfull[0]), bar_hempty = smem_u32(&S.hempty[0]);
-  const uint32_t bar_tfull = smem_u32(&S.tfull[0]), bar_tempty = smem_u32(&S.tempty[0]);
-
-  if (threadIdx.x == 0) {
-    prefetch_tmap(&tmA);
-    prefetch_tmap(&tmB);
-    for (int s = 0; s < kQStages; ++s) {
-      mbar_init(&S.full8[s], 1);
-      mbar_init(&S.empty8[s], kConvWarps);
-    }
-    for (int s = 0; s < kHStages; ++s) {
-      mbar_init(&S.hfull[s], kConvWarps);
-      mbar_init(&S.hempty[s], 1);
-    }
-    for (int b = 0; b < kPairSlots; ++b) {
-      mbar_init(&S.tfull[b], 1);
-      mbar_init(&S.tempty[b], kEpiWarps);
-    }
-    fence_barrier_init();
-  }
-  if (warp == 0) tmem_alloc(&S.tmem_base, kTmemCols);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = S.tmem_base;
-
-  // Converters take the HIGHEST warp ids: the SMSP arbiter favours high warp
-  // ids, and the converters (plus the TMA producer among them) are the
-  // latency-critical producers; with low ids they starved behind the
-  // promotion warps (trace: 2.6k clk per stage vs ~0.3k of work).
-  const int cw = warp - kEpiWarps;  // converter index, valid when >= 0
-  if (cw >= 0) {
-    // ───────────── converters (converter 0 lane 0 is also the TMA producer) ─────────────
-    auto issue_tma = [&](int g) {
-      const int s = g % kQStages;
-      mbar_wait_u32(bar_empty8 + 8 * s, ((g / kQStages) & 1) ^ 1);
-      const int lt = g / nh, kh = g - lt * nh;
-      const int64_t tile = blockIdx.x + (int64_t)lt * gridDim.x;
-      const int m0 = (int)((tile % mt) * BM), n0 = (int)((tile / mt) * BN), k0 = kh * BKH;
-      mbar_arrive_expect_tx(&S.full8[s], 2 * kI8Bytes);
-      tma_load_2d(qA + s * kI8Bytes, &tmA, &S.full8[s], k0, m0);
-      tma_load_2d(qB + s * kI8Bytes, &tmB, &S.full8[s], k0, n0);
-    };
-    if (cw == 0 && lane == 0)
-      for (int g = 0; g < min(kQStages - 1, total); ++g) issue_tma(g);
-    __syncwarp();
-    const uint32_t q_base = smem_u32(qA), h_base = smem_u32(hA);
-    // item = (row of the 256 A|B rows, 16-byte source chunk c4 of its 64 bytes);
-    // thread handles rows 8*j + lane/4 of this warp's 64, chunk c4 = lane % 4
-    const int c4 = lane & 3;
-    for (int g = 0; g < total; ++g) {
-      const int s = g % kHStages, s8 = g % kQStages;
-      if (cw == 0 && lane == 0) JF_TR(0, g);
-      if (cw == 0 && lane == 0 && g + kQStages - 1 < total) issue_tma(g + kQStages - 1);
-      mbar_wait_u32(bar_full8 + 8 * s8, (g / kQStages) & 1);
-      if (cw == 0 && lane == 0) JF_TR(1, g);
-      mbar_wait_u32(bar_hempty + 8 * s, ((g / kHStages) & 1) ^ 1);
-      if (cw == 0 && lane == 0) JF_TR(2, g);
-      if (kProbe != 1) {
-        uint4 v[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int rl = cw * 64 + j * 8 + (lane >> 2);  // 0..255
-          const int isB = rl >> 7, r = rl & 127;
-          v[j] = lds128(q_base + (uint32_t)(isB * kQStages + s8) * kI8Bytes + r * BKH + c4 * 16);
-        }
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int rl = cw * 64 + j * 8 + (lane >> 2);
-          const int isB = rl >> 7, r = rl & 127;
-          const uint32_t row = h_base + (uint32_t)(isB * kHStages + s) * kF16Bytes + r * 128;
-          uint32_t h[8];
-          i8x4_to_f16x4(v[j].x, h[0], h[1]);
-          i8x4_to_f16x4(v[j].y, h[2], h[3]);
-          i8x4_to_f16x4(v[j].z, h[4], h[5]);
-          i8x4_to_f16x4(v[j].w, h[6], h[7]);
-          // f16 chunks 2*c4, 2*c4+1 of the row, 128-byte swizzle (chunk ^ row % 8)
-          sts128(row + (((2 * c4) ^ (r & 7)) << 4), h[0], h[1], h[2], h[3]);
-          sts128(row + (((2 * c4 + 1) ^ (r & 7)) << 4), h[4], h[5], h[6], h[7]);
-        }
-      }
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive_u32(bar_hfull + 8 * s);
-        mbar_arrive_u32(bar_empty8 + 8 * s8);
-      }
-      if (cw == 0 && lane == 0) JF_TR(3, g);
-    }
-  } else {
-    // ───────────── promotion + epilogue (warp 0 lane 0 also issues the MMAs) ─────────────
-    const int ew = warp;
-    const int lq = warp & 3;
-    const int cg = ew >> 2;
-    const uint32_t tcol = tmem + ((uint32_t)(lq * 32) << 16) + cg * 32;
-    const bool vec_scales = (p.sa_s1 == 1) && (p.sb_s1 == 1) && (nchunks % 4 == 0);
-    const bool issuer = (ew == 0) && (lane == 0);
-    const uint64_t adesc0 = smem_desc_sw128(smem_u32(hA), 16, 1024);
-    const uint64_t bdesc0 = smem_desc_sw128(smem_u32(hB), 16, 1024);
-    constexpr uint32_t idesc = idesc_f16_f32(BM, BN);
-    // MMAs of stage g (a chunk pair) into TMEM slot g % 2; slot must be free
-    auto issue_mma = [&](int g) {
-      const int s = g % kHStages;
-      const uint32_t slot = g & 1;
-      const bool two = 2 * (g % nh) + 1 < nchunks;
-      JF_TR(4, g);
-      mbar_wait_u32(bar_hfull + 8 * s, (g / kHStages) & 1);
-      JF_TR(5, g);
-      mbar_wait_u32(bar_tempty + 8 * slot, ((g >> 1) & 1) ^ 1);
-      JF_TR(6, g);
-      tc_fence_after();
-      const uint64_t ad = adesc0 + (uint64_t)((s * kF16Bytes) >> 4);
-      const uint64_t bd = bdesc0 + (uint64_t)((s * kF16Bytes) >> 4);
-      const uint32_t d0 = tmem + slot * (2 * BN);
-      // chunk 0: K 0..31 = row bytes 0..63 (two K=16 MMAs, +32 B each); chunk 1: bytes 64..127
-      mma_f16_ss(d0, ad, bd, idesc, 0u);
-      mma_f16_ss(d0, ad + 2, bd + 2, idesc, 1u);
-      if (two) {
-        mma_f16_ss(d0 + BN, ad + 4, bd + 4, idesc, 0u);
-        mma_f16_ss(d0 + BN, ad + 6, bd + 6, idesc, 1u);
-      }
-      mma_commit(&S.tfull[slot]);
-      mma_commit(&S.hempty[s]);
-    };
-    if (issuer)
-      for (int g = 0; g < min(kPairSlots, total); ++g) issue_mma(g);
-    __syncwarp();
-    uint32_t q = 0;
-    int flags = 0;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      const int64_t I = (tile % mt) * (BM / 32) + lq;
-      const int64_t J = (tile / mt) * (BN / 32) + cg;
-      const bool valid = (I * 32 < p.M) && (J * 32 < p.N);
-      float acc[32];
-#pragma unroll
-      for (int j = 0; j < 32; ++j) acc[j] = 0.0f;
-      const float *pa = p.sa + (valid ? I * p.sa_s0 : 0);
-      const float *pb = p.sb + (valid ? J * p.sb_s0 : 0);
-      float4 nsa = make_float4(0.f, 0.f, 0.f, 0.f), nsb = nsa;
-      auto load_scales = [&](int cb, float4 &a4, float4 &b4) {
-        if (!valid || cb >= nchunks) return;
-        if (vec_scales) {
-          a4 = __ldg(reinterpret_cast<const float4 *>(pa + cb));
-          b4 = __ldg(reinterpret_cast<const float4 *>(pb + cb));
-        } else {
-          float t[4], u[4];
-#pragma unroll
-          for (int b = 0; b < 4; ++b) {
-            t[b] = cb + b < nchunks ? __ldg(pa + (cb + b) * p.sa_s1) : 0.f;
-            u[b] = cb + b < nchunks ? __ldg(pb + (cb + b) * p.sb_s1) : 0.f;
-          }
-          a4 = make_float4(t[0], t[1], t[2], t[3]);
-          b4 = make_float4(u[0], u[1], u[2], u[3]);
-        }
-      };
-      load_scales(0, nsa, nsb);
-      for (int cb = 0; cb < nchunks; cb += 4) {
-        const float sav[4] = {nsa.x, nsa.y, nsa.z, nsa.w};
-        const float sbv[4] = {nsb.x, nsb.y, nsb.z, nsb.w};
-        load_scales(cb + 4, nsa, nsb);
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int c0 = cb + 2 * h;
-          if (c0 >= nchunks) break;
-          const bool two = c0 + 1 < nchunks;
-          const uint32_t slot = q & 1;
-          mbar_wait_u32(bar_tfull + 8 * slot, (q >> 1) & 1);
-          if (issuer) JF_TR(7, (int)q);
-          tc_fence_after();
-          uint32_t r[32];
-          const uint32_t t0 = tcol + slot * (2 * BN);
-          if (kProbe != 2) {
-            tmem_ld_32x32b_x32(t0, r);
-            tmem_wait_ld();
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) r[j] = __float_as_uint((float)(j + lane));
-          }
-          promote32f<kFast>(acc, r, sav[2 * h], sbv[2 * h], p.zero);
-          if (two && kProbe != 2) {
-            tmem_ld_32x32b_x32(t0 + BN, r);
-            tmem_wait_ld();
-          }
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive_u32(bar_tempty + 8 * slot);
-          if (issuer && (int)q + kPairSlots < total) issue_mma((int)q + kPairSlots);
-          __syncwarp();
-          ++q;
-          if (two) promote32f<kFast>(acc, r, sav[2 * h + 1], sbv[2 * h + 1], p.zero);
-        }
-      }
-      if (valid) flags |= finish_block(p, acc, I, J, lane);
-    }
-    if (lane == 0) raise_flags(p.err, flags);
-  }
-
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 0) tmem_dealloc(tmem, kTmemCols);
-}
-
 }  // namespace gemm
 }  // namespace jf
 
@@ -1085,6 +654,7 @@ using namespace jf;
 int jf_launch_check(const char *what);
 void jf_set_error(const char *msg);
 int jf_num_sms();
+int jf_set_smem_attr(const void *func, int bytes, const char *what);
 bool jf_make_tmap_i8(CUtensorMap *map, const void *ptr, int64_t rows, int64_t cols, int64_t ld,
                      int box_cols, int box_rows, bool swizzle128);
 bool jf_make_tmap_f32(CUtensorMap *map, const void *ptr, int64_t rows, int64_t cols, int64_t ld,
@@ -1092,184 +662,132 @@ bool jf_make_tmap_f32(CUtensorMap *map, const void *ptr, int64_t rows, int64_t c
 bool jf_make_tmap_f16(CUtensorMap *map, const void *ptr, int64_t rows, int64_t cols, int64_t ld,
                       int box_cols, int box_rows);
 
-#ifdef JF_GEMM_TRACE
-static long long *g_trace = nullptr;
-extern "C" int jf_gemm_trace_read(long long *host) {
-  if (!g_trace) return 1;
-  return cudaMemcpy(host, g_trace, 8 * 512 * sizeof(long long), cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 2;
-}
-#endif
-
-// Launch options (diagnostics / A-B experiments).  Defaults are the measured
-// best; JF_GEMM_IMPL / JF_GEMM_EPI / JF_GEMM_ISSUERS / JF_GEMM_CTL set them at
+// Launch options (diagnostics / A-B experiments; results are bit-identical for every
+// option).  Defaults are the measured best.  JF_GEMM_COLS / JF_GEMM_PIPE set them at
 // load time, jf_gemm_set_option() at run time.
 struct GemmOptions {
-  int impl = 0;      // 0 kind::i8, 1 kind::f16 (h16)
-  int epi = 16;      // promotion warps (16 or 8)
-  int issuers = 1;   // MMA issuer warps (1 or 3)
-  int ctl_kind = 1;  // control-thread wait flavour (see ctl_wait; JF_CTL_RUNTIME builds only)
-  int ctl_ns = 200;
-  int tma_scales = 1;  // gemm_i8s_kernel when the shape allows
-  GemmOptions() {
-    if (const char *e = getenv("JF_GEMM_IMPL")) impl = strcmp(e, "h16") == 0 ? 1 : 0;
-    if (const char *e = getenv("JF_GEMM_EPI")) epi = atoi(e) == 8 ? 8 : 16;
-    if (const char *e = getenv("JF_GEMM_ISSUERS")) issuers = atoi(e) == 3 ? 3 : 1;
-    if (const char *e = getenv("JF_GEMM_CTL")) sscanf(e, "%d,%d", &ctl_kind, &ctl_ns);
-  }
+  int tma_scales = 1;  // 0: every shape on the generic kernel
 };
 static GemmOptions g_opt;
 
 extern "C" int jf_gemm_set_option(const char *key, int value) {
-  if (!strcmp(key, "impl")) g_opt.impl = value ? 1 : 0;
-  else if (!strcmp(key, "epi")) g_opt.epi = value == 8 ? 8 : 16;
-  else if (!strcmp(key, "issuers")) g_opt.issuers = value == 3 ? 3 : 1;
-  else if (!strcmp(key, "ctl_kind")) g_opt.ctl_kind = value;
-  else if (!strcmp(key, "ctl_ns")) g_opt.ctl_ns = value;
-  else if (!strcmp(key, "tma_scales")) g_opt.tma_scales = value;
+  if (!strcmp(key, "tma_scales")) g_opt.tma_scales = value;
   else return JF_ERR_ARG;
   return JF_OK;
 }
 
-// gemm_i8s_kernel launch.  A is [M x K] (K-major) or [K x M] (a_mn: MN-major), row
-// stride lda bytes; likewise B as [N x K] or [K x N].  Returns -1 when the shape
-// or the scale-grid layout does not qualify (caller falls back).
-static int launch_i8s(const int8_t *A, bool a_mn, int64_t lda, const int8_t *B, bool b_mn, int64_t ldb, int64_t M,
-                      int64_t N, int64_t K, const float *sa, int64_t sa_s0, int64_t sa_s1, const float *sb,
-                      int64_t sb_s0, int64_t sb_s1, const float *bias, int mode, int out_kind, int8_t *yq,
-                      float *ys, void *yf, int32_t *err, cudaStream_t stream) {
+#ifdef JF_GEMM_TRACE
+static long long *g_trace = nullptr;
+extern "C" int jf_gemm_trace_read(long long *host) {
+  if (!g_trace) return 1;
+  return cudaMemcpy(host, g_trace, gemm::kTrEv * gemm::kTrChunks * sizeof(long long), cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 2;
+}
+#endif
+
+namespace {
+using TcFn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap, const gemm::Params,
+                      const int, const int);
+
+template <int kOp, bool kAmn, bool kBmn>
+TcFn pick_tc_mode(bool fast) {
+  using namespace jf::gemm;
+  return fast ? gemm_tc_kernel<kOp, true, kAmn, kBmn> : gemm_tc_kernel<kOp, false, kAmn, kBmn>;
+}
+
+bool grid_ok(const float *s, int64_t s0, int64_t s1) {
+  return ((uintptr_t)s % 16 == 0) && ((s1 == 1 && s0 % 4 == 0) || (s0 == 1 && s1 % 4 == 0));
+}
+
+// gemm_tc_kernel launch.  OP_I8: A is [M x K] (K-major) or [K x M] (a_mn: MN-major),
+// row stride lda elements; likewise B as [N x K] or [K x N].  OP_F16: K-major only.
+// Returns -1 when the shape or the scale-grid layout does not qualify (caller falls back).
+int launch_tc(int op, const void *A, bool a_mn, int64_t lda, const void *B, bool b_mn, int64_t ldb, int64_t M,
+              int64_t N, int64_t K, const float *sa, int64_t sa_s0, int64_t sa_s1, const float *sb, int64_t sb_s0,
+              int64_t sb_s1, const float *bias, int mode, int out_kind, int8_t *yq, float *ys, void *yf,
+              int32_t *err, cudaStream_t stream) {
   using namespace jf::gemm;
   if (!g_opt.tma_scales || out_kind == OUT_I32 || M % 128 || N % 128 || K % 128 || lda % 16 || ldb % 16 ||
-      (uintptr_t)A % 16 || (uintptr_t)B % 16)
+      (uintptr_t)A % 16 || (uintptr_t)B % 16 || !grid_ok(sa, sa_s0, sa_s1) || !grid_ok(sb, sb_s0, sb_s1))
     return -1;
-  // scale grids: each contiguous along K or along M/N, 16-byte row pitch
-  auto grid_ok = [](const float *s, int64_t s0, int64_t s1) {
-    return ((uintptr_t)s % 16 == 0) && ((s1 == 1 && s0 % 4 == 0) || (s0 == 1 && s1 % 4 == 0));
-  };
-  if (!grid_ok(sa, sa_s0, sa_s1) || !grid_ok(sb, sb_s0, sb_s1)) return -1;
+  if (op == OP_F16 && (a_mn || b_mn)) return -1;
   const int64_t kb = K / 32;
   const int saT = sa_s1 != 1, sbT = sb_s1 != 1;
   CUtensorMap ta, tb, tsa, tsb;
-  const bool ok =
-      (a_mn ? jf_make_tmap_i8(&ta, A, K, M, lda, BM, BK, true) : jf_make_tmap_i8(&ta, A, M, K, lda, BK, BM, true)) &&
-      (b_mn ? jf_make_tmap_i8(&tb, B, K, N, ldb, BN, BK, true) : jf_make_tmap_i8(&tb, B, N, K, ldb, BK, BN, true)) &&
-      (saT ? jf_make_tmap_f32(&tsa, sa, kb, M / 32, sa_s1, 4, 4) : jf_make_tmap_f32(&tsa, sa, M / 32, kb, sa_s0, 4, 4)) &&
-      (sbT ? jf_make_tmap_f32(&tsb, sb, kb, N / 32, sb_s1, 4, 4) : jf_make_tmap_f32(&tsb, sb, N / 32, kb, sb_s0, 4, 4));
-  if (!ok) return JF_ERR_LAUNCH;
-  Params p{M, N, K, sa, sa_s0, sa_s1, sb, sb_s0, sb_s1, bias, yq, ys, (float *)yf, err, out_kind, 0.0f, nullptr,
-           g_opt.ctl_kind, (uint32_t)g_opt.ctl_ns};
-  const bool fast = mode == JF_MODE_FAST;
-  using KFn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap, const Params,
-                       const int, const int);
-  KFn ks;
-  int ki;
-  if (!a_mn && !b_mn) {
-    ks = fast ? gemm_i8s_kernel<true, false, false> : gemm_i8s_kernel<false, false, false>;
-    ki = 0;
-  } else if (!a_mn && b_mn) {
-    ks = fast ? gemm_i8s_kernel<true, false, true> : gemm_i8s_kernel<false, false, true>;
-    ki = 1;
-  } else if (a_mn && b_mn) {
-    ks = fast ? gemm_i8s_kernel<true, true, true> : gemm_i8s_kernel<false, true, true>;
-    ki = 2;
+  bool ok;
+  if (op == OP_F16) {
+    ok = jf_make_tmap_f16(&ta, A, M, K, lda, 64, BM) && jf_make_tmap_f16(&tb, B, N, K, ldb, 64, BN);
   } else {
-    return -1;
+    ok = (a_mn ? jf_make_tmap_i8(&ta, A, K, M, lda, BM, BK, true) : jf_make_tmap_i8(&ta, A, M, K, lda, BK, BM, true)) &&
+         (b_mn ? jf_make_tmap_i8(&tb, B, K, N, ldb, BN, BK, true) : jf_make_tmap_i8(&tb, B, N, K, ldb, BK, BN, true));
   }
-  static bool done[3][2] = {};
-  if (!done[ki][fast]) {
-    if (cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytesS) != cudaSuccess)
-      return jf_launch_check("gemm_i8s attr");
-    done[ki][fast] = true;
+  ok = ok &&
+       (saT ? jf_make_tmap_f32(&tsa, sa, kb, M / 32, sa_s1, 4, 4) : jf_make_tmap_f32(&tsa, sa, M / 32, kb, sa_s0, 4, 4)) &&
+       (sbT ? jf_make_tmap_f32(&tsb, sb, kb, N / 32, sb_s1, 4, 4) : jf_make_tmap_f32(&tsb, sb, N / 32, kb, sb_s0, 4, 4));
+  if (!ok) return JF_ERR_LAUNCH;
+  Params p{M, N, K, sa, sa_s0, sa_s1, sb, sb_s0, sb_s1, bias, yq, ys, (float *)yf, err, out_kind, 0.0f, nullptr};
+#ifdef JF_GEMM_TRACE
+  if (!g_trace) cudaMalloc(&g_trace, gemm::kTrEv * gemm::kTrChunks * sizeof(long long));
+  cudaMemsetAsync(g_trace, 0, gemm::kTrEv * gemm::kTrChunks * sizeof(long long), stream);
+  p.trace = g_trace;
+#endif
+  const bool fast = mode == JF_MODE_FAST;
+  TcFn k;
+  size_t smem;
+  if (op == OP_F16) {
+    k = pick_tc_mode<OP_F16, false, false>(fast);
+    smem = Cfg<OP_F16>::kSmem;
+  } else {
+    if (!a_mn && !b_mn) k = pick_tc_mode<OP_I8, false, false>(fast);
+    else if (!a_mn && b_mn) k = pick_tc_mode<OP_I8, false, true>(fast);
+    else if (a_mn && b_mn) k = pick_tc_mode<OP_I8, true, true>(fast);
+    else return -1;
+    smem = Cfg<OP_I8>::kSmem;
   }
+  if (int rc = jf_set_smem_attr((const void *)k, (int)smem, "gemm_tc attr")) return rc;
   const int64_t tiles = (M / BM) * (N / BN);
   const int grid = (int)(tiles < jf_num_sms() ? tiles : jf_num_sms());
-  ks<<<grid, 18 * 32, kSmemBytesS, stream>>>(ta, tb, tsa, tsb, p, saT, sbT);
-  return jf_launch_check("gemm_i8s");
+  const int threads = (2 + kEpiTC) * 32;
+  k<<<grid, threads, smem, stream>>>(ta, tb, tsa, tsb, p, saT, sbT);
+  return jf_launch_check("gemm_tc");
 }
+}  // namespace
 
 // Core launcher: A [M x K] (row stride lda), Bt [N x K] (row stride ldb), both K-major codes.
-int jf_gemm_launch(const int8_t *A, int64_t lda, const int8_t *Bt, int64_t ldb, int64_t M,
-                   int64_t N, int64_t K, const float *sa, int64_t sa_s0, int64_t sa_s1,
-                   const float *sb, int64_t sb_s0, int64_t sb_s1, const float *bias, int mode,
-                   int out_kind, int8_t *yq, float *ys, void *yf, int32_t *err,
+int jf_gemm_launch(const int8_t *A, int64_t lda, const int8_t *Bt, int64_t ldb, int64_t M, int64_t N, int64_t K,
+                   const float *sa, int64_t sa_s0, int64_t sa_s1, const float *sb, int64_t sb_s0, int64_t sb_s1,
+                   const float *bias, int mode, int out_kind, int8_t *yq, float *ys, void *yf, int32_t *err,
                    cudaStream_t stream) {
   using namespace jf::gemm;
   if (M <= 0 || N <= 0 || K <= 0 || M % 32 || N % 32 || K % 32 || lda % 16 || ldb % 16) {
     jf_set_error("gemm: dims must be positive multiples of 32, strides multiples of 16");
     return JF_ERR_ARG;
   }
-  const bool h16p = g_opt.impl == 1 && out_kind != OUT_I32;
-  CUtensorMap ta, tb;
-  if (h16p) {
-    if (!jf_make_tmap_i8(&ta, A, M, K, lda, h16::BKH, BM, false) ||
-        !jf_make_tmap_i8(&tb, Bt, N, K, ldb, h16::BKH, BN, false))
-      return JF_ERR_LAUNCH;
-  } else if (!jf_make_tmap_i8(&ta, A, M, K, lda, BK, BM, true) ||
-             !jf_make_tmap_i8(&tb, Bt, N, K, ldb, BK, BN, true)) {
-    return JF_ERR_LAUNCH;
+  const bool partials = out_kind == OUT_I32;
+  if (!partials) {
+    const int rc = launch_tc(OP_I8, A, false, lda, Bt, false, ldb, M, N, K, sa, sa_s0, sa_s1, sb, sb_s0, sb_s1, bias,
+                             mode, out_kind, yq, ys, yf, err, stream);
+    if (rc >= 0) return rc;
   }
-  Params p{M, N, K, sa, sa_s0, sa_s1, sb, sb_s0, sb_s1, bias, yq, ys, (float *)yf, err, out_kind, 0.0f, nullptr,
-           g_opt.ctl_kind, (uint32_t)g_opt.ctl_ns};
-#ifdef JF_GEMM_TRACE
-  if (!g_trace) cudaMalloc(&g_trace, 8 * 512 * sizeof(long long));
-  cudaMemsetAsync(g_trace, 0, 8 * 512 * sizeof(long long), stream);
-  p.trace = g_trace;
-#endif
+  CUtensorMap ta, tb;
+  if (!jf_make_tmap_i8(&ta, A, M, K, lda, BK, BM, true) || !jf_make_tmap_i8(&tb, Bt, N, K, ldb, BK, BN, true))
+    return JF_ERR_LAUNCH;
+  Params p{M, N, K, sa, sa_s0, sa_s1, sb, sb_s0, sb_s1, bias, yq, ys, (float *)yf, err, out_kind, 0.0f, nullptr};
   const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   const int grid = (int)(tiles < jf_num_sms() ? tiles : jf_num_sms());
   const bool fast = mode == JF_MODE_FAST;
-  const bool partials = out_kind == OUT_I32;
-  if (h16p) {
-    void (*hk)(const CUtensorMap, const CUtensorMap, const Params) =
-        fast ? gemm_h16_kernel<true> : gemm_h16_kernel<false>;
-    static bool hdone[2] = {};
-    if (!hdone[fast]) {
-      if (cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h16::kSmemBytes) !=
-          cudaSuccess)
-        return jf_launch_check("gemm_h16 attr");
-      hdone[fast] = true;
-    }
-    hk<<<grid, h16::kWarps * 32, h16::kSmemBytes, stream>>>(ta, tb, p);
-    return jf_launch_check("gemm_h16");
-  }
-  if (!partials && !h16p) {
-    const int rc = launch_i8s(A, false, lda, Bt, false, ldb, M, N, K, sa, sa_s0, sa_s1, sb, sb_s0, sb_s1, bias,
-                              mode, out_kind, yq, ys, yf, err, stream);
-    if (rc >= 0) return rc;
-  }
-  const int epi = g_opt.epi, iss_env = g_opt.issuers;
-  // multi-issuer pipeline needs whole 4-chunk stages (K % 128 == 0)
-  const int iss = (!partials && K % BK == 0) ? iss_env : 1;
-  void (*kern)(const CUtensorMap, const CUtensorMap, const Params);
-#define JF_PICK(E, IS)                                                                 \
-  kern = partials ? gemm_i8_kernel<false, true, E, 1>                                  \
-                  : (fast ? gemm_i8_kernel<true, false, E, IS> : gemm_i8_kernel<false, false, E, IS>);
-  if (epi == 16) {
-    if (iss == 3) { JF_PICK(16, 3) } else { JF_PICK(16, 1) }
-  } else {
-    if (iss == 3) { JF_PICK(8, 3) } else { JF_PICK(8, 1) }
-  }
-#undef JF_PICK
-  static bool attr_done[2][2][3] = {};
-  const int ki = partials ? 2 : (fast ? 1 : 0);
-  bool &done = attr_done[epi == 16][iss == 3][ki];
-  if (!done) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes) !=
-        cudaSuccess)
-      return jf_launch_check("gemm attr");
-    done = true;
-  }
-  const int threads = (1 + iss + epi) * 32;
-  kern<<<grid, threads, kSmemBytes, stream>>>(ta, tb, p);
+  void (*kern)(const CUtensorMap, const CUtensorMap, const Params) =
+      partials ? gemm_i8_kernel<false, true> : (fast ? gemm_i8_kernel<true, false> : gemm_i8_kernel<false, false>);
+  if (int rc = jf_set_smem_attr((const void *)kern, (int)kSmemG, "gemm attr")) return rc;
+  kern<<<grid, (2 + kEpiG) * 32, kSmemG, stream>>>(ta, tb, p);
   return jf_launch_check("gemm_i8");
 }
 
-extern "C" int jf_gemm_fwd(const int8_t *x, const float *xs, const int8_t *w, const float *ws,
-                           const float *bias, int64_t n, int64_t c, int64_t d, int32_t mode,
-                           int32_t out_kind, int8_t *yq, float *ys, float *yf, int32_t *err,
-                           jf_stream_t stream) {
+extern "C" int jf_gemm_fwd(const int8_t *x, const float *xs, const int8_t *w, const float *ws, const float *bias,
+                           int64_t n, int64_t c, int64_t d, int32_t mode, int32_t out_kind, int8_t *yq, float *ys,
+                           float *yf, int32_t *err, jf_stream_t stream) {
   const int64_t cb = c / 32;
-  return jf_gemm_launch(x, c, w, c, n, d, c, xs, cb, 1, ws, cb, 1, bias, mode, out_kind, yq, ys,
-                        yf, err, (cudaStream_t)stream);
+  return jf_gemm_launch(x, c, w, c, n, d, c, xs, cb, 1, ws, cb, 1, bias, mode, out_kind, yq, ys, yf, err,
+                        (cudaStream_t)stream);
 }
 
 extern "C" size_t jf_gemm_scratch_bytes(int32_t which, int64_t n, int64_t d, int64_t c) {
@@ -1277,14 +795,14 @@ extern "C" size_t jf_gemm_scratch_bytes(int32_t which, int64_t n, int64_t d, int
   return (size_t)(n * d + n * c);
 }
 
-extern "C" int jf_gemm_dgrad(const int8_t *dy, const float *dys, const int8_t *w, const float *ws,
-                             const int8_t *wt, const float *wts, int64_t n, int64_t d, int64_t c,
-                             int32_t mode, int32_t out_kind, int8_t *dxq, float *dxs, float *dxf,
-                             void *scratch, int32_t *err, jf_stream_t stream) {
+extern "C" int jf_gemm_dgrad(const int8_t *dy, const float *dys, const int8_t *w, const float *ws, const int8_t *wt,
+                             const float *wts, int64_t n, int64_t d, int64_t c, int32_t mode, int32_t out_kind,
+                             int8_t *dxq, float *dxs, float *dxf, void *scratch, int32_t *err, jf_stream_t stream) {
+  using namespace jf::gemm;
   // W [d x c] is the MN-major B operand as stored (no W^T needed)
   {
-    const int rc = launch_i8s(dy, false, d, w, true, c, n, c, d, dys, d / 32, 1, ws, 1, c / 32, nullptr, mode,
-                              out_kind, dxq, dxs, dxf, err, (cudaStream_t)stream);
+    const int rc = launch_tc(OP_I8, dy, false, d, w, true, c, n, c, d, dys, d / 32, 1, ws, 1, c / 32, nullptr, mode,
+                             out_kind, dxq, dxs, dxf, err, (cudaStream_t)stream);
     if (rc >= 0) return rc;
   }
   if (wt == nullptr) {
@@ -1297,21 +815,21 @@ extern "C" int jf_gemm_dgrad(const int8_t *dy, const float *dys, const int8_t *w
   }
   // A = dY [n x d] (K = d), Bt = W^T [c x d]; sB(ci, J) = W.scales[ci, J] = W^T.scales[J, ci]
   if (wts != nullptr)
-    return jf_gemm_launch(dy, d, wt, d, n, c, d, dys, d / 32, 1, wts, d / 32, 1, nullptr, mode,
-                          out_kind, dxq, dxs, dxf, err, (cudaStream_t)stream);
-  return jf_gemm_launch(dy, d, wt, d, n, c, d, dys, d / 32, 1, ws, 1, c / 32, nullptr, mode,
-                        out_kind, dxq, dxs, dxf, err, (cudaStream_t)stream);
+    return jf_gemm_launch(dy, d, wt, d, n, c, d, dys, d / 32, 1, wts, d / 32, 1, nullptr, mode, out_kind, dxq, dxs,
+                          dxf, err, (cudaStream_t)stream);
+  return jf_gemm_launch(dy, d, wt, d, n, c, d, dys, d / 32, 1, ws, 1, c / 32, nullptr, mode, out_kind, dxq, dxs, dxf,
+                        err, (cudaStream_t)stream);
 }
 
-extern "C" int jf_gemm_wgrad(const int8_t *dy, const float *dys, const int8_t *x, const float *xs,
-                             const int8_t *dyt, const float *dyts, const int8_t *xt,
-                             const float *xts, int64_t n, int64_t d, int64_t c, int32_t mode,
-                             int32_t out_kind, int8_t *dwq, float *dws, float *dwf, void *scratch,
+extern "C" int jf_gemm_wgrad(const int8_t *dy, const float *dys, const int8_t *x, const float *xs, const int8_t *dyt,
+                             const float *dyts, const int8_t *xt, const float *xts, int64_t n, int64_t d, int64_t c,
+                             int32_t mode, int32_t out_kind, int8_t *dwq, float *dws, float *dwf, void *scratch,
                              int32_t *err, jf_stream_t stream) {
+  using namespace jf::gemm;
   // dY [n x d] and X [n x c] are the MN-major A and B operands as stored (no transposes)
   {
-    const int rc = launch_i8s(dy, true, d, x, true, c, d, c, n, dys, 1, d / 32, xs, 1, c / 32, nullptr, mode,
-                              out_kind, dwq, dws, dwf, err, (cudaStream_t)stream);
+    const int rc = launch_tc(OP_I8, dy, true, d, x, true, c, d, c, n, dys, 1, d / 32, xs, 1, c / 32, nullptr, mode,
+                             out_kind, dwq, dws, dwf, err, (cudaStream_t)stream);
     if (rc >= 0) return rc;
   }
   int8_t *s8 = static_cast<int8_t *>(scratch);
@@ -1336,17 +854,16 @@ extern "C" int jf_gemm_wgrad(const int8_t *dy, const float *dys, const int8_t *x
   const int64_t sa0 = dyts ? n / 32 : 1, sa1 = dyts ? 1 : d / 32;
   const float *sb = xts ? xts : xs;
   const int64_t sb0 = xts ? n / 32 : 1, sb1 = xts ? 1 : c / 32;
-  return jf_gemm_launch(dyt, n, xt, n, d, c, n, sa, sa0, sa1, sb, sb0, sb1, nullptr, mode,
-                        out_kind, dwq, dws, dwf, err, (cudaStream_t)stream);
+  return jf_gemm_launch(dyt, n, xt, n, d, c, n, sa, sa0, sa1, sb, sb0, sb1, nullptr, mode, out_kind, dwq, dws, dwf,
+                        err, (cudaStream_t)stream);
 }
 
-extern "C" int jf_gemm_partials(const int8_t *a, const int8_t *bt, int64_t m, int64_t n,
-                                int64_t k, int64_t kblk, int32_t *out, jf_stream_t stream) {
+extern "C" int jf_gemm_partials(const int8_t *a, const int8_t *bt, int64_t m, int64_t n, int64_t k, int64_t kblk,
+                                int32_t *out, jf_stream_t stream) {
   if (kblk < 0 || kblk * 32 >= k) return JF_ERR_ARG;
   // K restricted to one chunk via pointer offset + row stride = k
-  return jf_gemm_launch(a + kblk * 32, k, bt + kblk * 32, k, m, n, 32, nullptr, 0, 0, nullptr, 0,
-                        0, nullptr, JF_MODE_EXACT, jf::gemm::OUT_I32, nullptr, nullptr, out,
-                        nullptr, (cudaStream_t)stream);
+  return jf_gemm_launch(a + kblk * 32, k, bt + kblk * 32, k, m, n, 32, nullptr, 0, 0, nullptr, 0, 0, nullptr,
+                        JF_MODE_EXACT, jf::gemm::OUT_I32, nullptr, nullptr, out, nullptr, (cudaStream_t)stream);
 }
 
 // ─────────────── f16-widened operand path (C ABI) ───────────────
@@ -1371,38 +888,18 @@ extern "C" int jf_widen_codes(const int8_t *x, int64_t rows, int64_t cols, uint1
 
 extern "C" int jf_gemm_f16(const uint16_t *a, const float *sa, int64_t sa_s0, int64_t sa_s1, const uint16_t *b,
                            const float *sb, int64_t sb_s0, int64_t sb_s1, const float *bias, int64_t m, int64_t n,
-                           int64_t k, int32_t mode, int32_t out_kind, int8_t *yq, float *ys, float *yf,
-                           int32_t *err, jf_stream_t stream) {
+                           int64_t k, int32_t mode, int32_t out_kind, int8_t *yq, float *ys, float *yf, int32_t *err,
+                           jf_stream_t stream) {
   using namespace jf::gemm;
-  auto grid_ok = [](const float *s, int64_t s0, int64_t s1) {
-    return ((uintptr_t)s % 16 == 0) && ((s1 == 1 && s0 % 4 == 0) || (s0 == 1 && s1 % 4 == 0));
-  };
-  if (m <= 0 || n <= 0 || k <= 0 || m % 128 || n % 128 || k % 128 || (uintptr_t)a % 16 || (uintptr_t)b % 16 ||
-      !grid_ok(sa, sa_s0, sa_s1) || !grid_ok(sb, sb_s0, sb_s1) || out_kind == OUT_I32) {
+  if (m <= 0 || n <= 0 || k <= 0 || out_kind == OUT_I32) {
+    jf_set_error("gemm_f16: dims must be positive");
+    return JF_ERR_ARG;
+  }
+  const int rc = launch_tc(OP_F16, a, false, k, b, false, k, m, n, k, sa, sa_s0, sa_s1, sb, sb_s0, sb_s1, bias, mode,
+                           out_kind, yq, ys, yf, err, (cudaStream_t)stream);
+  if (rc < 0) {
     jf_set_error("gemm_f16: dims must be multiples of 128, scale grids contiguous along one axis");
     return JF_ERR_ARG;
   }
-  const int64_t kb = k / 32;
-  const int saT = sa_s1 != 1, sbT = sb_s1 != 1;
-  CUtensorMap ta, tb, tsa, tsb;
-  const bool ok = jf_make_tmap_f16(&ta, a, m, k, k, 64, BM) && jf_make_tmap_f16(&tb, b, n, k, k, 64, BN) &&
-                  (saT ? jf_make_tmap_f32(&tsa, sa, kb, m / 32, sa_s1, 4, 4)
-                       : jf_make_tmap_f32(&tsa, sa, m / 32, kb, sa_s0, 4, 4)) &&
-                  (sbT ? jf_make_tmap_f32(&tsb, sb, kb, n / 32, sb_s1, 4, 4)
-                       : jf_make_tmap_f32(&tsb, sb, n / 32, kb, sb_s0, 4, 4));
-  if (!ok) return JF_ERR_LAUNCH;
-  Params p{m, n, k, sa, sa_s0, sa_s1, sb, sb_s0, sb_s1, bias, yq, ys, yf, err, out_kind, 0.0f, nullptr,
-           g_opt.ctl_kind, (uint32_t)g_opt.ctl_ns};
-  const bool fast = mode == JF_MODE_FAST;
-  auto kf = fast ? gemm_f16s_kernel<true> : gemm_f16s_kernel<false>;
-  static bool done[2] = {};
-  if (!done[fast]) {
-    if (cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytesF) != cudaSuccess)
-      return jf_launch_check("gemm_f16s attr");
-    done[fast] = true;
-  }
-  const int64_t tiles = (m / BM) * (n / BN);
-  const int grid = (int)(tiles < jf_num_sms() ? tiles : jf_num_sms());
-  kf<<<grid, 18 * 32, kSmemBytesF, (cudaStream_t)stream>>>(ta, tb, tsa, tsb, p, saT, sbT);
-  return jf_launch_check("gemm_f16s");
+  return rc;
 }

@@ -1,13 +1,14 @@
-"""CTA-0 event timeline of the f16-path GEMM (JF_GEMM_IMPL=h16; diagnostics; needs `make trace`).
+"""CTA-0 event timeline of gemm_tc_kernel (diagnostics; needs `make trace`).
 
-python tools/gemm_trace.py [--shape proj] [--mode fast]
-Loads libjetfire_trace.so in place of libjetfire.so, runs one GEMM, and
-prints per-stage clock deltas: converter (stage start -> int8 ready ->
-f16 slot free -> converted), MMA issuer (hfull wait, tempty wait) and the
-epilogue's tfull arrival.
+python tools/gemm_trace.py [--shape mlp1] [--mode fast] [--operands int8|f16]
+Loads libjetfire_trace.so in place of libjetfire.so, runs one GEMM and prints, per
+chunk, clock64 deltas of the pipeline events: MMA issuer (tempty wait, issue) and
+promotion warp 2 (tfull wait, TMEM load, promotion) plus warp 17's promotion end,
+and the steady-state averages.
 """
 import argparse
 import ctypes
+import json
 import os
 import sys
 
@@ -19,45 +20,54 @@ sys.path.insert(0, ROOT)
 from paper_2403_12422_b200 import _lib  # noqa: E402
 
 SHAPES = {"proj": (4096, 4096, 4096), "mlp1": (4096, 4096, 16384)}
+NAMES = ["iss_wait", "iss_free", "iss_done", "w2_wait", "w2_full", "w2_data", "w2_done", "w17_done"]
 
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--shape", default="proj")
+    ap.add_argument("--shape", default="mlp1")
     ap.add_argument("--mode", default="fast")
-    ap.add_argument("--impl", default="h16", choices=["h16"])
+    ap.add_argument("--operands", default="int8")
     a = ap.parse_args()
-    os.environ["JF_GEMM_IMPL"] = a.impl
     _lib.load_library(os.path.join(ROOT, "paper_2403_12422_b200", "libjetfire_trace.so"))
     import paper_2403_12422_b200 as jf
 
+    jf.runtime.set_gemm_operands(a.operands)
     n, c, d = SHAPES[a.shape]
     x = jf.quantize_per_block(torch.randn(n, c, device="cuda"))
     w = jf.quantize_per_block(torch.randn(d, c, device="cuda") * c ** -0.5)
     for _ in range(2):
         jf.block_mm_forward(x, w, promotion=a.mode)
     torch.cuda.synchronize()
-    buf = np.zeros(8 * 512, dtype=np.int64)
+    buf = np.zeros(32 * 256, dtype=np.int64)
     rc = _lib.lib().jf_gemm_trace_read(ctypes.c_void_p(buf.ctypes.data))
     assert rc == 0, rc
-    t = buf.reshape(8, 512).astype(np.float64)
-    t0 = t[t > 0].min()
-    names = ["conv_start", "int8_ready", "f16_free", "converted", "iss_start", "hfull_ok", "tempty_ok", "epi_tfull"]
-    print("stage " + " ".join(f"{n:>10}" for n in names))
-    for g in list(range(0, 12)) + list(range(100, 112)):
-        print(f"{g:5d} " + " ".join(f"{(t[e, g] - t0) if t[e, g] else float('nan'):10.0f}" for e in range(8)))
-    # steady-state averages over stages 50..400
-    rng = slice(50, 400)
+    t = buf.reshape(32, 256).astype(np.float64)
+    rng = slice(32, 240)
+    done = t[8:24, rng]                       # promotion end per warp (16) per chunk
+    ok = (done > 0).all(axis=0)
+    done = done[:, ok]
+    period = float(np.diff(done.mean(axis=0)).mean())
+    # lag of each promotion warp behind the earliest one, per chunk (clk), averaged
+    lag = (done - done.min(axis=0)).mean(axis=1)
+    sp = [(w + 2) % 4 for w in range(16)]
+    by_sp = {f"sp{q}": round(float(np.mean([lag[w] for w in range(16) if sp[w] == q])), 1) for q in range(4)}
+    iss = t[0:3, rng]
+    oki = (iss > 0).all(axis=0)
+    sp = [((w + 2) % 4) if os.environ.get("JF_GEMM_MULTI", "1") == "0" else (w % 4) for w in range(16)]
+    by_sp = {f"sp{q}": round(float(np.mean([lag[w] for w in range(16) if sp[w] == q])), 1) for q in range(4)}
+    out = {"shape": a.shape, "mode": a.mode, "operands": a.operands, "period_clk": round(period, 1),
+           "lag_by_subpartition": by_sp, "lag_by_warp": [round(float(v), 1) for v in lag],
+           "iss_wait_tempty": round(float((iss[1] - iss[0])[oki].mean()), 1),
+           "iss_issue_to_commit": round(float((iss[2] - iss[1])[oki].mean()), 1),
+           "iss_fence": round(float((t[6, rng] - t[1, rng])[(t[6, rng] > 0) & (t[1, rng] > 0)].mean()), 1),
+           "iss_mma": round(float((t[7, rng] - t[6, rng])[(t[7, rng] > 0) & (t[6, rng] > 0)].mean()), 1),
+           "iss_commit": round(float((t[2, rng] - t[7, rng])[(t[2, rng] > 0) & (t[7, rng] > 0)].mean()), 1),
+           "iss_between_chunks": round(float((t[0, rng.start + 1:rng.stop + 1] - t[2, rng])[(t[2, rng] > 0)].mean()), 1),
+           "w2_wait_tfull": round(float((t[4, rng] - t[3, rng])[(t[4, rng] > 0) & (t[3, rng] > 0)].mean()), 1),
+           "w2_ld": round(float((t[5, rng] - t[4, rng])[(t[5, rng] > 0) & (t[4, rng] > 0)].mean()), 1)}
+    print(json.dumps(out))
 
-    def avg(e1, e0):
-        v = t[e1, rng] - t[e0, rng]
-        v = v[(t[e1, rng] > 0) & (t[e0, rng] > 0)]
-        return float(v.mean()) if v.size else float("nan")
-
-    per = np.diff(t[7, rng][t[7, rng] > 0])
-    print(f"period per stage (epilogue tfull-to-tfull): {per.mean():.0f} clk")
-    print(f"converter: wait int8 {avg(1, 0):.0f}, wait f16 slot {avg(2, 1):.0f}, convert {avg(3, 2):.0f}")
-    print(f"issuer: wait hfull {avg(5, 4):.0f}, wait tempty {avg(6, 5):.0f}")
 
 if __name__ == "__main__":
     main()
