@@ -44,11 +44,16 @@ for s in $STEPS; do
     micro)
       timeout 300 ./paper_2403_12422_b200/microbench > "$OUT/microbench.jsonl" 2>&1 ;;
     gemm)
-      timeout 600 python tools/gemm_bench.py --shapes qkv,proj,mlp1,mlp2 > "$OUT/gemm_bench.jsonl" 2>&1 ;;
+      timeout 600 python tools/gemm_bench.py --shapes qkv,proj,mlp1,mlp2 > "$OUT/gemm_bench.jsonl" 2>&1
+      timeout 600 python tools/gemm_bench.py --shapes qkv,proj,mlp1,mlp2 --operands f16 > "$OUT/gemm_bench_f16.jsonl" 2>&1 ;;
     eltwise)
       timeout 300 python tools/eltwise_bench.py > "$OUT/eltwise_bench.jsonl" 2>&1 ;;
     bench)
       timeout 900 python bench.py > "$OUT/bench.json" 2> "$OUT/bench.err" ;;
+    benchx)
+      timeout 900 python bench.py --promotion fast --operands auto --no-cpu > "$OUT/bench_fast_auto.json" 2> "$OUT/bench_fast_auto.err"
+      timeout 900 python bench.py --operands auto --no-cpu > "$OUT/bench_exact_auto.json" 2> "$OUT/bench_exact_auto.err"
+      timeout 900 python bench.py --promotion fast --no-cpu --no-bf16 > "$OUT/bench_fast_int8.json" 2> "$OUT/bench_fast_int8.err" ;;
     launches)
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
         --log-file "$OUT/launches.csv" python bench.py --steps 1 --warmup 1 --no-bf16 --no-cpu \
