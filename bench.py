@@ -68,6 +68,9 @@ def parse(argv=None):
     ap.add_argument("--graph", type=int, default=1, choices=[0, 1],
                     help="model workloads, 1 GPU: replay forward+backward from a CUDA graph")
     ap.add_argument("--attn-dtype", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--nccl-algo", default="auto", choices=["auto", "ring", "tree", "nvls"],
+                    help="N>1: NCCL_ALGO for the gradient all-reduce (NVLS = in-switch reduction on "
+                         "NVSwitch); reported in the allreduce object")
     ap.add_argument("--no-bf16", action="store_true", help="skip the cuBLAS BF16 block baseline")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle baseline")
     ap.add_argument("--cpu-tokens", type=int, default=128, help="token sample for the CPU baseline")
@@ -77,8 +80,10 @@ def parse(argv=None):
 # ── distributed plumbing ────────────────────────────────────────────────
 
 
-def dist_setup():
+def dist_setup(nccl_algo: str = "auto"):
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1 and nccl_algo != "auto":
+        os.environ["NCCL_ALGO"] = {"ring": "Ring", "tree": "Tree", "nvls": "NVLS"}[nccl_algo]
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
@@ -149,6 +154,7 @@ def measure_allreduce(wl, world: int, reps: int = 5) -> dict:
     algbw = nbytes / (ms / 1e3) / 1e9
     return {"bytes_per_step": nbytes, "ms": round(ms, 4), "algbw_GBps": round(algbw, 1),
             "busbw_GBps": round(algbw * 2 * (world - 1) / world, 1), "world": world,
+            "nccl_algo": os.environ.get("NCCL_ALGO", "auto (NCCL's choice)"),
             "how": "FP32 parameter-gradient all-reduce of one step timed alone (NCCL, 64 MiB buckets), "
                    f"CUDA events, mean of {reps}, max over ranks; in the step it overlaps backward"}
 
@@ -818,7 +824,7 @@ def run_reference(args, world, rank):
 
 def main():
     args = parse()
-    world, rank, local = dist_setup()
+    world, rank, local = dist_setup(args.nccl_algo)
     if args.impl == "reference":
         out = run_reference(args, world, rank)
         if out is not None:

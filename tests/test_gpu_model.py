@@ -261,3 +261,41 @@ def test_fused_cross_entropy(jf):
     got = dl[:, :v].float()
     assert (got - ref_d).abs().max() <= 2 ** -8 * ref_d.abs().max()  # bf16 output rounding
     assert torch.count_nonzero(dl[:, v:]) == 0
+
+
+def test_loss_curve_matches_reference_run_training(jf, golden):
+    """60 AdamW steps of the reference's copy-task run (trainer.run_training, trainer.py:440-537,
+    fixture tests/golden/losscurve.npz made by the REAL reference) retraced on the GPU from the
+    same initial parameters on the same batches.  The INT8 path is the reference's numerics op
+    for op (FP32 island and head included), so the curves track: per step
+    |loss_gpu - loss_ref| <= 0.02 + 0.05 * loss_ref, the final losses agree to within 1e-2,
+    and the validation loss at the end too.  Also pins the hand-driven backward + the fused
+    AdamW/requantize path over many steps."""
+    from paper_2403_12422_b200.model import AdamW, JetfireLM, ModelConfig
+
+    g = golden("losscurve")
+    layers, c, heads, hidden, vocab, batch = (int(v) for v in g["cfg"])
+    seq = g["x"].shape[2]
+    cfg = ModelConfig(layers=layers, c_model=c, heads=heads, hidden=hidden, vocab=vocab, max_seq=seq,
+                      pos_emb=False, head_dtype="fp32", attn_dtype="fp32")
+    model = JetfireLM(cfg, {k[2:]: g[k] for k in g.files if k.startswith("p_")})
+    assert model.decay_keys == set(str(k) for k in g["decay_keys"])
+    opt = AdamW(model, lr=float(g["lr"]), weight_decay=float(g["weight_decay"]))
+    losses, gnorms, vals = [], [], []
+    vx, vy, vm = (torch.from_numpy(g[k]).cuda() for k in ("val_x", "val_y", "val_mask"))
+    for step in range(g["x"].shape[0]):
+        x, y, m = (torch.from_numpy(g[k][step]).cuda() for k in ("x", "y", "mask"))
+        loss, grads = model.loss_and_grads(x, y, m)
+        losses.append(float(loss))
+        gnorms.append(float(torch.sqrt(sum((v.double() ** 2).sum() for v in grads.values()))))
+        opt.step(grads)
+        vals.append(float(model.loss_and_grads(vx, vy, vm)[0]))
+    ref = g["train_loss"]
+    losses = np.array(losses)
+    dev = np.abs(losses - ref) - (0.02 + 0.05 * ref)
+    assert dev.max() <= 0, (int(dev.argmax()), losses[dev.argmax()], ref[dev.argmax()])
+    assert abs(losses[-1] - ref[-1]) <= 1e-2 and abs(vals[-1] - g["val_loss"][-1]) <= 1e-2
+    # gradient norms (trainer.py:430-437) track too, over the steps where learning is active
+    act = ref > 0.1
+    gref = g["grad_norm"][act]
+    assert np.abs(np.array(gnorms)[act] - gref).max() <= 0.1 * gref.max()

@@ -483,3 +483,83 @@ def test_gelu_backward_overflow_flag(jf):
     assert "overflows" in msg
     # GELU forward cannot overflow (|gelu(x)| <= |x|): the largest input stays clean
     _expect_same_error(jf, lambda: jf.gelu_forward(bqt(jf, dq, ds)), lambda: O.gelu_forward(dq, ds))
+
+
+# ── the torch.autograd form (autograd.py) pinned to the oracle ──
+
+
+def test_autograd_functions_vs_oracle(jf, cfg2_oracle):
+    """Every autograd Function, forward AND backward, on the oracle's config-2 inputs:
+    codes/scales/statistics/FP32 weight gradients bit-exact, axis-0 sums to 1e-5 / 1e-3."""
+    from paper_2403_12422_b200 import autograd as A
+
+    r = cfg2_oracle
+    p, W = r["p"], r["W"]
+    # Linear (mlp1): forward on LN2's output, backward with the GELU-backward gradient
+    lin = jf.QuantLinear(p["mlp1.w"], p["mlp1.b"])
+    wp = torch.nn.Parameter(lin.master_weight.clone())
+    bp = torch.nn.Parameter(lin.bias.clone())
+    xq = A.QTensor(bqt(jf, *r["l2"][:2]), requires_grad=True)
+    y = A.Linear.apply(xq, wp, bp, lin)
+    assert same_q(y.bq, *r["g1"])
+    y.backward(A.QTensor(bqt(jf, *r["b_gelu"])))
+    dxq, dxs, dw, db = r["b_mlp1"]
+    assert same_q(xq.grad.bq, dxq, dxs)
+    assert same(wp.grad, dw)
+    assert rel(npy(bp.grad), db) <= 1e-5
+    # GELU
+    g1 = A.QTensor(bqt(jf, *r["g1"]), requires_grad=True)
+    g = A.Gelu.apply(g1)
+    assert same_q(g.bq, *r["g"])
+    g.backward(A.QTensor(bqt(jf, *r["b_mlp2"][:2])))
+    d = np.abs(npy(g1.grad.bq.values).astype(np.int32) - r["b_gelu"][0])
+    assert d.max() <= 1 and (d > 0).mean() <= 1e-3
+    # Add (+ row statistics) and LayerNorm on them
+    a1q, a1s, _, _ = r["a1"]
+    pq, ps = r["proj"]
+    x1 = A.QTensor(bqt(jf, a1q, a1s), requires_grad=True)
+    x2 = A.QTensor(bqt(jf, pq, ps), requires_grad=True)
+    h = A.Add.apply(x1, x2, 64)
+    hq, hs, m2, ss2 = r["h"]
+    assert same_q(h.bq, hq, hs) and same(h.stats.mean, m2) and same(h.stats.sumsq, ss2)
+    gam = torch.nn.Parameter(cu(p["ln2.gamma"]))
+    bet = torch.nn.Parameter(cu(p["ln2.beta"]))
+    ln = A.LayerNorm.apply(h, gam, bet, 1e-5)
+    assert same_q(ln.bq, *r["l2"][:2])
+    ln.backward(A.QTensor(bqt(jf, *r["b_mlp1"][:2])))
+    q, s, rdg, rdb = r["b_ln2"]
+    assert rel(npy(gam.grad), rdg) <= 1e-3 and rel(npy(bet.grad), rdb) <= 1e-3
+    # the Add's backward hands the LayerNorm gradient to both inputs unchanged
+    assert same_q(x1.grad.bq, q, s) and same_q(x2.grad.bq, q, s)
+
+
+@pytest.mark.parametrize("attn_dtype", [torch.float32, torch.bfloat16])
+def test_autograd_block_config2_vs_oracle(jf, cfg2_oracle, attn_dtype):
+    """JetfireTransformerBlock driven by torch.autograd vs the chained oracle block:
+    the reference's block tolerances, and identical bits to the hand-driven block."""
+    from paper_2403_12422_b200 import autograd as A
+
+    r = cfg2_oracle
+    p = r["p"]
+    cfg = jf.BlockConfig(c_model=C2, heads=HEADS2, hidden=HID2, block=32, dropout_p=0.0)
+    mod = A.JetfireTransformerBlock(cfg, attn_dtype=attn_dtype)
+    with torch.no_grad():
+        for k in ("qkv", "proj", "mlp1", "mlp2"):
+            getattr(mod, k).weight.copy_(cu(p[k + ".w"]))
+            getattr(mod, k).bias.copy_(cu(p[k + ".b"]))
+        for k in ("ln1", "ln2"):
+            getattr(mod, k + "_gamma").copy_(cu(p[k + ".gamma"]))
+            getattr(mod, k + "_beta").copy_(cu(p[k + ".beta"]))
+    x = A.QTensor(bqt(jf, *r["x"]), requires_grad=True)
+    out = mod(x, BATCH2, SEQ2)
+    e_out = rel(npy(out.bq.dequantize()), O.dequantize(*r["out"][:2]))
+    out.backward(A.QTensor(bqt(jf, *r["dy"])))
+    e_dx = rel(npy(x.grad.bq.dequantize()), O.dequantize(*r["dx"][:2]))
+    grads = {"mlp2.w": mod.mlp2.weight.grad, "mlp1.w": mod.mlp1.weight.grad, "proj.w": mod.proj.weight.grad,
+             "qkv.w": mod.qkv.weight.grad, "ln1.gamma": mod.ln1_gamma.grad, "ln2.gamma": mod.ln2_gamma.grad}
+    ref_g = {"mlp2.w": r["b_mlp2"][2], "mlp1.w": r["b_mlp1"][2], "proj.w": r["b_proj"][2],
+             "qkv.w": r["b_qkv"][2], "ln1.gamma": r["b_ln1"][2], "ln2.gamma": r["b_ln2"][2]}
+    e_g = {k: rel(npy(grads[k]), v) for k, v in ref_g.items()}
+    assert e_out <= 0.06 and e_dx <= 0.08 and max(e_g.values()) <= 0.12, (e_out, e_dx, e_g)
+    if attn_dtype == torch.float32:  # only SDPA's FP32 summation order differs from numpy
+        assert e_out <= 0.01 and e_dx <= 0.02 and max(e_g.values()) <= 0.02, (e_out, e_dx, e_g)
