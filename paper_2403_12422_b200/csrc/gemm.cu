@@ -192,6 +192,14 @@ struct Bars {
 // Scales: per stage the 4x4 sub-grids of sA (row blocks x chunks) and sB, 64 B
 // each, by TMA into the stage's 256-byte scale slot.
 constexpr int kEpiTC = 16;  // promotion warps of gemm_tc_kernel
+// Chunks per tfull commit / wait: the MMA issuer commits tfull only after every
+// kGroup-th chunk, and a commit covers all earlier MMAs of the issuing thread, so the
+// promotion warps wait once per group.  Each commit costs ~68 clk of tensor pipe
+// (r1e microbenchmark); per-chunk commits (1) measured 2-5% slower than pairs (2).
+#ifndef JF_GEMM_GROUP
+#define JF_GEMM_GROUP 2
+#endif
+constexpr int kGroup = JF_GEMM_GROUP;
 
 template <int kOp>
 struct Cfg {
@@ -346,7 +354,7 @@ __global__ void __launch_bounds__((2 + kEpiTC) * 32, 1)
             if (lane == 0) JF_TR(6, gch + c);
             if (elect_one()) {
               mma_chunk(stage, c);
-              mma_commit(&S.tfull[c]);
+              if (c % kGroup == kGroup - 1) mma_commit(&S.tfull[c]);
             }
             __syncwarp();
             if (lane == 0) JF_TR(2, gch + c);
@@ -412,9 +420,12 @@ __global__ void __launch_bounds__((2 + kEpiTC) * 32, 1)
         for (int b = 0; b < kTmemBufs; ++b) {
           uint32_t r[kCols];
           if (trw) JF_TR(3, gch + b);
-          mbar_wait_u32(bar_tfull + 8 * b, (tphase >> b) & 1);
+          if (b % kGroup == 0) {  // the group's last chunk landed => the whole group did
+            const int bl = b + kGroup - 1;
+            mbar_wait_u32(bar_tfull + 8 * bl, (tphase >> bl) & 1);
+            tphase ^= 1u << bl;
+          }
           if (trw) JF_TR(4, gch + b);
-          tphase ^= 1u << b;
           tc_fence_after();
           tmem_ld_32x32b_x32(tcol + b * BN, r);
           tmem_wait_ld_dep(r);
