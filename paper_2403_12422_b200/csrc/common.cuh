@@ -70,15 +70,41 @@ JF_DEV int quant_code_fast(float x, float s, float r) {
 
 // quant_code_fast's common path only: the code of fl(x * r), and `tie` raised when
 // y is within 3e-5 of a half-integer (the caller then redoes the element with
-// quant_code_fast).  Straight-line code: no per-element branch / reconvergence.
+// quant_code_fast).  Straight-line code: no per-element branch / reconvergence,
+// and no XU-pipe instruction (the quarter-rate XU pipe -- F2I, FRND, I2F -- was the
+// saturated unit of the memory-bound kernels, ncu r2): round-half-even to an
+// integer by adding 1.5 * 2^23 (|y| <= 128 << 2^22: the sum's ulp is 1), the code
+// read from the sum's low mantissa bits, the distance to the rounded value exact.
 JF_DEV int quant_code_try(float x, float r, bool &tie) {
   const float y = __fmul_rn(x, r);
-  const float d = fabsf(__fsub_rn(__fsub_rn(y, floorf(y)), 0.5f));
-  tie = tie || !(d > 3.0e-5f);
-  int q = __float2int_rn(y);
+  const float t = __fadd_rn(y, 12582912.0f);  // 1.5 * 2^23
+  const float e = __fsub_rn(y, __fsub_rn(t, 12582912.0f));  // y - rint(y), exact
+  tie = tie || !(fabsf(e) < 0.49997f);
+  int q = __float_as_int(t) - 0x4B400000;
   q = q > kQmax ? kQmax : q;
   q = q < -kQmax ? -kQmax : q;
   return q;
+}
+
+// Exact dequantization fl(code * s) without an int->float conversion (XU pipe):
+// the biased code byte u = code + 128 goes into bits 8..15 of 0x4B000000, i.e. the
+// float f = 2^23 + 2^15 + 256 * code exactly; then
+//   fma(f, s * 2^-8, -(2^15 + 2^7) * s) = fl(code * s)
+// with one rounding (s * 2^-8 and the 20-bit constant are exact).  PRMT + FFMA.
+struct DeqScale {
+  float s8, c;
+};
+JF_DEV DeqScale deq_scale(float s) { return {__fmul_rn(s, 0.00390625f), __fmul_rn(-32896.0f, s)}; }
+JF_DEV float deq_code(uint32_t biased_word, int j, DeqScale k) {
+  uint32_t bits;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(bits) : "r"(biased_word), "r"(0x4B000000u), "r"(0x7404u | (j << 4)));
+  return __fmaf_rn(__uint_as_float(bits), k.s8, k.c);
+}
+// 4 codes of a word -> v[0..3]
+JF_DEV void deq4(uint32_t word, DeqScale k, float *v) {
+  const uint32_t u = word ^ 0x80808080u;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) v[j] = deq_code(u, j, k);
 }
 
 JF_DEV uint32_t abs_bits(float x) { return __float_as_uint(x) & 0x7fffffffu; }

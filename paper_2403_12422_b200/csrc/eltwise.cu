@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(256) ln_bwd_rows_leaf_kernel(LnRowArgs A, int 
       const int64_t k0 = col0 + seg * 16;
       const uint4 xq = *reinterpret_cast<const uint4 *>(sx_ + seg * 16);
       const uint4 dq = *reinterpret_cast<const uint4 *>(sd_ + seg * 16);
-      const float sx = __ldg(sxr + (k0 >> 5)), sd = __ldg(sdr + (k0 >> 5));
+      const DeqScale kx = deq_scale(__ldg(sxr + (k0 >> 5))), kd = deq_scale(__ldg(sdr + (k0 >> 5)));
       float g[16];
       const float *gl = gsm + leaf * gstride + seg * 16;
 #pragma unroll
@@ -294,11 +294,12 @@ __global__ void __launch_bounds__(256) ln_bwd_rows_leaf_kernel(LnRowArgs A, int 
         g[4 * q + 2] = g4.z;
         g[4 * q + 3] = g4.w;
       }
-      const uint32_t xw[4] = {xq.x, xq.y, xq.z, xq.w}, dw[4] = {dq.x, dq.y, dq.z, dq.w};
+      const uint32_t xw[4] = {xq.x ^ 0x80808080u, xq.y ^ 0x80808080u, xq.z ^ 0x80808080u, xq.w ^ 0x80808080u};
+      const uint32_t dw[4] = {dq.x ^ 0x80808080u, dq.y ^ 0x80808080u, dq.z ^ 0x80808080u, dq.w ^ 0x80808080u};
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
-        const float xv = __fmul_rn(code_at(xw[e >> 2], e & 3), sx);
-        const float dv = __fmul_rn(code_at(dw[e >> 2], e & 3), sd);
+        const float xv = deq_code(xw[e >> 2], e & 3, kx);
+        const float dv = deq_code(dw[e >> 2], e & 3, kd);
         const float xh = __fmul_rn(__fsub_rn(xv, mr), ir);
         const float dxh = __fmul_rn(dv, g[e]);
         const float pr = __fmul_rn(dxh, xh);

@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(256) dequantize_kernel(const int8_t *__restric
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t e = i * 16;
     const int64_t r = e / c, cc = e - r * c;
-    const float sc = __ldg(s + (r >> 5) * cb + (cc >> 5));
+    const DeqScale dk = deq_scale(__ldg(s + (r >> 5) * cb + (cc >> 5)));
     const uint4 w = __ldg(reinterpret_cast<const uint4 *>(q) + i);
     const uint32_t u[4] = {w.x, w.y, w.z, w.w};
     if (BF16) {
@@ -72,9 +72,9 @@ __global__ void __launch_bounds__(256) dequantize_kernel(const int8_t *__restric
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         // products are exact in fp32; bf16 output rounds them RNE
-        const float f0 = __fmul_rn(code_at(u[k], 0), sc), f1 = __fmul_rn(code_at(u[k], 1), sc);
-        const float f2 = __fmul_rn(code_at(u[k], 2), sc), f3 = __fmul_rn(code_at(u[k], 3), sc);
-        __nv_bfloat162 a = __floats2bfloat162_rn(f0, f1), b = __floats2bfloat162_rn(f2, f3);
+        float f[4];
+        deq4(u[k], dk, f);
+        __nv_bfloat162 a = __floats2bfloat162_rn(f[0], f[1]), b = __floats2bfloat162_rn(f[2], f[3]);
         o[2 * k] = *reinterpret_cast<uint32_t *>(&a);
         o[2 * k + 1] = *reinterpret_cast<uint32_t *>(&b);
       }
@@ -84,9 +84,11 @@ __global__ void __launch_bounds__(256) dequantize_kernel(const int8_t *__restric
     } else {
       float4 *dst = reinterpret_cast<float4 *>(static_cast<float *>(y) + e);
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
-        dst[k] = make_float4(__fmul_rn(code_at(u[k], 0), sc), __fmul_rn(code_at(u[k], 1), sc),
-                             __fmul_rn(code_at(u[k], 2), sc), __fmul_rn(code_at(u[k], 3), sc));
+      for (int k = 0; k < 4; ++k) {
+        float f[4];
+        deq4(u[k], dk, f);
+        dst[k] = make_float4(f[0], f[1], f[2], f[3]);
+      }
     }
   }
 }
@@ -111,15 +113,15 @@ __global__ void __launch_bounds__(256) dequant_qkv_heads_kernel(const int8_t *__
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t e = i * 16;
     const int64_t r = e / c3, cc = e - r * c3;
-    const float sc = __ldg(s + (r >> 5) * cb + (cc >> 5));
+    const DeqScale dk = deq_scale(__ldg(s + (r >> 5) * cb + (cc >> 5)));
     const uint4 w = __ldg(reinterpret_cast<const uint4 *>(q) + i);
     const uint32_t u[4] = {w.x, w.y, w.z, w.w};
     uint32_t o[8];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const float f0 = __fmul_rn(code_at(u[k], 0), sc), f1 = __fmul_rn(code_at(u[k], 1), sc);
-      const float f2 = __fmul_rn(code_at(u[k], 2), sc), f3 = __fmul_rn(code_at(u[k], 3), sc);
-      __nv_bfloat162 a = __floats2bfloat162_rn(f0, f1), b = __floats2bfloat162_rn(f2, f3);
+      float f[4];
+      deq4(u[k], dk, f);
+      __nv_bfloat162 a = __floats2bfloat162_rn(f[0], f[1]), b = __floats2bfloat162_rn(f[2], f[3]);
       o[2 * k] = *reinterpret_cast<uint32_t *>(&a);
       o[2 * k + 1] = *reinterpret_cast<uint32_t *>(&b);
     }

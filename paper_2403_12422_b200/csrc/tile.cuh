@@ -43,15 +43,12 @@ JF_DEV TilePos tile_pos(int64_t n, int64_t c) {
 JF_DEV void load_deq(const TilePos &t, const int8_t *__restrict__ q, const float *__restrict__ s,
                      float (&v)[4][8]) {
   if (!t.active) return;
-  const float sc = __ldg(s + t.scale_idx(t.r0, t.col()));  // 4 rows share one row block
+  const DeqScale k = deq_scale(__ldg(s + t.scale_idx(t.r0, t.col())));  // 4 rows share one row block
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const uint2 w = __ldg(reinterpret_cast<const uint2 *>(q + t.row(i) * t.c + t.col()));
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      v[i][j] = __fmul_rn(code_at(w.x, j), sc);
-      v[i][4 + j] = __fmul_rn(code_at(w.y, j), sc);
-    }
+    deq4(w.x, k, v[i]);
+    deq4(w.y, k, v[i] + 4);
   }
 }
 
