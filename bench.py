@@ -68,6 +68,9 @@ def parse(argv=None):
     ap.add_argument("--graph", type=int, default=1, choices=[0, 1],
                     help="model workloads, 1 GPU: replay forward+backward from a CUDA graph")
     ap.add_argument("--attn-dtype", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--attention", default="sdpa", choices=["sdpa", "fused"],
+                    help="attention island (runtime.set_attention): cuDNN SDPA between boundary kernels, or the "
+                         "fused tcgen05 kernels that read/write INT8 codes directly (bf16 only)")
     ap.add_argument("--nccl-algo", default="auto", choices=["auto", "ring", "tree", "nvls"],
                     help="N>1: NCCL_ALGO for the gradient all-reduce (NVLS = in-switch reduction on "
                          "NVSwitch); reported in the allreduce object")
@@ -476,6 +479,7 @@ def run_ours(args, world, rank, local):
     jf.set_error_check("deferred")
     jf.set_promotion(args.promotion)
     jf.runtime.set_gemm_operands(args.operands)
+    jf.runtime.set_attention(args.attention)
     jf.runtime.set_overlap_wgrad(bool(args.overlap_wgrad))
     w = dict(WORKLOADS[args.workload])
     if args.batch:
@@ -543,7 +547,8 @@ def run_ours(args, world, rank, local):
     cfg.update(wl.config())
     cfg.update({"global_tokens": world * n, "block": 32, "promotion": args.promotion, "operands": args.operands,
                 "overlap_wgrad": bool(args.overlap_wgrad),
-                "attention": f"torch SDPA ({args.attn_dtype})",
+                "attention": ("fused INT8-boundary tcgen05 kernels (bf16)" if args.attention == "fused"
+                              else f"torch SDPA ({args.attn_dtype})"),
                 "parallelism": f"dp{world}" if world > 1 else "single"})
     out = {
         "metric": METRIC, "value": round(tokens_per_s, 1), "unit": "tokens/s", "n_gpus": world,

@@ -77,6 +77,11 @@ SIGNATURES = {
     "jf_dequantize_qkv_heads": (ctypes.c_int, [_P, _P, _I64, _I64, _I64, _I64, _P, _P, _P, _P]),
     "jf_quantize_heads_bf16": (ctypes.c_int, [_P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _P, _I64, _P, _I64,
                                               _P, _P]),
+    "jf_attn_supported": (ctypes.c_int, [_I64, _I64]),
+    "jf_attn_set_mn_desc": (ctypes.c_int, [ctypes.c_uint32, ctypes.c_uint32]),
+    "jf_attn_set_trace": (ctypes.c_int, [_P]),
+    "jf_attn_fwd_q": (ctypes.c_int, [_P, _P, _I64, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P]),
+    "jf_attn_bwd_q": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _P, _P, _P, _P]),
 }
 
 _lib = None
@@ -134,7 +139,7 @@ KERNELS_PER_CALL = {
     "quantize": 1, "dequantize": 1, "transpose": 1, "gemm_fwd": 1, "gemm_dgrad": 1, "gemm_wgrad": 1,
     "gemm_partials": 1, "add_stats": 1, "ln_fwd": 2, "ln_bwd": 4, "gelu_fwd": 1, "gelu_bwd": 1,
     "colsum": 2, "dropout": 1, "gelu_tables": 1, "dequant_qkv_heads": 1, "quantize_heads": 1,
-    "cross_entropy": 1, "adamw": 1, "adamw_quantize": 1, "adamw_multi": 1, "widen_codes": 1, "gemm_f16": 1,
+    "cross_entropy": 1, "attn_fwd": 1, "attn_bwd": 2, "adamw": 1, "adamw_quantize": 1, "adamw_multi": 1, "widen_codes": 1, "gemm_f16": 1,
 }
 launch_count = [0]
 

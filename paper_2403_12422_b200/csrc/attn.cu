@@ -1,0 +1,1009 @@
+// attn.cu — the attention island with its INT8 boundary fused in.
+//
+// Reference: qlayers.py:187-236 (AttentionCore, causal softmax attention in FP32)
+// and its INT8 boundary in TransformerBlock: qkv = qkv_q.dequantize() ->
+// attention -> quantize_per_block(out) (qlayers.py:350-351), and backward
+// dO = dattn_q.dequantize() -> attention backward -> quantize(dQ|dK|dV)
+// (qlayers.py:406-408).  Here those crossings happen inside the attention
+// kernels: Q/K/V (and dO) tiles are read from HBM as INT8 codes + block scales
+// and dequantized while they are staged in shared memory; O (and dQ/dK/dV)
+// leave the kernel as INT8 codes + 32x32 block scales.  No BF16/FP32 head tensor
+// is written to HBM (the only FP side outputs are the per-row log-sum-exp and,
+// for the backward's D_i = rowsum(dO * O), O itself in bf16).
+//
+// Forward (attn_fwd_kernel), one CTA per (128 query rows, head, batch), 9 warps:
+//   warps 0-3  softmax: thread = query row = TMEM lane.  tcgen05.ld of the S row,
+//              online softmax in the log2 domain with conditional rescaling (O in
+//              TMEM is rescaled only when the running max grows by > 2^8), P in
+//              bf16 to shared memory; epilogue O / l -> 32x32 requantization.
+//   warps 4-7  producers: INT8 Q (once), K, V tiles (128 rows) from HBM, exact
+//              dequantization fl(code * s) -> bf16 into SW128 K-major tiles.
+//   warp 8     MMA issuer: S_j = Q K_j^T (tcgen05 kind::f16, bf16 in, f32 in TMEM,
+//              double-buffered) issued ahead of O += P_{j-1} V_{j-1} (V read
+//              MN-major from the same tile layout).
+// Numerics: tolerance class: the reference island is FP32; here the
+// dequantized operands and P are rounded to bf16, accumulation is FP32.
+#include <math.h>
+#include <stdio.h>
+
+#include "common.cuh"
+
+int jf_launch_check(const char *what);
+int jf_set_smem_attr(const void *func, int bytes, const char *what);
+
+namespace jf {
+namespace attn {
+
+constexpr int BQ = 128;   // query rows per CTA (= TMEM lanes)
+constexpr int BKV = 128;  // key/value rows per tile
+constexpr uint32_t kHalf = 128 * 128;  // bytes of one 128-row x 64-bf16 SW128 half tile
+
+// ── small PTX helpers ─────────────────────────────────────────────────
+JF_DEV void mma_bf16_ss(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+// Same with A read from tensor memory (M=128 lanes x 16 bf16 = 8 columns per K step).
+JF_DEV void mma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+JF_DEV void cp_async16(uint32_t dst, const void *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+JF_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+JF_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// kind::f16 instruction descriptor, f32 D; operands bf16 (bf = 1) or f16 (bf = 0).
+__host__ __device__ constexpr uint32_t idesc_16(int m, int n, int a_mn, int b_mn, int bf) {
+  return (1u << 4) | ((uint32_t)bf << 7) | ((uint32_t)bf << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
+         ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+}
+
+JF_DEV void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, "
+      "%17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
+      "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
+      "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+
+template <int N>
+JF_DEV void wait_ld_dep(uint32_t (&r)[N]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < N; i += 8)
+    asm volatile("" : "+r"(r[i]), "+r"(r[i + 1]), "+r"(r[i + 2]), "+r"(r[i + 3]), "+r"(r[i + 4]),
+                 "+r"(r[i + 5]), "+r"(r[i + 6]), "+r"(r[i + 7]));
+}
+
+JF_DEV bool elect_one() {
+  uint32_t p;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "elect.sync _|P, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, P;\n\t}"
+      : "=r"(p));
+  return p != 0;
+}
+
+JF_DEV float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+JF_DEV uint32_t bf2(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t *>(&v);
+}
+
+// Byte offset of 16-byte chunk c8 (8 bf16 = columns 8*c8 .. +7) of row r in a
+// 128-row tile of SW128 half tiles (64 columns each): the layout TMA writes for
+// SWIZZLE_128B boxes {64, 128}, which the UMMA descriptors below read.
+JF_DEV uint32_t sw_off(int r, int c8) {
+  return (uint32_t)(c8 >> 3) * kHalf + (uint32_t)r * 128u + ((uint32_t)((c8 & 7) ^ (r & 7)) << 4);
+}
+
+// 16 INT8 codes with block scale s -> 16 bf16 (exact fl(code*s), then RNE to bf16),
+// written as two 16-byte chunks (c8, c8 + 1) of row r.
+JF_DEV void deq16_store(uint32_t tile, int r, int c8, uint4 w, float s) {
+  const DeqScale k = deq_scale(s);
+  const uint32_t u[4] = {w.x ^ 0x80808080u, w.y ^ 0x80808080u, w.z ^ 0x80808080u, w.w ^ 0x80808080u};
+  uint32_t o[8];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    o[2 * i] = bf2(deq_code(u[i], 0, k), deq_code(u[i], 1, k));
+    o[2 * i + 1] = bf2(deq_code(u[i], 2, k), deq_code(u[i], 3, k));
+  }
+  sts128(tile + sw_off(r, c8), o[0], o[1], o[2], o[3]);
+  sts128(tile + sw_off(r, c8 + 1), o[4], o[5], o[6], o[7]);
+}
+
+JF_DEV float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
+// K-major SW128 operand: rows = M/N index, 64 K-elements per 128-byte row.  K step
+// of 16 elements = +32 bytes inside the row; the second 64-column half is +kHalf.
+JF_DEV uint64_t kdesc(uint32_t tile, int kstep) {
+  return smem_desc_sw128(tile + (uint32_t)(kstep >> 2) * kHalf + (uint32_t)(kstep & 3) * 32u, 16, 1024);
+}
+// MN-major SW128 operand in the same tile layout: rows = K index, 64 MN-elements
+// per row; K step of 16 rows = +2048 bytes; MN atoms (64 wide) kHalf apart.
+JF_DEV uint64_t mndesc(uint32_t tile, int kstep, uint32_t lbo, uint32_t sbo) {
+  return smem_desc_sw128(tile + (uint32_t)kstep * 2048u, lbo, sbo);
+}
+
+struct FwdParams {
+  const int8_t *qkv;  // [n x 3c] codes, n = batch*seq, c = heads*D
+  const float *qkv_s; // [n/32 x 3c/32]
+  int64_t batch, seq, heads;
+  int8_t *o;          // [n x c] codes
+  float *o_s;         // [n/32 x c/32]
+  uint16_t *o_bf;     // [n x c] bf16 copy of O (backward's D_i), may be null
+  float *lse;         // [batch, heads, seq], log2 domain: m + log2(l)
+  int32_t *err;
+  float scale_log2;   // log2(e) / sqrt(D)
+  uint32_t mn_lbo, mn_sbo;
+  long long *trace;   // diagnostics: CTA (0,0,0) event clocks [16 events][64 tiles], or null
+};
+
+#define ATR(ev, j)                                                                             \
+  do {                                                                                         \
+    if (p.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (j) < 64)          \
+      p.trace[(ev) * 64 + (j)] = clock64();                                                    \
+  } while (0)
+
+// ── forward kernel: two query tiles (A = rows 0..127, B = rows 128..255) per CTA ──
+constexpr int kProdWarps = 3;                 // warps 8..10
+constexpr int kFwdThreads = 32 * (8 + kProdWarps + 1);
+
+template <int D>
+struct FwdSmem {
+  static constexpr uint32_t kTile = (uint32_t)BKV * D * 2;  // one K or V tile (16-bit, SW128)
+  static constexpr uint32_t kQ = (uint32_t)BQ * D * 2;      // one query tile
+  static constexpr uint32_t kStage8 = (uint32_t)BKV * D;    // one K or V tile of INT8 codes
+  static constexpr uint32_t kBytes = 1024 + 2 * kQ + 4 * kTile + 2 * kStage8 + 256;
+};
+
+struct FwdBars {
+  uint64_t q_full, kv_full[2], kv_free[2], s_full[2], p_full[2], o_done[2];
+  uint32_t tmem;
+};
+
+// TMEM columns: S_A [0,128), S_B [128,256) (P_X overwrites S_X in place as bf16 pairs,
+// columns [0,64) of its buffer), O_A [256, 256 + D), O_B [256 + D, 256 + 2D).
+template <int D>
+__global__ void __launch_bounds__(kFwdThreads, 1) attn_fwd_kernel(const FwdParams p) {
+  using SM = FwdSmem<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sQ = smem_u32(base);          // Q_A, Q_B at sQ + X*kQ
+  const uint32_t sK0 = sQ + 2 * SM::kQ;         // K stage s at sK0 + 2*s*kTile, V stage s at +kTile
+  const uint32_t s8 = sK0 + 4 * SM::kTile;      // INT8 staging: K at s8, V at s8 + kStage8
+  FwdBars &B = *reinterpret_cast<FwdBars *>(base + 2 * SM::kQ + 4 * SM::kTile + 2 * SM::kStage8);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t S = p.seq, H = p.heads, C = H * D, C3 = 3 * C;
+  const int qp = (int)(S / (2 * BQ)) - 1 - (int)blockIdx.x;  // query-tile pair, heaviest first
+  const int h = blockIdx.y, b = blockIdx.z;
+  const int64_t row0 = (int64_t)b * S + (int64_t)qp * 2 * BQ;  // first token row of Q_A
+  const int nB = 2 * qp + 2, nA = nB - 1;                      // causal kv tiles of Q_B / Q_A
+
+  if (threadIdx.x == 0) {
+    mbar_init(&B.q_full, 32 * kProdWarps);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&B.kv_full[i], 32 * kProdWarps);
+      mbar_init(&B.kv_free[i], 1);
+      mbar_init(&B.s_full[i], 1);
+      mbar_init(&B.p_full[i], 128);
+      mbar_init(&B.o_done[i], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 11) tmem_alloc(&B.tmem, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = B.tmem;
+  constexpr int kC16 = D / 16;                  // 16-code chunks per row
+  constexpr int kTileChunks = BKV * kC16;        // per K or V tile
+  constexpr int kNP = 32 * kProdWarps;
+  constexpr int kPer = (kTileChunks + kNP - 1) / kNP;
+
+  if (warp >= 8 && warp < 8 + kProdWarps) {
+    // ───────────── producers: INT8 -> 16-bit SW128 tiles ─────────────
+    // Thread t copies (cp.async, one tile ahead) and converts chunks t + 96 i of each
+    // tile, so the staging slot needs no cross-thread synchronization.
+    const int t = threadIdx.x - 256;
+    const int64_t kcol = C + (int64_t)h * D, vcol = 2 * C + (int64_t)h * D;
+    auto issue = [&](int j) {
+      const int64_t r0 = (int64_t)b * S + (int64_t)j * BKV;
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) {
+        const int ci = t + kNP * i;
+        if (ci < kTileChunks) {
+          const int r = ci / kC16, c16 = ci % kC16;
+          const int8_t *src = p.qkv + (r0 + r) * C3 + 16 * c16;
+          cp_async16(s8 + 16 * ci, src + kcol);
+          cp_async16(s8 + SM::kStage8 + 16 * ci, src + vcol);
+        }
+      }
+      cp_async_commit();
+    };
+    float sk[kPer], sv[kPer];
+    auto scales = [&](int j) {
+      const int64_t r0 = (int64_t)b * S + (int64_t)j * BKV;
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) {
+        const int ci = min(t + kNP * i, kTileChunks - 1), r = ci / kC16, c16 = ci % kC16;
+        const float *srow = p.qkv_s + ((r0 + r) >> 5) * (C3 >> 5);
+        sk[i] = __ldg(srow + ((kcol + 16 * c16) >> 5));
+        sv[i] = __ldg(srow + ((vcol + 16 * c16) >> 5));
+      }
+    };
+    issue(0);
+    scales(0);
+    // Q_A and Q_B (256 rows), straight from global memory, kPer chunks in flight
+#pragma unroll 1
+    for (int base = 0; base < 2 * BQ * kC16; base += kNP * kPer) {
+      uint4 w[kPer];
+      float sq[kPer];
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) {
+        const int ci = min(base + t + kNP * i, 2 * BQ * kC16 - 1), r = ci / kC16, c16 = ci % kC16;
+        const int64_t row = row0 + r, cc = (int64_t)h * D + 16 * c16;
+        w[i] = __ldg(reinterpret_cast<const uint4 *>(p.qkv + row * C3 + cc));
+        sq[i] = __ldg(p.qkv_s + (row >> 5) * (C3 >> 5) + (cc >> 5));
+      }
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) {
+        const int ci = base + t + kNP * i, r = ci / kC16, c16 = ci % kC16;
+        if (ci < 2 * BQ * kC16) deq16_store(sQ + (r >> 7) * SM::kQ, r & 127, 2 * c16, w[i], sq[i]);
+      }
+    }
+    fence_proxy_async_smem();
+    mbar_arrive(&B.q_full);
+#pragma unroll 1
+    for (int j = 0; j < nB; ++j) {
+      const int st = j & 1;
+      if (t == 0) ATR(0, j);
+      cp_async_wait<0>();  // tile j's codes landed
+      if (t == 0) ATR(1, j);
+      mbar_wait(&B.kv_free[st], ((j >> 1) & 1) ^ 1);
+      if (t == 0) ATR(2, j);
+      const uint32_t tk = sK0 + 2 * st * SM::kTile, tv = tk + SM::kTile;
+      uint4 wk[kPer], wv[kPer];
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) {
+        const int ci = t + kNP * i;
+        if (ci < kTileChunks) {
+          wk[i] = lds128(s8 + 16 * ci);
+          wv[i] = lds128(s8 + SM::kStage8 + 16 * ci);
+        }
+      }
+      if (j + 1 < nB) issue(j + 1);  // the slot's codes are in registers now
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) {
+        const int ci = t + kNP * i;
+        if (ci < kTileChunks) {
+          const int r = ci / kC16, c16 = ci % kC16;
+          deq16_store(tk, r, 2 * c16, wk[i], sk[i]);
+          deq16_store(tv, r, 2 * c16, wv[i], sv[i]);
+        }
+      }
+      fence_proxy_async_smem();
+      if (t == 0) ATR(3, j);
+      mbar_arrive(&B.kv_full[st]);
+      if (j + 1 < nB) scales(j + 1);
+    }
+    cp_async_wait<0>();
+  } else if (warp == 11) {
+    // ───────────── MMA issuer ─────────────
+    // Issues whichever is ready: O_X += P_X(j) V_j (P in TMEM) before S_X(j) = Q_X K_j^T.
+    // S_X(j) needs kv tile j and PV_X(j-1) issued: the tensor pipe runs MMAs in issue
+    // order, so PV_X(j-1) has read P_X(j-1) from the S_X buffer before S_X(j) lands.
+    constexpr uint32_t idS = idesc_16(BQ, BKV, 0, 0, 1);  // bf16 Q, K
+    constexpr uint32_t idO = idesc_16(BQ, D, 0, 1, 1);    // bf16 P (TMEM), V (MN-major)
+    const uint32_t a_kv_full = smem_u32(&B.kv_full[0]), a_p_full = smem_u32(&B.p_full[0]);
+    mbar_wait(&B.q_full, 0);
+    int sx[2] = {0, 0}, px[2] = {0, 0};
+    const int nx[2] = {nA, nB};
+#pragma unroll 1
+    while (px[0] < nA || px[1] < nB) {
+      int go = -1;  // 0/1: PV of X; 2/3: S of X-2
+      if (lane == 0) {
+        while (go < 0) {
+#pragma unroll
+          for (int X = 0; X < 2; ++X)
+            if (go < 0 && px[X] < sx[X] && mbar_test_u32(a_p_full + 8 * X, px[X] & 1)) go = X;
+#pragma unroll
+          for (int X = 0; X < 2; ++X)
+            if (go < 0 && sx[X] < nx[X] && sx[X] <= px[X] &&
+                mbar_test_u32(a_kv_full + 8 * (sx[X] & 1), (sx[X] >> 1) & 1))
+              go = 2 + X;
+        }
+      }
+      go = __shfl_sync(0xffffffffu, go, 0);
+      tc_fence_after();
+      if (go >= 2) {
+        const int X = go - 2, j = sx[X], st = j & 1;
+        if (lane == 0 && X == 0) ATR(5, j);
+        if (elect_one()) {
+          const uint32_t tk = sK0 + 2 * st * SM::kTile, q = sQ + X * SM::kQ;
+#pragma unroll
+          for (int k = 0; k < D / 16; ++k)
+            mma_bf16_ss(tmem + X * BKV, kdesc(q, k), kdesc(tk, k), idS, k > 0 ? 1u : 0u);
+          mma_commit(&B.s_full[X]);
+        }
+        ++sx[X];
+      } else {
+        const int X = go, j = px[X], st = j & 1;
+        if (lane == 0 && X == 0) ATR(6, j);
+        const uint32_t tv = sK0 + (2 * st + 1) * SM::kTile;
+        px[X] = j + 1;
+        const bool release = X == 0 ? px[1] > j : (j >= nA || px[0] > j);
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < BKV / 16; ++k)
+            mma_bf16_ts(tmem + 2 * BKV + X * D, tmem + X * BKV + 8 * k, mndesc(tv, k, p.mn_lbo, p.mn_sbo), idO,
+                        (j > 0 || k > 0) ? 1u : 0u);
+          mma_commit(&B.o_done[X]);
+          if (release) mma_commit(&B.kv_free[st]);
+        }
+      }
+      __syncwarp();
+    }
+  } else if (warp < 8) {
+    // ───────────── softmax + epilogue (thread = query row of tile X) ─────────────
+    const int X = warp >> 2;
+    const int r = threadIdx.x & 127;  // TMEM lane
+    const int n = X == 0 ? nA : nB, qt = 2 * qp + X;  // qt: this tile's index == its diagonal kv tile
+    const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    const uint32_t tS = lane_base + X * BKV, tO = lane_base + 2 * BKV + X * D;
+    const float c = p.scale_log2;
+    float m = -INFINITY, l = 0.0f;
+#pragma unroll 1
+    for (int j = 0; j < n; ++j) {
+      if (r == 0 && X == 0) ATR(8, j);
+      mbar_wait(&B.s_full[X], j & 1);
+      if (r == 0 && X == 0) ATR(9, j);
+      tc_fence_after();
+      uint32_t sr[BKV];
+#pragma unroll
+      for (int q = 0; q < BKV / 32; ++q)
+        tmem_ld_32x32b_x32(tS + 32 * q, *reinterpret_cast<uint32_t(*)[32]>(sr + 32 * q));
+      wait_ld_dep(sr);
+      float *sf = reinterpret_cast<float *>(sr);
+      if (j == qt) {  // diagonal tile: key k > query r is masked
+#pragma unroll
+        for (int k = 0; k < BKV; ++k)
+          if (k > r) sf[k] = -INFINITY;
+      }
+      float mx = fmax3(sf[0], sf[1], sf[2]);
+#pragma unroll
+      for (int k = 3; k < BKV - 1; k += 2) mx = fmax3(mx, sf[k], sf[k + 1]);
+      mx = fmaxf(mx, sf[BKV - 1]);
+      const float mnew = mx * c;
+      bool resc = false;
+      float alpha = 1.0f;
+      if (j == 0) {
+        m = mnew;
+      } else if (mnew > m + 8.0f) {
+        alpha = ex2(m - mnew);
+        m = mnew;
+        resc = true;
+      }
+      float rs0 = 0.0f, rs1 = 0.0f;
+      uint32_t pk[BKV / 2];
+#pragma unroll
+      for (int k = 0; k < BKV; k += 2) {
+        float x0, x1;
+        ffma2_rn(x0, x1, sf[k], sf[k + 1], c, c, -m, -m);
+        const float p0 = ex2(x0), p1 = ex2(x1);
+        fadd2_rn(rs0, rs1, rs0, rs1, p0, p1);
+        pk[k / 2] = bf2(p0, p1);
+      }
+      l = fmaf(l, alpha, rs0 + rs1);
+      // P_X(j) -> TMEM (columns [0, 64) of S_X): S_X(j) is fully read above
+      tmem_st_32x32b_x32(tS, *reinterpret_cast<uint32_t(*)[32]>(pk));
+      tmem_st_32x32b_x32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(pk + 32));
+      if (r == 0 && X == 0) ATR(10, j);
+      if (j > 0) {
+        mbar_wait(&B.o_done[X], (j - 1) & 1);  // PV_X(j-1) done: O_X current
+        if (r == 0 && X == 0) ATR(11, j);
+        tc_fence_after();
+        if (__any_sync(0xffffffffu, resc)) {
+#pragma unroll 1
+          for (int q = 0; q < D / 32; ++q) {
+            uint32_t o[32];
+            tmem_ld_32x32b_x32(tO + 32 * q, o);
+            wait_ld_dep(o);
+#pragma unroll
+            for (int k = 0; k < 32; ++k) o[k] = __float_as_uint(__uint_as_float(o[k]) * alpha);
+            tmem_st_32x32b_x32(tO + 32 * q, o);
+          }
+        }
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      if (r == 0 && X == 0) ATR(12, j);
+      mbar_arrive(&B.p_full[X]);
+    }
+    // epilogue: O / l, 32x32 requantization (warp = one 32-row block)
+    mbar_wait(&B.o_done[X], (n - 1) & 1);
+    if (r == 0 && X == 0) ATR(13, 0);
+    tc_fence_after();
+    const float inv = 1.0f / l;
+    const int64_t row = row0 + X * BQ + r;
+    int flags = 0;
+#pragma unroll 1
+    for (int q = 0; q < D / 32; ++q) {
+      uint32_t o[32];
+      tmem_ld_32x32b_x32(tO + 32 * q, o);
+      wait_ld_dep(o);
+      float v[32];
+      uint32_t am = 0;
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        v[k] = __uint_as_float(o[k]) * inv;
+        am = max(am, abs_bits(v[k]));
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) am = max(am, __shfl_xor_sync(0xffffffffu, am, off));
+      const float sc = block_scale(am, flags);
+      const float rc = __frcp_rn(sc);
+      uint32_t w[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        w[k] = pack4(quant_code_fast(v[4 * k], sc, rc), quant_code_fast(v[4 * k + 1], sc, rc),
+                     quant_code_fast(v[4 * k + 2], sc, rc), quant_code_fast(v[4 * k + 3], sc, rc));
+      const int64_t col = (int64_t)h * D + 32 * q;
+      uint4 *dst = reinterpret_cast<uint4 *>(p.o + row * C + col);
+      dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+      dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+      if (lane == 0) p.o_s[(row >> 5) * (C >> 5) + (col >> 5)] = sc;
+      if (p.o_bf) {
+        uint4 *ob = reinterpret_cast<uint4 *>(p.o_bf + row * C + col);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          ob[k] = make_uint4(bf2(v[8 * k], v[8 * k + 1]), bf2(v[8 * k + 2], v[8 * k + 3]),
+                             bf2(v[8 * k + 4], v[8 * k + 5]), bf2(v[8 * k + 6], v[8 * k + 7]));
+      }
+    }
+    p.lse[((int64_t)b * H + h) * S + (int64_t)qt * BQ + r] = m + __log2f(l);
+    if (lane == 0) raise_flags(p.err, flags);
+    if (r == 0 && X == 0) ATR(14, 0);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 11) tmem_dealloc(tmem, 512);
+}
+
+
+JF_DEV void tmem_ld_32x32b_x16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+JF_DEV void tmem_st_32x32b_x16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+
+// Requantize one 32-column block of a TMEM row tile (thread = row, warp = 32-row block):
+// fp32 = TMEM value * mul -> 32x32 block absmax -> binary16 scale -> RNE codes.
+JF_DEV int quant_tmem_block(uint32_t taddr, float mul, int8_t *q, float *sdst, int lane) {
+  uint32_t o[32];
+  tmem_ld_32x32b_x32(taddr, o);
+  wait_ld_dep(o);
+  float v[32];
+  uint32_t am = 0;
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    v[k] = __uint_as_float(o[k]) * mul;
+    am = max(am, abs_bits(v[k]));
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) am = max(am, __shfl_xor_sync(0xffffffffu, am, off));
+  int flags = 0;
+  const float sc = block_scale(am, flags);
+  const float rc = __frcp_rn(sc);
+  uint32_t w[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    w[k] = pack4(quant_code_fast(v[4 * k], sc, rc), quant_code_fast(v[4 * k + 1], sc, rc),
+                 quant_code_fast(v[4 * k + 2], sc, rc), quant_code_fast(v[4 * k + 3], sc, rc));
+  reinterpret_cast<uint4 *>(q)[0] = make_uint4(w[0], w[1], w[2], w[3]);
+  reinterpret_cast<uint4 *>(q)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+  if (lane == 0) *sdst = sc;
+  return flags;
+}
+
+// ── backward ─────────────────────────────────────────────────────────
+// One INT8 row-tile source: codes q (row stride ld bytes), scale grid s (row stride
+// ld/32), head columns starting at col.
+struct Src {
+  const int8_t *q;
+  const float *s;
+  int64_t ld, col;
+};
+
+struct BwdParams {
+  const int8_t *qkv;   // [n x 3c] codes + scales (the forward's input)
+  const float *qkv_s;
+  const int8_t *dout;  // [n x c] codes + scales: dL/d(attention output)
+  const float *dout_s;
+  const uint16_t *o_bf; // [n x c] bf16 O (forward)
+  const float *lse;     // [batch, heads, seq] log2 domain (forward)
+  float *dsum;          // [batch, heads, seq] D_i = rowsum(dO * O): written by dq, read by dkv
+  int64_t batch, seq, heads;
+  int8_t *dqkv;         // [n x 3c] codes + scales: dQ | dK | dV
+  float *dqkv_s;
+  int32_t *err;
+  float scale_log2, scale;
+  uint32_t mn_lbo, mn_sbo;
+};
+
+template <int D>
+struct BwdSmem {
+  static constexpr uint32_t kTile = (uint32_t)BKV * D * 2;
+  static constexpr uint32_t kStage8 = (uint32_t)BKV * D;
+  // own tiles (2) + loop tiles (2 stages x 2) + INT8 staging (2 tiles)
+  static constexpr uint32_t kBytes = 1024 + 6 * kTile + 2 * kStage8 + 256;
+};
+
+struct BwdBars {
+  uint64_t own_full, full[2], free_[2], s_full, p_full, done;
+  uint32_t tmem;
+};
+
+// Producer role shared by both backward kernels (warps 4..7): the CTA's own two
+// row tiles (rows own_row0..+127 of own0/own1) once, then `count` loop tiles
+// (rows row_b + 128*(first + j) of loop0/loop1) through the cp.async staging slot
+// into the 2-stage bf16 ring.
+template <int D>
+JF_DEV void bwd_producer(int t, uint32_t sOwn, uint32_t sLoop, uint32_t s8, BwdBars &B, Src own0, Src own1,
+                         int64_t own_row0, Src l0, Src l1, int64_t row_b, int first, int count) {
+  using SM = BwdSmem<D>;
+  constexpr int kC16 = D / 16, kChunks = BKV * kC16, kPer = kChunks / 128;
+  auto issue = [&](int j) {
+    const int64_t r0 = row_b + (int64_t)(first + j) * BKV;
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      const int ci = t + 128 * i, r = ci / kC16, c16 = ci % kC16;
+      cp_async16(s8 + 16 * ci, l0.q + (r0 + r) * l0.ld + l0.col + 16 * c16);
+      cp_async16(s8 + SM::kStage8 + 16 * ci, l1.q + (r0 + r) * l1.ld + l1.col + 16 * c16);
+    }
+    cp_async_commit();
+  };
+  float sa[kPer], sb[kPer];
+  auto scales = [&](int j) {
+    const int64_t r0 = row_b + (int64_t)(first + j) * BKV;
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      const int ci = t + 128 * i, r = ci / kC16, c16 = ci % kC16;
+      sa[i] = __ldg(l0.s + ((r0 + r) >> 5) * (l0.ld >> 5) + ((l0.col + 16 * c16) >> 5));
+      sb[i] = __ldg(l1.s + ((r0 + r) >> 5) * (l1.ld >> 5) + ((l1.col + 16 * c16) >> 5));
+    }
+  };
+  if (count > 0) issue(0);
+  {
+    uint4 w0[kPer], w1[kPer];
+    float a0[kPer], a1[kPer];
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      const int ci = t + 128 * i, r = ci / kC16, c16 = ci % kC16;
+      const int64_t row = own_row0 + r;
+      w0[i] = __ldg(reinterpret_cast<const uint4 *>(own0.q + row * own0.ld + own0.col + 16 * c16));
+      w1[i] = __ldg(reinterpret_cast<const uint4 *>(own1.q + row * own1.ld + own1.col + 16 * c16));
+      a0[i] = __ldg(own0.s + (row >> 5) * (own0.ld >> 5) + ((own0.col + 16 * c16) >> 5));
+      a1[i] = __ldg(own1.s + (row >> 5) * (own1.ld >> 5) + ((own1.col + 16 * c16) >> 5));
+    }
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      const int ci = t + 128 * i, r = ci / kC16, c16 = ci % kC16;
+      deq16_store(sOwn, r, 2 * c16, w0[i], a0[i]);
+      deq16_store(sOwn + SM::kTile, r, 2 * c16, w1[i], a1[i]);
+    }
+    fence_proxy_async_smem();
+    mbar_arrive(&B.own_full);
+  }
+  if (count > 0) scales(0);
+#pragma unroll 1
+  for (int j = 0; j < count; ++j) {
+    const int st = j & 1;
+    cp_async_wait<0>();
+    mbar_wait(&B.free_[st], ((j >> 1) & 1) ^ 1);
+    const uint32_t t0 = sLoop + 2 * st * SM::kTile, t1 = t0 + SM::kTile;
+    uint4 w0[kPer], w1[kPer];
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      w0[i] = lds128(s8 + 16 * (t + 128 * i));
+      w1[i] = lds128(s8 + SM::kStage8 + 16 * (t + 128 * i));
+    }
+    if (j + 1 < count) issue(j + 1);
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      const int ci = t + 128 * i, r = ci / kC16, c16 = ci % kC16;
+      deq16_store(t0, r, 2 * c16, w0[i], sa[i]);
+      deq16_store(t1, r, 2 * c16, w1[i], sb[i]);
+    }
+    fence_proxy_async_smem();
+    mbar_arrive(&B.full[st]);
+    if (j + 1 < count) scales(j + 1);
+  }
+  cp_async_wait<0>();
+}
+
+JF_DEV void bwd_init(BwdBars &B, int warp) {
+  if (threadIdx.x == 0) {
+    mbar_init(&B.own_full, 128);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&B.full[i], 128);
+      mbar_init(&B.free_[i], 1);
+    }
+    mbar_init(&B.s_full, 1);
+    mbar_init(&B.p_full, 128);
+    mbar_init(&B.done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 8) tmem_alloc(&B.tmem, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+}
+
+// dQ kernel: CTA = query tile i of (b, h); loops over kv tiles 0..i.
+//   S = Q K_j^T, dP = dO V_j^T (TMEM), dS = P (dP - D) / sqrt(d) (bf16, into S's columns),
+//   dQ += dS K_j (K_j read MN-major).  Also writes D_i = rowsum(dO * O) for the dK/dV kernel.
+// TMEM: S [0,128), dP [128,256), dQ [256, 256 + D).
+template <int D>
+__global__ void __launch_bounds__(288, 1) attn_bwd_dq_kernel(const BwdParams p) {
+  using SM = BwdSmem<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sOwn = smem_u32(base);        // Q, dO
+  const uint32_t sLoop = sOwn + 2 * SM::kTile; // stage s: K at +2s*kTile, V at +(2s+1)*kTile
+  const uint32_t s8 = sLoop + 4 * SM::kTile;
+  BwdBars &B = *reinterpret_cast<BwdBars *>(base + 6 * SM::kTile + 2 * SM::kStage8);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t S = p.seq, H = p.heads, C = H * D, C3 = 3 * C;
+  const int qt = (int)(S / BQ) - 1 - (int)blockIdx.x;
+  const int h = blockIdx.y, b = blockIdx.z;
+  const int64_t row0 = (int64_t)b * S + (int64_t)qt * BQ;
+  const int n = qt + 1;
+  bwd_init(B, warp);
+  const uint32_t tmem = B.tmem;
+
+  if (warp >= 4 && warp < 8) {
+    const Src q{p.qkv, p.qkv_s, C3, (int64_t)h * D}, dO{p.dout, p.dout_s, C, (int64_t)h * D};
+    const Src k{p.qkv, p.qkv_s, C3, C + (int64_t)h * D}, v{p.qkv, p.qkv_s, C3, 2 * C + (int64_t)h * D};
+    bwd_producer<D>(threadIdx.x - 128, sOwn, sLoop, s8, B, q, dO, row0, k, v, (int64_t)b * S, 0, n);
+  } else if (warp == 8) {
+    constexpr uint32_t idS = idesc_16(BQ, BKV, 0, 0, 1);
+    constexpr uint32_t idQ = idesc_16(BQ, D, 0, 1, 1);
+    mbar_wait(&B.own_full, 0);
+#pragma unroll 1
+    for (int j = 0; j < n; ++j) {
+      const int st = j & 1;
+      const uint32_t tk = sLoop + 2 * st * SM::kTile, tv = tk + SM::kTile;
+      mbar_wait(&B.full[st], (j >> 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) mma_bf16_ss(tmem, kdesc(sOwn, k), kdesc(tk, k), idS, k > 0 ? 1u : 0u);
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k)
+          mma_bf16_ss(tmem + BKV, kdesc(sOwn + SM::kTile, k), kdesc(tv, k), idS, k > 0 ? 1u : 0u);
+        mma_commit(&B.s_full);
+      }
+      __syncwarp();
+      mbar_wait(&B.p_full, j & 1);
+      tc_fence_after();
+      if (elect_one()) {
+#pragma unroll
+        for (int k = 0; k < BKV / 16; ++k)
+          mma_bf16_ts(tmem + 2 * BKV, tmem + 8 * k, mndesc(tk, k, p.mn_lbo, p.mn_sbo), idQ, (j > 0 || k > 0) ? 1u : 0u);
+        mma_commit(&B.free_[st]);
+        if (j == n - 1) mma_commit(&B.done);
+      }
+      __syncwarp();
+    }
+  } else if (warp < 4) {
+    const int r = threadIdx.x;
+    const int64_t row = row0 + r;
+    const uint32_t lb = tmem + ((uint32_t)(warp * 32) << 16);
+    const int64_t hs = ((int64_t)b * H + h) * S + (int64_t)qt * BQ + r;
+    // D_i = sum_d dO[i, d] * O[i, d] (dO dequantized exactly, O in bf16)
+    float dsum = 0.0f;
+    {
+      const int8_t *dq = p.dout + row * C + (int64_t)h * D;
+      const uint16_t *ob = p.o_bf + row * C + (int64_t)h * D;
+#pragma unroll 1
+      for (int c = 0; c < D; c += 32) {
+        const DeqScale ks = deq_scale(__ldg(p.dout_s + (row >> 5) * (C >> 5) + ((h * D + c) >> 5)));
+        const uint4 w0 = __ldg(reinterpret_cast<const uint4 *>(dq + c)),
+                    w1 = __ldg(reinterpret_cast<const uint4 *>(dq + c + 16));
+        const uint32_t u[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          const uint4 ov = __ldg(reinterpret_cast<const uint4 *>(ob + c + 8 * g));
+          const uint32_t o4[4] = {ov.x, ov.y, ov.z, ov.w};
+          float f[8];
+          deq4(u[2 * g], ks, f);
+          deq4(u[2 * g + 1], ks, f + 4);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            dsum = fmaf(f[2 * e], __uint_as_float(o4[e] << 16), dsum);
+            dsum = fmaf(f[2 * e + 1], __uint_as_float(o4[e] & 0xffff0000u), dsum);
+          }
+        }
+      }
+    }
+    p.dsum[hs] = dsum;
+    const float lse = p.lse[hs], c = p.scale_log2, sc = p.scale;
+#pragma unroll 1
+    for (int j = 0; j < n; ++j) {
+      mbar_wait(&B.s_full, j & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int q = 0; q < BKV / 32; ++q) {
+        uint32_t sr[32], dr[32];
+        tmem_ld_32x32b_x32(lb + 32 * q, sr);
+        tmem_ld_32x32b_x32(lb + BKV + 32 * q, dr);
+        wait_ld_dep(sr);
+        wait_ld_dep(dr);
+        uint32_t pk[16];
+#pragma unroll
+        for (int k = 0; k < 32; k += 2) {
+          float pr[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const bool masked = j == qt && 32 * q + k + e > r;
+            const float pe = masked ? 0.0f : ex2(fmaf(__uint_as_float(sr[k + e]), c, -lse));
+            pr[e] = pe * (__uint_as_float(dr[k + e]) - dsum) * sc;
+          }
+          pk[k / 2] = bf2(pr[0], pr[1]);
+        }
+        tmem_st_32x32b_x16(lb + 16 * q, pk);  // dS over the already-read S columns
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&B.p_full);
+    }
+    mbar_wait(&B.done, 0);
+    tc_fence_after();
+    int flags = 0;
+#pragma unroll 1
+    for (int q = 0; q < D / 32; ++q) {
+      const int64_t col = (int64_t)h * D + 32 * q;
+      flags |= quant_tmem_block(lb + 2 * BKV + 32 * q, 1.0f, p.dqkv + row * C3 + col,
+                                p.dqkv_s + (row >> 5) * (C3 >> 5) + (col >> 5), lane);
+    }
+    if (lane == 0) raise_flags(p.err, flags);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 8) tmem_dealloc(tmem, 512);
+}
+
+// dK/dV kernel: CTA = kv tile j of (b, h); loops over query tiles j..nq-1.
+//   S^T = K Q_i^T, dP^T = V dO_i^T (TMEM; thread = key row), P^T = exp2(S^T c - lse_q),
+//   dS^T = P^T (dP^T - D_q) / sqrt(d); dV += P^T dO_i, dK += dS^T Q_i (A from TMEM,
+//   Q_i / dO_i read MN-major).  TMEM: S^T [0,128), dP^T [128,256), dV, dK after.
+template <int D>
+__global__ void __launch_bounds__(288, 1) attn_bwd_dkv_kernel(const BwdParams p) {
+  using SM = BwdSmem<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sOwn = smem_u32(base);        // K, V
+  const uint32_t sLoop = sOwn + 2 * SM::kTile; // stage s: Q at +2s*kTile, dO at +(2s+1)*kTile
+  const uint32_t s8 = sLoop + 4 * SM::kTile;
+  BwdBars &B = *reinterpret_cast<BwdBars *>(base + 6 * SM::kTile + 2 * SM::kStage8);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t S = p.seq, H = p.heads, C = H * D, C3 = 3 * C;
+  const int nq = (int)(S / BQ);
+  const int kt = (int)blockIdx.x;  // heaviest (most query tiles) first
+  const int h = blockIdx.y, b = blockIdx.z;
+  const int64_t row0 = (int64_t)b * S + (int64_t)kt * BKV;
+  const int n = nq - kt;
+  bwd_init(B, warp);
+  const uint32_t tmem = B.tmem;
+
+  if (warp >= 4 && warp < 8) {
+    const Src k{p.qkv, p.qkv_s, C3, C + (int64_t)h * D}, v{p.qkv, p.qkv_s, C3, 2 * C + (int64_t)h * D};
+    const Src q{p.qkv, p.qkv_s, C3, (int64_t)h * D}, dO{p.dout, p.dout_s, C, (int64_t)h * D};
+    bwd_producer<D>(threadIdx.x - 128, sOwn, sLoop, s8, B, k, v, row0, q, dO, (int64_t)b * S, kt, n);
+  } else if (warp == 8) {
+    constexpr uint32_t idS = idesc_16(BKV, BQ, 0, 0, 1);
+    constexpr uint32_t idG = idesc_16(BKV, D, 0, 1, 1);
+    mbar_wait(&B.own_full, 0);
+#pragma unroll 1
+    for (int j = 0; j < n; ++j) {
+      const int st = j & 1;
+      const uint32_t tq = sLoop + 2 * st * SM::kTile, tdo = tq + SM::kTile;
+      mbar_wait(&B.full[st], (j >> 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) mma_bf16_ss(tmem, kdesc(sOwn, k), kdesc(tq, k), idS, k > 0 ? 1u : 0u);
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k)
+          mma_bf16_ss(tmem + BQ, kdesc(sOwn + SM::kTile, k), kdesc(tdo, k), idS, k > 0 ? 1u : 0u);
+        mma_commit(&B.s_full);
+      }
+      __syncwarp();
+      mbar_wait(&B.p_full, j & 1);
+      tc_fence_after();
+      if (elect_one()) {
+#pragma unroll
+        for (int k = 0; k < BQ / 16; ++k)
+          mma_bf16_ts(tmem + 2 * BQ, tmem + 8 * k, mndesc(tdo, k, p.mn_lbo, p.mn_sbo), idG, (j > 0 || k > 0) ? 1u : 0u);
+#pragma unroll
+        for (int k = 0; k < BQ / 16; ++k)
+          mma_bf16_ts(tmem + 2 * BQ + D, tmem + BQ + 8 * k, mndesc(tq, k, p.mn_lbo, p.mn_sbo), idG,
+                      (j > 0 || k > 0) ? 1u : 0u);
+        mma_commit(&B.free_[st]);
+        if (j == n - 1) mma_commit(&B.done);
+      }
+      __syncwarp();
+    }
+  } else if (warp < 4) {
+    const int r = threadIdx.x;  // key row
+    const int64_t row = row0 + r;
+    const uint32_t lb = tmem + ((uint32_t)(warp * 32) << 16);
+    const float c = p.scale_log2, sc = p.scale;
+    const int64_t hs0 = ((int64_t)b * H + h) * S;
+#pragma unroll 1
+    for (int j = 0; j < n; ++j) {
+      const int qt = kt + j;
+      const float *lse = p.lse + hs0 + (int64_t)qt * BQ, *dsv = p.dsum + hs0 + (int64_t)qt * BQ;
+      mbar_wait(&B.s_full, j & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int q = 0; q < BQ / 32; ++q) {
+        uint32_t sr[32], dr[32];
+        tmem_ld_32x32b_x32(lb + 32 * q, sr);
+        tmem_ld_32x32b_x32(lb + BQ + 32 * q, dr);
+        float lq[32], dq[32];
+#pragma unroll
+        for (int k = 0; k < 32; k += 4) {
+          *reinterpret_cast<float4 *>(lq + k) = __ldg(reinterpret_cast<const float4 *>(lse + 32 * q + k));
+          *reinterpret_cast<float4 *>(dq + k) = __ldg(reinterpret_cast<const float4 *>(dsv + 32 * q + k));
+        }
+        wait_ld_dep(sr);
+        wait_ld_dep(dr);
+        uint32_t pk[16], dk[16];
+#pragma unroll
+        for (int k = 0; k < 32; k += 2) {
+          float pr[2], ds[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const bool masked = j == 0 && 32 * q + k + e < r;  // query before key (diagonal tile)
+            pr[e] = masked ? 0.0f : ex2(fmaf(__uint_as_float(sr[k + e]), c, -lq[k + e]));
+            ds[e] = pr[e] * (__uint_as_float(dr[k + e]) - dq[k + e]) * sc;
+          }
+          pk[k / 2] = bf2(pr[0], pr[1]);
+          dk[k / 2] = bf2(ds[0], ds[1]);
+        }
+        tmem_st_32x32b_x16(lb + 16 * q, pk);
+        tmem_st_32x32b_x16(lb + BQ + 16 * q, dk);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&B.p_full);
+    }
+    mbar_wait(&B.done, 0);
+    tc_fence_after();
+    int flags = 0;
+#pragma unroll 1
+    for (int q = 0; q < D / 32; ++q) {
+      const int64_t ck = C + (int64_t)h * D + 32 * q, cv = 2 * C + (int64_t)h * D + 32 * q;
+      flags |= quant_tmem_block(lb + 2 * BQ + D + 32 * q, 1.0f, p.dqkv + row * C3 + ck,
+                                p.dqkv_s + (row >> 5) * (C3 >> 5) + (ck >> 5), lane);
+      flags |= quant_tmem_block(lb + 2 * BQ + 32 * q, 1.0f, p.dqkv + row * C3 + cv,
+                                p.dqkv_s + (row >> 5) * (C3 >> 5) + (cv >> 5), lane);
+    }
+    if (lane == 0) raise_flags(p.err, flags);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 8) tmem_dealloc(tmem, 512);
+}
+
+}  // namespace attn
+}  // namespace jf
+
+using namespace jf;
+using namespace jf::attn;
+
+static uint32_t g_mn_lbo = kHalf, g_mn_sbo = 1024;
+static long long *g_trace = nullptr;
+
+// diagnostics: MN-major descriptor strides and a device buffer for CTA-0 event clocks
+extern "C" int jf_attn_set_mn_desc(uint32_t lbo, uint32_t sbo) {
+  g_mn_lbo = lbo;
+  g_mn_sbo = sbo;
+  return JF_OK;
+}
+extern "C" int jf_attn_set_trace(long long *buf) {
+  g_trace = buf;
+  return JF_OK;
+}
+
+extern "C" int jf_attn_supported(int64_t seq, int64_t head_dim) {
+  return (seq > 0 && seq % (2 * BQ) == 0 && (head_dim == 64 || head_dim == 128)) ? 1 : 0;
+}
+
+extern "C" int jf_attn_fwd_q(const int8_t *qkv, const float *qkv_s, int64_t batch, int64_t seq, int64_t heads,
+                             int64_t head_dim, int8_t *o, float *o_s, uint16_t *o_bf, float *lse, int32_t *err,
+                             jf_stream_t stream) {
+  if (!jf_attn_supported(seq, head_dim) || batch <= 0 || heads <= 0 || heads > 65535 || batch > 65535)
+    return JF_ERR_UNSUPPORTED;
+  FwdParams p{qkv, qkv_s, batch, seq, heads, o, o_s, o_bf, lse, err,
+              (float)(1.4426950408889634 / sqrt((double)head_dim)), g_mn_lbo, g_mn_sbo, g_trace};
+  dim3 grid((unsigned)(seq / (2 * BQ)), (unsigned)heads, (unsigned)batch);
+  if (head_dim == 64) {
+    const int smem = FwdSmem<64>::kBytes;
+    if (int rc = jf_set_smem_attr((const void *)attn_fwd_kernel<64>, smem, "attn_fwd attr")) return rc;
+    attn_fwd_kernel<64><<<grid, kFwdThreads, smem, (cudaStream_t)stream>>>(p);
+  } else {
+    const int smem = FwdSmem<128>::kBytes;
+    if (int rc = jf_set_smem_attr((const void *)attn_fwd_kernel<128>, smem, "attn_fwd attr")) return rc;
+    attn_fwd_kernel<128><<<grid, kFwdThreads, smem, (cudaStream_t)stream>>>(p);
+  }
+  return jf_launch_check("attn_fwd");
+}
+
+extern "C" int jf_attn_bwd_q(const int8_t *qkv, const float *qkv_s, const int8_t *dout, const float *dout_s,
+                             const uint16_t *o_bf, const float *lse, float *dsum, int64_t batch, int64_t seq,
+                             int64_t heads, int64_t head_dim, int8_t *dqkv, float *dqkv_s, int32_t *err,
+                             jf_stream_t stream) {
+  if (!jf_attn_supported(seq, head_dim) || batch <= 0 || heads <= 0 || heads > 65535 || batch > 65535)
+    return JF_ERR_UNSUPPORTED;
+  BwdParams p{qkv, qkv_s, dout, dout_s, o_bf, lse, dsum, batch, seq, heads, dqkv, dqkv_s, err,
+              (float)(1.4426950408889634 / sqrt((double)head_dim)), (float)(1.0 / sqrt((double)head_dim)),
+              g_mn_lbo, g_mn_sbo};
+  dim3 grid((unsigned)(seq / BQ), (unsigned)heads, (unsigned)batch);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (head_dim == 64) {
+    const int smem = BwdSmem<64>::kBytes;
+    if (int rc = jf_set_smem_attr((const void *)attn_bwd_dq_kernel<64>, smem, "attn_bwd attr")) return rc;
+    if (int rc = jf_set_smem_attr((const void *)attn_bwd_dkv_kernel<64>, smem, "attn_bwd attr")) return rc;
+    attn_bwd_dq_kernel<64><<<grid, 288, smem, st>>>(p);
+    attn_bwd_dkv_kernel<64><<<grid, 288, smem, st>>>(p);
+  } else {
+    const int smem = BwdSmem<128>::kBytes;
+    if (int rc = jf_set_smem_attr((const void *)attn_bwd_dq_kernel<128>, smem, "attn_bwd attr")) return rc;
+    if (int rc = jf_set_smem_attr((const void *)attn_bwd_dkv_kernel<128>, smem, "attn_bwd attr")) return rc;
+    attn_bwd_dq_kernel<128><<<grid, 288, smem, st>>>(p);
+    attn_bwd_dkv_kernel<128><<<grid, 288, smem, st>>>(p);
+  }
+  return jf_launch_check("attn_bwd");
+}

@@ -236,6 +236,44 @@ class AttentionCore:
     def supports_q(self) -> bool:
         return self.dtype == torch.bfloat16 and self.head_dim % 16 == 0
 
+    def fused(self, seq: int) -> bool:
+        """runtime.set_attention('fused') and a shape the fused kernels take."""
+        return (_rt.attention() == "fused" and self.dtype == torch.bfloat16
+                and bool(_lib.lib().jf_attn_supported(seq, self.head_dim)))
+
+    def _forward_fused(self, qkv_q: BlockQuantTensor, batch: int, seq: int) -> BlockQuantTensor:
+        """One kernel: INT8 QKV codes -> causal attention (tcgen05, bf16 operands, FP32
+        accumulation) -> INT8 O codes + block scales.  Saves O (bf16) and the per-row
+        log-sum-exp for the backward."""
+        L = _lib.lib()
+        c = self.heads * self.head_dim
+        dev = qkv_q.device
+        out = empty_like_shape(batch * seq, c, dev)
+        o_bf = torch.empty(batch * seq, c, dtype=torch.bfloat16, device=dev)
+        lse = torch.empty(batch, self.heads, seq, dtype=torch.float32, device=dev)
+        _lib.check(L.jf_attn_fwd_q(qkv_q.values.data_ptr(), qkv_q.scales.data_ptr(), batch, seq, self.heads,
+                                   self.head_dim, out.values.data_ptr(), out.scales.data_ptr(), o_bf.data_ptr(),
+                                   lse.data_ptr(), _rt.err_ptr(), _lib.stream_handle()), "attn_fwd")
+        _rt.maybe_check()
+        self._saved = ("fused", qkv_q, o_bf, lse)
+        return out
+
+    def _backward_fused(self, dattn_q: BlockQuantTensor, batch: int, seq: int) -> BlockQuantTensor:
+        """Two kernels (dQ, then dK/dV): INT8 dO codes in, INT8 dQ|dK|dV out."""
+        _, qkv_q, o_bf, lse = self._saved
+        self._saved = None
+        L = _lib.lib()
+        c = self.heads * self.head_dim
+        dev = dattn_q.device
+        dqkv = empty_like_shape(batch * seq, 3 * c, dev)
+        dsum = torch.empty(batch, self.heads, seq, dtype=torch.float32, device=dev)
+        _lib.check(L.jf_attn_bwd_q(qkv_q.values.data_ptr(), qkv_q.scales.data_ptr(), dattn_q.values.data_ptr(),
+                                   dattn_q.scales.data_ptr(), o_bf.data_ptr(), lse.data_ptr(), dsum.data_ptr(),
+                                   batch, seq, self.heads, self.head_dim, dqkv.values.data_ptr(),
+                                   dqkv.scales.data_ptr(), _rt.err_ptr(), _lib.stream_handle()), "attn_bwd")
+        _rt.maybe_check()
+        return dqkv
+
     def forward_q(self, qkv_q: BlockQuantTensor, batch: int, seq: int) -> BlockQuantTensor:
         """deq(QKV) -> SDPA -> quantize (qlayers.py:350-351), per-head layouts end to end:
         the codes are dequantized straight into contiguous [b, h, s, d] q/k/v and the
@@ -243,6 +281,8 @@ class AttentionCore:
         c = self.heads * self.head_dim
         if qkv_q.shape != (batch * seq, 3 * c):
             raise ValueError(f"expected ({batch * seq}, {3 * c}), got {qkv_q.shape}")
+        if self.fused(seq):
+            return self._forward_fused(qkv_q, batch, seq)
         L = _lib.lib()
         shape = (batch, self.heads, seq, self.head_dim)
         q, k, v = (torch.empty(shape, dtype=torch.bfloat16, device=qkv_q.device) for _ in range(3))
@@ -263,6 +303,8 @@ class AttentionCore:
         """deq(dO) -> SDPA backward -> quantize dQ|dK|dV into one [N, 3C] tensor (qlayers.py:406-408)."""
         if self._saved is None:
             raise RuntimeError("backward called before forward")
+        if self._saved[0] == "fused":
+            return self._backward_fused(dattn_q, batch, seq)
         q, k, v, o = self._saved
         self._saved = None
         c = self.heads * self.head_dim

@@ -20,7 +20,7 @@ _MSG_NONFINITE = "input contains non-finite values"
 _MSG_OVERFLOW = "scale overflows the binary16 range; input magnitude too large"
 
 _state = threading.local()
-_config = {"error_check": "eager", "promotion": "exact", "operands": "int8"}
+_config = {"error_check": "eager", "promotion": "exact", "operands": "int8", "attention": "sdpa"}
 _gemm_options = {"tma_scales": 1}
 
 
@@ -70,6 +70,22 @@ def set_gemm_operands(kind: str) -> None:
     if kind not in ("int8", "f16", "auto"):
         raise ValueError(f"operands must be 'int8', 'f16' or 'auto', got {kind!r}")
     _config["operands"] = kind
+
+
+def set_attention(kind: str) -> None:
+    """Attention island of the INT8 block (qlayers.py:187-236, boundary :350-351/:406-408):
+    'sdpa' (default: codes dequantized to bf16 head tensors, cuDNN SDPA, outputs
+    requantized by boundary kernels) or 'fused' (libjetfire's tcgen05 attention kernels
+    read the INT8 QKV / dO codes and write INT8 O / dQ|dK|dV directly: no bf16 head
+    tensor in HBM).  Both compute in bf16 with FP32 accumulation; 'fused' needs
+    seq % 256 == 0 and head_dim in {64, 128} (other shapes use 'sdpa')."""
+    if kind not in ("sdpa", "fused"):
+        raise ValueError(f"attention must be 'sdpa' or 'fused', got {kind!r}")
+    _config["attention"] = kind
+
+
+def attention() -> str:
+    return _config["attention"]
 
 
 # 'auto' threshold: measured on B200 -- 4096x12288x4096 and larger gain 7% with f16

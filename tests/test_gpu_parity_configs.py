@@ -251,6 +251,29 @@ def test_config2_block_end_to_end(jf, cfg2_oracle, attn_dtype):
         assert e_out <= 0.01 and e_dx <= 0.02 and max(e_g.values()) <= 0.02, (e_out, e_dx, e_g)
 
 
+def test_config2_block_fused_attention_vs_oracle(jf, cfg2_oracle):
+    """The config-2 block with the fused INT8-boundary attention kernels
+    (runtime.set_attention('fused'), csrc/attn.cu) against the chained oracle block:
+    the reference's block tolerances (test_qlayers.py:257-273)."""
+    r = cfg2_oracle
+    p = r["p"]
+    cfg = jf.BlockConfig(c_model=C2, heads=HEADS2, hidden=HID2, block=32, dropout_p=0.0)
+    jf.runtime.set_attention("fused")
+    try:
+        blk = jf.TransformerBlock.from_parameters(cfg, dict(p), attn_dtype=torch.bfloat16)
+        assert blk.attn.fused(SEQ2)
+        out = blk.forward(bqt(jf, *r["x"]), BATCH2, SEQ2)
+        dx, grads = blk.backward(bqt(jf, *r["dy"]))
+    finally:
+        jf.runtime.set_attention("sdpa")
+    e_out = rel(npy(out.dequantize()), O.dequantize(*r["out"][:2]))
+    e_dx = rel(npy(dx.dequantize()), O.dequantize(*r["dx"][:2]))
+    ref_g = {"mlp2.w": r["b_mlp2"][2], "mlp1.w": r["b_mlp1"][2], "proj.w": r["b_proj"][2],
+             "qkv.w": r["b_qkv"][2], "qkv.b": r["b_qkv"][3], "ln1.gamma": r["b_ln1"][2]}
+    e_g = {k: rel(npy(grads[k]), v) for k, v in ref_g.items()}
+    assert e_out <= 0.06 and e_dx <= 0.08 and max(e_g.values()) <= 0.12, (e_out, e_dx, e_g)
+
+
 # ── config 4: all 12 GEMMs, full width and full K, row-sampled oracle ───
 
 N4, C4, H4 = 4096, 4096, 16384
