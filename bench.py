@@ -36,6 +36,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "transformer-block fwd+bwd tokens/s; per-block INT8 GEMM TOPS vs INT8 peak"
 INT8_PEAK_TOPS = 4500.0  # B200 dense INT8 datasheet (no measured INT8 figure in MEASURED_PEAKS.json)
+KIND_I8_MEASURED_TOPS = 8178.0 * 2 * 148 * 1965e6 / 1e12  # our raw tcgen05 kind::i8 microbenchmark ceiling
 
 WORKLOADS = {
     # BASELINE.json configs[0]: one QuantLinear fwd+bwd, the reference's own CPU-runnable case
@@ -610,6 +611,10 @@ def roofline(gemm_tops: float, promotion: str, clocks_mhz=None, operands: str = 
             "traffic": traffic, "traffic_launch": tr_src,
             "peak_source": "B200 dense INT8 datasheet 4.5 POPS (int ops counted as FLOP); "
                            "MEASURED_PEAKS.json has no INT8 entry",
+            "measured_peak": {"value": round(KIND_I8_MEASURED_TOPS, 1), "unit": "TFLOP/s",
+                              "frac": round(gemm_tops / KIND_I8_MEASURED_TOPS, 4),
+                              "source": "raw tcgen05.mma kind::i8 M128 N128 K32 back to back: 8178 MAC/clk/SM "
+                                        "x 148 SMs x 1965 MHz (microbench.cu, profiles/r1e_microbench.jsonl)"},
             "promotion_bound": {"value": round(bound, 1), "unit": "TFLOP/s", "why": why,
                                 "frac": round(gemm_tops / bound, 4)}}
 
@@ -753,6 +758,27 @@ def bf16_model_tokens_per_s(w, steps, warmup):
 # ── CPU oracle (the reference's algorithm, numpy port) ──────────────────
 
 
+def host_info():
+    """What the CPU baseline ran on: CPU model, numpy and its BLAS."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    blas = None
+    try:
+        cfg = np.show_config(mode="dicts")
+        b = cfg["Build Dependencies"]["blas"]
+        blas = f"{b.get('name')} {b.get('version')}"
+    except Exception:  # noqa: BLE001 -- informational only
+        pass
+    return {"cpu": model, "logical_cpus": os.cpu_count(), "numpy": np.__version__, "blas": blas}
+
+
 def cpu_block_sample(w, tokens, reps=1):
     """Time oracle block fwd+bwd on `tokens` tokens of the workload's block dims."""
     from oracle import int8flow_oracle as O
@@ -774,7 +800,7 @@ def cpu_block_sample(w, tokens, reps=1):
     return {"value": round(batch * seq / t, 2), "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
             "sample": f"oracle (numpy port of int8flow) block fwd+bwd, {batch}x{seq} tokens at "
                       f"hidden {c}/mlp {h}, OpenBLAS threads = all host cores, best of {reps}",
-            "seconds": round(t, 3)}
+            "seconds": round(t, 3), "host": host_info()}
 
 
 def cpu_linear_sample(w, tokens, reps=1):
@@ -798,7 +824,7 @@ def cpu_linear_sample(w, tokens, reps=1):
     return {"value": round(tokens / t, 2), "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
             "sample": f"oracle (numpy port of int8flow) QuantLinear {c}->{d} fwd+bwd, {tokens} tokens, "
                       f"OpenBLAS threads = all host cores, best of {reps}",
-            "seconds": round(t, 3)}
+            "seconds": round(t, 3), "host": host_info()}
 
 
 def cpu_sample(w, tokens):

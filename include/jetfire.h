@@ -206,6 +206,10 @@ int jf_adamw_multi(const void *tensors, const int32_t *chunk_tensor, const int64
 
 /* Dropout by scale folding  [qnonlinear.py:207-240]: codes zeroed where keep[i]==0,
  * scales snapped f16(s * keep_factor).  keep: [n x c] uint8 (the materialized mask). */
+/* DropoutState.generate's keep mask  [qnonlinear.py:190-200]: keep[i] = (numpy
+ * Generator(Philox(key=(key0, key1))).random() of element i) >= p, bit-identical to numpy
+ * (Philox4x64-10, 53-bit doubles); total = rows*cols elements, keep is uint8 0/1. */
+int jf_philox_keep(uint64_t key0, uint64_t key1, double p, int64_t total, uint8_t *keep, jf_stream_t stream);
 int jf_dropout(const int8_t *q, const float *s, const uint8_t *keep, float keep_factor,
                int64_t n, int64_t c, int8_t *oq, float *os, int32_t *err, jf_stream_t stream);
 

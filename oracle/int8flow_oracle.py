@@ -414,3 +414,34 @@ def block_backward(p, saved, dyq, dys):
              "mlp1.b": db_m1, "mlp2.w": dw_m2, "mlp2.b": db_m2, "ln1.gamma": dg1, "ln1.beta": db1,
              "ln2.gamma": dg2, "ln2.beta": db2}
     return (dxq, dxs), grads
+
+
+# ── DropoutState.generate's random stream (qnonlinear.py:190-200) ──────
+# numpy's Generator(Philox(key=seed)).random(n), restated (the algorithm the CUDA
+# kernel jf_philox_keep runs): Philox4x64-10 (Random123), counter incremented before
+# each block of four 64-bit outputs (the first block uses counter 1), doubles =
+# (u64 >> 11) * 2^-53.  Pure-Python integers: for small n only.
+_M64 = (1 << 64) - 1
+
+
+def philox4x64_10(ctr, key):
+    c0, c1, c2, c3 = ctr
+    k0, k1 = key
+    for r in range(10):
+        if r:
+            k0 = (k0 + 0x9E3779B97F4A7C15) & _M64
+            k1 = (k1 + 0xBB67AE8584CAA73B) & _M64
+        p0 = 0xD2E7470EE14C6C93 * c0
+        p1 = 0xCA5A826395121157 * c2
+        c0, c1, c2, c3 = ((p1 >> 64) ^ c1 ^ k0, p1 & _M64, (p0 >> 64) ^ c3 ^ k1, p0 & _M64)
+    return c0, c1, c2, c3
+
+
+def philox_random(key, n):
+    out = np.empty(n, dtype=np.float64)
+    for g in range((n + 3) // 4):
+        words = philox4x64_10((g + 1, 0, 0, 0), key)
+        for e in range(4):
+            if 4 * g + e < n:
+                out[4 * g + e] = (words[e] >> 11) * (1.0 / 9007199254740992.0)
+    return out

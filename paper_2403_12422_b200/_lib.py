@@ -65,6 +65,7 @@ SIGNATURES = {
     "jf_gelu_bwd": (ctypes.c_int, [_P, _P, _P, _P, _I64, _I64, _P, _P, _P, _P, _P]),
     "jf_colsum": (ctypes.c_int, [_P, _P, _I64, _I64, _P, _P, _P]),
     "jf_colsum_workspace_bytes": (_SZ, [_I64, _I64]),
+    "jf_philox_keep": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_double, _I64, _P, _P]),
     "jf_dropout": (ctypes.c_int, [_P, _P, _P, _F32, _I64, _I64, _P, _P, _P, _P]),
     "jf_gemm_set_option": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int]),
     "jf_adamw": (ctypes.c_int, [_P, _P, _P, _P, _I64, _F32, ctypes.c_double, ctypes.c_double, _F32, _F32, _F32,
@@ -138,7 +139,7 @@ def stream_handle() -> int:
 KERNELS_PER_CALL = {
     "quantize": 1, "dequantize": 1, "transpose": 1, "gemm_fwd": 1, "gemm_dgrad": 1, "gemm_wgrad": 1,
     "gemm_partials": 1, "add_stats": 1, "ln_fwd": 2, "ln_bwd": 4, "gelu_fwd": 1, "gelu_bwd": 1,
-    "colsum": 2, "dropout": 1, "gelu_tables": 1, "dequant_qkv_heads": 1, "quantize_heads": 1,
+    "colsum": 2, "dropout": 1, "philox_keep": 1, "gelu_tables": 1, "dequant_qkv_heads": 1, "quantize_heads": 1,
     "cross_entropy": 1, "attn_fwd": 1, "attn_bwd": 2, "adamw": 1, "adamw_quantize": 1, "adamw_multi": 1, "widen_codes": 1, "gemm_f16": 1,
 }
 launch_count = [0]

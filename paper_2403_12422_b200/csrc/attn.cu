@@ -568,6 +568,7 @@ struct BwdParams {
   int32_t *err;
   float scale_log2, scale;
   uint32_t mn_lbo, mn_sbo;
+  long long *trace;
 };
 
 template <int D>
@@ -589,7 +590,8 @@ struct BwdBars {
 // into the 2-stage bf16 ring.
 template <int D>
 JF_DEV void bwd_producer(int t, uint32_t sOwn, uint32_t sLoop, uint32_t s8, BwdBars &B, Src own0, Src own1,
-                         int64_t own_row0, Src l0, Src l1, int64_t row_b, int first, int count) {
+                         int64_t own_row0, Src l0, Src l1, int64_t row_b, int first, int count,
+                         const BwdParams &p) {
   using SM = BwdSmem<D>;
   constexpr int kC16 = D / 16, kChunks = BKV * kC16, kPer = kChunks / 128;
   auto issue = [&](int j) {
@@ -639,7 +641,9 @@ JF_DEV void bwd_producer(int t, uint32_t sOwn, uint32_t sLoop, uint32_t s8, BwdB
   for (int j = 0; j < count; ++j) {
     const int st = j & 1;
     cp_async_wait<0>();
+    if (t == 0) ATR(0, j);
     mbar_wait(&B.free_[st], ((j >> 1) & 1) ^ 1);
+    if (t == 0) ATR(1, j);
     const uint32_t t0 = sLoop + 2 * st * SM::kTile, t1 = t0 + SM::kTile;
     uint4 w0[kPer], w1[kPer];
 #pragma unroll
@@ -655,6 +659,7 @@ JF_DEV void bwd_producer(int t, uint32_t sOwn, uint32_t sLoop, uint32_t s8, BwdB
       deq16_store(t1, r, 2 * c16, w1[i], sb[i]);
     }
     fence_proxy_async_smem();
+    if (t == 0) ATR(2, j);
     mbar_arrive(&B.full[st]);
     if (j + 1 < count) scales(j + 1);
   }
@@ -704,7 +709,7 @@ __global__ void __launch_bounds__(288, 1) attn_bwd_dq_kernel(const BwdParams p) 
   if (warp >= 4 && warp < 8) {
     const Src q{p.qkv, p.qkv_s, C3, (int64_t)h * D}, dO{p.dout, p.dout_s, C, (int64_t)h * D};
     const Src k{p.qkv, p.qkv_s, C3, C + (int64_t)h * D}, v{p.qkv, p.qkv_s, C3, 2 * C + (int64_t)h * D};
-    bwd_producer<D>(threadIdx.x - 128, sOwn, sLoop, s8, B, q, dO, row0, k, v, (int64_t)b * S, 0, n);
+    bwd_producer<D>(threadIdx.x - 128, sOwn, sLoop, s8, B, q, dO, row0, k, v, (int64_t)b * S, 0, n, p);
   } else if (warp == 8) {
     constexpr uint32_t idS = idesc_16(BQ, BKV, 0, 0, 1);
     constexpr uint32_t idQ = idesc_16(BQ, D, 0, 1, 1);
@@ -839,7 +844,7 @@ __global__ void __launch_bounds__(288, 1) attn_bwd_dkv_kernel(const BwdParams p)
   if (warp >= 4 && warp < 8) {
     const Src k{p.qkv, p.qkv_s, C3, C + (int64_t)h * D}, v{p.qkv, p.qkv_s, C3, 2 * C + (int64_t)h * D};
     const Src q{p.qkv, p.qkv_s, C3, (int64_t)h * D}, dO{p.dout, p.dout_s, C, (int64_t)h * D};
-    bwd_producer<D>(threadIdx.x - 128, sOwn, sLoop, s8, B, k, v, row0, q, dO, (int64_t)b * S, kt, n);
+    bwd_producer<D>(threadIdx.x - 128, sOwn, sLoop, s8, B, k, v, row0, q, dO, (int64_t)b * S, kt, n, p);
   } else if (warp == 8) {
     constexpr uint32_t idS = idesc_16(BKV, BQ, 0, 0, 1);
     constexpr uint32_t idG = idesc_16(BKV, D, 0, 1, 1);
@@ -849,6 +854,7 @@ __global__ void __launch_bounds__(288, 1) attn_bwd_dkv_kernel(const BwdParams p)
       const int st = j & 1;
       const uint32_t tq = sLoop + 2 * st * SM::kTile, tdo = tq + SM::kTile;
       mbar_wait(&B.full[st], (j >> 1) & 1);
+      if (lane == 0) ATR(4, j);
       tc_fence_after();
       if (elect_one()) {
 #pragma unroll
@@ -860,6 +866,7 @@ __global__ void __launch_bounds__(288, 1) attn_bwd_dkv_kernel(const BwdParams p)
       }
       __syncwarp();
       mbar_wait(&B.p_full, j & 1);
+      if (lane == 0) ATR(5, j);
       tc_fence_after();
       if (elect_one()) {
 #pragma unroll
@@ -884,7 +891,9 @@ __global__ void __launch_bounds__(288, 1) attn_bwd_dkv_kernel(const BwdParams p)
     for (int j = 0; j < n; ++j) {
       const int qt = kt + j;
       const float *lse = p.lse + hs0 + (int64_t)qt * BQ, *dsv = p.dsum + hs0 + (int64_t)qt * BQ;
+      if (r == 0) ATR(7, j);
       mbar_wait(&B.s_full, j & 1);
+      if (r == 0) ATR(8, j);
       tc_fence_after();
 #pragma unroll 1
       for (int q = 0; q < BQ / 32; ++q) {
@@ -917,6 +926,7 @@ __global__ void __launch_bounds__(288, 1) attn_bwd_dkv_kernel(const BwdParams p)
       }
       tmem_wait_st();
       tc_fence_before();
+      if (r == 0) ATR(9, j);
       mbar_arrive(&B.p_full);
     }
     mbar_wait(&B.done, 0);
@@ -989,7 +999,7 @@ extern "C" int jf_attn_bwd_q(const int8_t *qkv, const float *qkv_s, const int8_t
     return JF_ERR_UNSUPPORTED;
   BwdParams p{qkv, qkv_s, dout, dout_s, o_bf, lse, dsum, batch, seq, heads, dqkv, dqkv_s, err,
               (float)(1.4426950408889634 / sqrt((double)head_dim)), (float)(1.0 / sqrt((double)head_dim)),
-              g_mn_lbo, g_mn_sbo};
+              g_mn_lbo, g_mn_sbo, g_trace};
   dim3 grid((unsigned)(seq / BQ), (unsigned)heads, (unsigned)batch);
   cudaStream_t st = (cudaStream_t)stream;
   if (head_dim == 64) {

@@ -7,6 +7,8 @@
 // pairwise order (see oracle.pairwise_sum) so codes, scales and statistics
 // are bit-exact; column (axis-0) parameter-gradient sums are reduced
 // strip-wise (tolerance).
+#include <algorithm>
+
 #include "tile.cuh"
 
 namespace jf {
@@ -702,6 +704,50 @@ __global__ void __launch_bounds__(256) dropout_kernel(const int8_t *__restrict__
   }
 }
 
+// ── DropoutState.generate's keep mask on the device (qnonlinear.py:190-200) ──
+// numpy's Generator(Philox(key=seed)).random(shape) >= p, bit for bit: Philox4x64-10
+// (Random123), 128-bit counter starting at 1 for the first block of four outputs
+// (numpy increments before generating), element i = word i % 4 of block i / 4 + 1,
+// random() = (u64 >> 11) * 2^-53 in double precision.
+JF_DEV void philox4x64_10(uint64_t (&c)[4], uint64_t k0, uint64_t k1) {
+  constexpr uint64_t M0 = 0xD2E7470EE14C6C93ull, M1 = 0xCA5A826395121157ull;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) {
+      k0 += 0x9E3779B97F4A7C15ull;
+      k1 += 0xBB67AE8584CAA73Bull;
+    }
+    const uint64_t lo0 = M0 * c[0], hi0 = __umul64hi(M0, c[0]);
+    const uint64_t lo1 = M1 * c[2], hi1 = __umul64hi(M1, c[2]);
+    const uint64_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+    c[0] = n0;
+    c[1] = lo1;
+    c[2] = n2;
+    c[3] = lo0;
+  }
+}
+
+__global__ void __launch_bounds__(256) philox_keep_kernel(uint64_t k0, uint64_t k1, double p, int64_t total,
+                                                          uint8_t *keep) {
+  const int64_t groups = (total + 3) / 4;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < groups;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t c[4] = {(uint64_t)g + 1, 0, 0, 0};
+    philox4x64_10(c, k0, k1);
+    uint32_t w = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const double u = (double)(c[e] >> 11) * (1.0 / 9007199254740992.0);
+      w |= (uint32_t)(u >= p) << (8 * e);
+    }
+    if (4 * g + 3 < total) {
+      reinterpret_cast<uint32_t *>(keep)[g] = w;
+    } else {
+      for (int e = 0; 4 * g + e < total; ++e) keep[4 * g + e] = (w >> (8 * e)) & 1u;
+    }
+  }
+}
+
 }  // namespace jf
 
 using namespace jf;
@@ -850,6 +896,15 @@ extern "C" int jf_gelu_bwd(const int8_t *x, const float *xs, const int8_t *dy, c
   gelu_bwd_kernel<<<tile_grid(n, c), kTileThreads, 0, (cudaStream_t)stream>>>(x, xs, dy, dys, n,
                                                                               c, dxq, dxs, err, tables);
   return jf_launch_check("gelu_bwd");
+}
+
+extern "C" int jf_philox_keep(uint64_t key0, uint64_t key1, double p, int64_t total, uint8_t *keep,
+                              jf_stream_t stream) {
+  if (total <= 0 || !(p >= 0.0 && p < 1.0)) return JF_ERR_ARG;
+  const int64_t groups = (total + 3) / 4;
+  const int blocks = (int)std::min<int64_t>((groups + 255) / 256, 148 * 16);
+  philox_keep_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(key0, key1, p, total, keep);
+  return jf_launch_check("philox_keep");
 }
 
 extern "C" int jf_dropout(const int8_t *q, const float *s, const uint8_t *keep, float keep_factor,

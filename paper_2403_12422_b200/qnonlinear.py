@@ -140,8 +140,10 @@ def gelu_backward(xq: BlockQuantTensor, dyq: BlockQuantTensor,
 class DropoutState:
     """Drop probability, seed and the materialized keep mask (qnonlinear.py:181-204).
 
-    The mask is drawn on the host with numpy's Philox keyed by ``seed`` —
-    the reference's generator, so masks are bit-identical — and uploaded.
+    The mask is drawn on the device (``jf_philox_keep``): numpy's Philox4x64-10
+    stream keyed by ``seed`` and its 53-bit ``random()`` doubles, restated in CUDA,
+    so masks are bit-identical to the reference's without a host draw or upload.
+    The key words come from numpy's own seed conversion (``Philox(key=seed)``).
     """
 
     p: float
@@ -154,8 +156,12 @@ class DropoutState:
             raise ValueError(f"drop probability must be in [0, 1), got {p}")
         if p == 0.0:
             return cls(p, seed, None)  # identity: every element kept
-        u = np.random.Generator(np.random.Philox(key=seed)).random(shape)
-        return cls(p, seed, torch.from_numpy(u >= p).cuda())
+        k0, k1 = (int(w) for w in np.random.Philox(key=seed).state["state"]["key"])
+        rows, cols = shape
+        mask = torch.empty((rows, cols), dtype=torch.bool, device="cuda")
+        _lib.check(_lib.lib().jf_philox_keep(k0, k1, float(p), rows * cols, mask.data_ptr(),
+                                             _lib.stream_handle()), "philox_keep")
+        return cls(p, seed, mask)
 
     @property
     def keep_factor(self) -> np.float32:

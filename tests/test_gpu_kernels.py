@@ -457,11 +457,23 @@ def test_dropout_mask_and_scales(jf):
     t = bqt(jf, q, s)
     st = jf.DropoutState.generate(0.5, 10, (64, 64))
     mask = npy(st.mask)
+    # drawn on the device, bit-identical to the reference's numpy Philox draw
+    assert np.array_equal(mask, np.random.Generator(np.random.Philox(key=10)).random((64, 64)) >= 0.5)
     y = jf.dropout_forward(t, st)
     assert same(y.values, np.where(mask, q, np.int8(0)))
     assert same(y.scales, O.f16_snap(s * np.float32(2.0)))
     same0 = jf.dropout_forward(t, jf.DropoutState.generate(0.0, 1, (64, 64)))
     assert same0 is t
+
+
+@pytest.mark.parametrize("p,seed,shape", [(0.1, (3, 1), (4096, 1024)), (0.37, 2**70 + 5, (96, 160)),
+                                          (0.9, 0, (32, 32)), (0.5, (2**64 - 1, 7), (2048, 4096))])
+def test_dropout_mask_device_philox_vs_numpy(jf, p, seed, shape):
+    """jf_philox_keep == Generator(Philox(key=seed)).random(shape) >= p (qnonlinear.py:190-200)
+    for int, 128-bit and pair seeds, including masks past 2^22 elements."""
+    st = jf.DropoutState.generate(p, seed, shape)
+    want = np.random.Generator(np.random.Philox(key=seed)).random(shape) >= p
+    assert np.array_equal(npy(st.mask), want)
 
 
 # ── layers ──────────────────────────────────────────────────────────────

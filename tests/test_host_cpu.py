@@ -141,3 +141,14 @@ def test_runtime_knobs():
     with pytest.raises(ValueError):
         runtime.set_error_check("never")
     assert runtime.promotion_code("fast") == 1 and runtime.promotion_code("exact") == 0
+
+
+@pytest.mark.parametrize("seed", [0, 10, (7, 2), 2**70 + 3, (2**64 - 1, 5)])
+def test_philox_restatement_matches_numpy(seed):
+    """The Philox4x64-10 stream jf_philox_keep computes == numpy's Generator(Philox).random()
+    (DropoutState.generate, qnonlinear.py:190-200)."""
+    from oracle import int8flow_oracle as O
+
+    key = tuple(int(w) for w in np.random.Philox(key=seed).state["state"]["key"])
+    want = np.random.Generator(np.random.Philox(key=seed)).random(37)
+    assert np.array_equal(O.philox_random(key, 37), want)

@@ -89,6 +89,16 @@ def runb():
                          err.data_ptr(), _lib.stream_handle())
     assert rc == 0, L.jf_last_error()
 runb(); torch.cuda.synchronize()
+if a.trace:
+    tr = torch.zeros(16 * 64, dtype=torch.int64, device="cuda")
+    L.jf_attn_set_trace(tr.data_ptr()); runb(); torch.cuda.synchronize(); L.jf_attn_set_trace(None)
+    t = tr.view(16, 64).cpu()
+    t0 = t[t > 0].min().item()
+    names = {0: "P:cp_done", 1: "P:free", 2: "P:conv_done", 4: "M:full", 5: "M:p_full", 7: "C:wait_s", 8: "C:s_full",
+             9: "C:p_done"}
+    print("bwd (dkv CTA 0; dq kernel ran first and shares events 0-2) tile " + " ".join(f"{v:>11s}" for v in names.values()))
+    for j in range(s // 128):
+        print(f"{j:4d} " + " ".join(f"{(t[e, j].item() - t0) if t[e, j] > 0 else -1:11d}" for e in names))
 gg = (dq.float().view(b * s // 32, 32, 3 * c // 32, 32) * dqs.view(b * s // 32, 1, 3 * c // 32, 1)).view(b * s, 3 * c)
 dref = (dO * o32.detach()).sum(-1)
 print(f"  bwd: dsum rel {((dsum - dref).abs().max() / dref.abs().max()).item():.3e}", end="")
