@@ -94,12 +94,48 @@ JF_DEV int quant_code_try(float x, float r, bool &tie) {
 struct DeqScale {
   float s8, c;
 };
+JF_DEV uint32_t prmt_raw(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+  return d;
+}
 JF_DEV DeqScale deq_scale(float s) { return {__fmul_rn(s, 0.00390625f), __fmul_rn(-32896.0f, s)}; }
 JF_DEV float deq_code(uint32_t biased_word, int j, DeqScale k) {
   uint32_t bits;
   asm("prmt.b32 %0, %1, %2, %3;" : "=r"(bits) : "r"(biased_word), "r"(0x4B000000u), "r"(0x7404u | (j << 4)));
   return __fmaf_rn(__uint_as_float(bits), k.s8, k.c);
 }
+// ── packed / 3-input helpers of the tile kernels ──────────────────────
+// fp32x2 ops (defined below the PTX wrappers) are forward-declared here.
+JF_DEV void ffma2_rn(float &d0, float &d1, float a0, float a1, float b0, float b1, float c0, float c1);
+JF_DEV void fadd2_rn(float &d0, float &d1, float a0, float a1, float b0, float b1);
+JF_DEV void fsub2_rn(float &d0, float &d1, float a0, float a1, float b0, float b1);
+
+// max(|a|, |b|, |c|), NaN if any input is NaN (3-input max, sm_100).
+JF_DEV float absmax3_nan(float a, float b, float c) {
+  float d;
+  asm("max.NaN.abs.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
+// +0.0f read through a volatile global: a value neither NVVM nor ptxas can fold, used
+// as the addend that turns a packed product into an FFMA2 (no mul/add contraction).
+__device__ float g_opaque_zero = 0.0f;
+JF_DEV float opaque_zero() { return *reinterpret_cast<volatile float *>(&g_opaque_zero); }
+
+// 8 codes (two words) -> v[0..7], exact: PRMT into a 2^23 mantissa + packed FFMA2.
+JF_DEV void deq8_packed(uint32_t w0, uint32_t w1, DeqScale k, float *v) {
+  const uint32_t u[2] = {w0 ^ 0x80808080u, w1 ^ 0x80808080u};
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int j = 0; j < 4; j += 2) {
+      const uint32_t b0 = prmt_raw(u[h], 0x4B000000u, 0x7404u | (j << 4));
+      const uint32_t b1 = prmt_raw(u[h], 0x4B000000u, 0x7404u | ((j + 1) << 4));
+      ffma2_rn(v[4 * h + j], v[4 * h + j + 1], __uint_as_float(b0), __uint_as_float(b1), k.s8, k.s8, k.c, k.c);
+    }
+}
+
 // 4 codes of a word -> v[0..3]
 JF_DEV void deq4(uint32_t word, DeqScale k, float *v) {
   const uint32_t u = word ^ 0x80808080u;
@@ -381,6 +417,13 @@ JF_DEV void fadd2_rn(float &d0, float &d1, float a0, float a1, float b0, float b
   asm("{\n\t.reg .b64 a, b, d;\n\t"
       "mov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
       "add.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;\n\t}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+JF_DEV void fsub2_rn(float &d0, float &d1, float a0, float a1, float b0, float b1) {
+  asm("{\n\t.reg .b64 a, b, d;\n\t"
+      "mov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
+      "sub.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;\n\t}"
       : "=f"(d0), "=f"(d1)
       : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
 }

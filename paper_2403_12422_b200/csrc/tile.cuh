@@ -47,69 +47,32 @@ JF_DEV void load_deq(const TilePos &t, const int8_t *__restrict__ q, const float
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const uint2 w = __ldg(reinterpret_cast<const uint2 *>(q + t.row(i) * t.c + t.col()));
-    deq4(w.x, k, v[i]);
-    deq4(w.y, k, v[i] + 4);
+    deq8_packed(w.x, w.y, k, v[i]);
   }
 }
 
-// Requantize the FP32 tile per 32x32 block and store codes + scales
-// (quantize_per_block semantics, qtensor.py:219-246).  `red` is >= 64 words
-// of shared memory.  Ends with the CTA synchronized (red reusable).
-JF_DEV void quant_store(const TilePos &t, const float (&v)[4][8], int8_t *__restrict__ q,
-                        float *__restrict__ s, uint32_t *red, int32_t *err) {
-  uint32_t m = 0;
-  if (t.active) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 8; ++j) m = max(m, abs_bits(v[i][j]));
-  }
-  m = max(m, __shfl_xor_sync(0xffffffffu, m, 1));
-  m = max(m, __shfl_xor_sync(0xffffffffu, m, 2));
-  const int qb = t.lane >> 2;
-  if ((t.lane & 3) == 0) red[t.warp * 8 + qb] = m;
-  __syncthreads();
-  uint32_t am = 0;
-#pragma unroll
-  for (int w = 0; w < 8; ++w) am = max(am, red[w * 8 + qb]);
-  int flags = 0;
-  const float sc = block_scale(am, flags);
-  const float rc = __frcp_rn(sc);
-  if (t.active) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      uint2 w;
-      bool tie = false;
-      w.x = pack4(quant_code_try(v[i][0], rc, tie), quant_code_try(v[i][1], rc, tie),
-                  quant_code_try(v[i][2], rc, tie), quant_code_try(v[i][3], rc, tie));
-      w.y = pack4(quant_code_try(v[i][4], rc, tie), quant_code_try(v[i][5], rc, tie),
-                  quant_code_try(v[i][6], rc, tie), quant_code_try(v[i][7], rc, tie));
-      if (tie) {  // rare: a code near a rounding tie takes the exact division
-        w.x = pack4(quant_code_fast(v[i][0], sc, rc), quant_code_fast(v[i][1], sc, rc),
-                    quant_code_fast(v[i][2], sc, rc), quant_code_fast(v[i][3], sc, rc));
-        w.y = pack4(quant_code_fast(v[i][4], sc, rc), quant_code_fast(v[i][5], sc, rc),
-                    quant_code_fast(v[i][6], sc, rc), quant_code_fast(v[i][7], sc, rc));
-      }
-      *reinterpret_cast<uint2 *>(q + t.row(i) * t.c + t.col()) = w;
-    }
-    if (t.warp == 0 && (t.lane & 3) == 0) {
-      s[t.scale_idx(t.r0, t.col())] = sc;
-      raise_flags(err, flags);
-    }
-  }
-  __syncthreads();
-}
-
-// quant_store into a column slice of a wider BlockQuantTensor: codes row stride
-// ldq, scale grid row stride lds (q and s already offset to the slice).
+// Requantize the FP32 tile per 32x32 block and store codes + scales into a column
+// slice of a BlockQuantTensor (quantize_per_block semantics, qtensor.py:219-246):
+// codes row stride ldq, scale grid row stride lds (q and s already offset to the
+// slice).  `red` is >= 64 words of shared memory.  Ends with the CTA synchronized.
+//
+// Common path, per element ~3 issue slots: y = fl(x * fl(1/s)) and its magic-number
+// rounding t = fl(y + 1.5*2^23) in packed f32x2 ops (the product is an FFMA2 with an
+// opaque +0 addend so ptxas cannot contract it into the add), the row's largest
+// distance |y - rint(y)| by 3-input max, and the code bytes taken straight from the
+// low bytes of t (t = 1.5*2^23 + q exactly, |y| < 2^22).  Exact exactly when the
+// scale is a normal binary16 value (then |x/s| <= 127 * (1 + 2^-11) < 127.5: the
+// reference's clip is a no-op) and no y lies within 3e-5 of a half-integer
+// (quant_code_try's argument).  Otherwise the row takes the exact per-element path.
 JF_DEV void quant_store_ld(const TilePos &t, const float (&v)[4][8], int8_t *__restrict__ q, int64_t ldq,
                            float *__restrict__ s, int64_t lds, uint32_t *red, int32_t *err) {
   uint32_t m = 0;
   if (t.active) {
+    float mf = absmax3_nan(v[0][0], v[0][1], v[0][2]);
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 8; ++j) m = max(m, abs_bits(v[i][j]));
+    for (int e = 3; e < 31; e += 2) mf = absmax3_nan(mf, v[e >> 3][e & 7], v[(e + 1) >> 3][(e + 1) & 7]);
+    mf = absmax3_nan(mf, v[3][7], 0.0f);
+    m = __float_as_uint(mf);  // NaN -> >= 0x7f800000 like the integer max of |bits|
   }
   m = max(m, __shfl_xor_sync(0xffffffffu, m, 1));
   m = max(m, __shfl_xor_sync(0xffffffffu, m, 2));
@@ -122,16 +85,28 @@ JF_DEV void quant_store_ld(const TilePos &t, const float (&v)[4][8], int8_t *__r
   int flags = 0;
   const float sc = block_scale(am, flags);
   const float rc = __frcp_rn(sc);
+  const bool fast_ok = flags == 0 && sc >= 6.103515625e-05f;  // normal binary16 scale
   if (t.active) {
+    const float zero = opaque_zero();
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       uint2 w;
-      bool tie = false;
-      w.x = pack4(quant_code_try(v[i][0], rc, tie), quant_code_try(v[i][1], rc, tie),
-                  quant_code_try(v[i][2], rc, tie), quant_code_try(v[i][3], rc, tie));
-      w.y = pack4(quant_code_try(v[i][4], rc, tie), quant_code_try(v[i][5], rc, tie),
-                  quant_code_try(v[i][6], rc, tie), quant_code_try(v[i][7], rc, tie));
-      if (tie) {  // rare: a code near a rounding tie takes the exact division
+      float tt[8], emax = 0.0f;
+#pragma unroll
+      for (int j = 0; j < 8; j += 2) {
+        float y0, y1, u0, u1, e0, e1;
+        ffma2_rn(y0, y1, v[i][j], v[i][j + 1], rc, rc, zero, zero);
+        fadd2_rn(tt[j], tt[j + 1], y0, y1, 12582912.0f, 12582912.0f);
+        fsub2_rn(u0, u1, tt[j], tt[j + 1], 12582912.0f, 12582912.0f);
+        fsub2_rn(e0, e1, y0, y1, u0, u1);
+        emax = absmax3_nan(emax, e0, e1);
+      }
+      if (fast_ok && emax < 0.49997f) {
+        w.x = prmt(prmt(__float_as_uint(tt[0]), __float_as_uint(tt[1]), 0x0040u),
+                   prmt(__float_as_uint(tt[2]), __float_as_uint(tt[3]), 0x0040u), 0x5410u);
+        w.y = prmt(prmt(__float_as_uint(tt[4]), __float_as_uint(tt[5]), 0x0040u),
+                   prmt(__float_as_uint(tt[6]), __float_as_uint(tt[7]), 0x0040u), 0x5410u);
+      } else {  // rare: near-tie, subnormal scale or flagged block -> exact per element
         w.x = pack4(quant_code_fast(v[i][0], sc, rc), quant_code_fast(v[i][1], sc, rc),
                     quant_code_fast(v[i][2], sc, rc), quant_code_fast(v[i][3], sc, rc));
         w.y = pack4(quant_code_fast(v[i][4], sc, rc), quant_code_fast(v[i][5], sc, rc),
@@ -145,6 +120,12 @@ JF_DEV void quant_store_ld(const TilePos &t, const float (&v)[4][8], int8_t *__r
     }
   }
   __syncthreads();
+}
+
+// quant_store into a whole [n x c] BlockQuantTensor.
+JF_DEV void quant_store(const TilePos &t, const float (&v)[4][8], int8_t *__restrict__ q,
+                        float *__restrict__ s, uint32_t *red, int32_t *err) {
+  quant_store_ld(t, v, q, t.c, s, t.c >> 5, red, err);
 }
 
 inline dim3 tile_grid(int64_t n, int64_t c) {
