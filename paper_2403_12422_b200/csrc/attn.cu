@@ -102,6 +102,10 @@ JF_DEV bool elect_one() {
   return p != 0;
 }
 
+// Control-role wait with a suspend hint (the MMA warp shares its sub-partition with
+// softmax warps; spinning would take their issue slots).
+JF_DEV void ctl_wait(uint32_t addr, uint32_t parity) { mbar_wait_u32_sleep(addr, parity, 200); }
+
 JF_DEV float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -324,53 +328,48 @@ __global__ void __launch_bounds__(kFwdThreads, 1) attn_fwd_kernel(const FwdParam
     constexpr uint32_t idS = idesc_16(BQ, BKV, 0, 0, 1);  // bf16 Q, K
     constexpr uint32_t idO = idesc_16(BQ, D, 0, 1, 1);    // bf16 P (TMEM), V (MN-major)
     const uint32_t a_kv_full = smem_u32(&B.kv_full[0]), a_p_full = smem_u32(&B.p_full[0]);
-    mbar_wait(&B.q_full, 0);
-    int sx[2] = {0, 0}, px[2] = {0, 0};
-    const int nx[2] = {nA, nB};
-#pragma unroll 1
-    while (px[0] < nA || px[1] < nB) {
-      int go = -1;  // 0/1: PV of X; 2/3: S of X-2
-      if (lane == 0) {
-        while (go < 0) {
-#pragma unroll
-          for (int X = 0; X < 2; ++X)
-            if (go < 0 && px[X] < sx[X] && mbar_test_u32(a_p_full + 8 * X, px[X] & 1)) go = X;
-#pragma unroll
-          for (int X = 0; X < 2; ++X)
-            if (go < 0 && sx[X] < nx[X] && sx[X] <= px[X] &&
-                mbar_test_u32(a_kv_full + 8 * (sx[X] & 1), (sx[X] >> 1) & 1))
-              go = 2 + X;
-        }
-      }
-      go = __shfl_sync(0xffffffffu, go, 0);
+    // Static schedule: S_A(0) S_B(0), then per kv tile j: PV_A(j) S_A(j+1) PV_B(j) S_B(j+1).
+    // Blocking (suspending) waits: this warp shares a sub-partition with two softmax warps.
+    auto issue_s = [&](int X, int j) {
+      const int st = j & 1;
+      ctl_wait(a_kv_full + 8 * st, (j >> 1) & 1);
       tc_fence_after();
-      if (go >= 2) {
-        const int X = go - 2, j = sx[X], st = j & 1;
-        if (lane == 0 && X == 0) ATR(5, j);
-        if (elect_one()) {
-          const uint32_t tk = sK0 + 2 * st * SM::kTile, q = sQ + X * SM::kQ;
+      if (lane == 0 && X == 0) ATR(5, j);
+      if (elect_one()) {
+        const uint32_t tk = sK0 + 2 * st * SM::kTile, q = sQ + X * SM::kQ;
 #pragma unroll
-          for (int k = 0; k < D / 16; ++k)
-            mma_bf16_ss(tmem + X * BKV, kdesc(q, k), kdesc(tk, k), idS, k > 0 ? 1u : 0u);
-          mma_commit(&B.s_full[X]);
-        }
-        ++sx[X];
-      } else {
-        const int X = go, j = px[X], st = j & 1;
-        if (lane == 0 && X == 0) ATR(6, j);
-        const uint32_t tv = sK0 + (2 * st + 1) * SM::kTile;
-        px[X] = j + 1;
-        const bool release = X == 0 ? px[1] > j : (j >= nA || px[0] > j);
-        if (elect_one()) {
-#pragma unroll
-          for (int k = 0; k < BKV / 16; ++k)
-            mma_bf16_ts(tmem + 2 * BKV + X * D, tmem + X * BKV + 8 * k, mndesc(tv, k, p.mn_lbo, p.mn_sbo), idO,
-                        (j > 0 || k > 0) ? 1u : 0u);
-          mma_commit(&B.o_done[X]);
-          if (release) mma_commit(&B.kv_free[st]);
-        }
+        for (int k = 0; k < D / 16; ++k) mma_bf16_ss(tmem + X * BKV, kdesc(q, k), kdesc(tk, k), idS, k > 0 ? 1u : 0u);
+        mma_commit(&B.s_full[X]);
       }
       __syncwarp();
+    };
+    auto issue_pv = [&](int X, int j, bool release) {
+      const int st = j & 1;
+      ctl_wait(a_p_full + 8 * X, j & 1);
+      tc_fence_after();
+      if (lane == 0 && X == 0) ATR(6, j);
+      if (elect_one()) {
+        const uint32_t tv = sK0 + (2 * st + 1) * SM::kTile;
+#pragma unroll
+        for (int k = 0; k < BKV / 16; ++k)
+          mma_bf16_ts(tmem + 2 * BKV + X * D, tmem + X * BKV + 8 * k, mndesc(tv, k, p.mn_lbo, p.mn_sbo), idO,
+                      (j > 0 || k > 0) ? 1u : 0u);
+        mma_commit(&B.o_done[X]);
+        if (release) mma_commit(&B.kv_free[st]);
+      }
+      __syncwarp();
+    };
+    mbar_wait(&B.q_full, 0);
+    issue_s(0, 0);
+    issue_s(1, 0);
+#pragma unroll 1
+    for (int j = 0; j < nB; ++j) {
+      if (j < nA) {
+        issue_pv(0, j, false);
+        if (j + 1 < nA) issue_s(0, j + 1);
+      }
+      issue_pv(1, j, true);  // B uses every kv tile and finishes each after A
+      if (j + 1 < nB) issue_s(1, j + 1);
     }
   } else if (warp < 8) {
     // ───────────── softmax + epilogue (thread = query row of tile X) ─────────────
@@ -392,6 +391,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) attn_fwd_kernel(const FwdParam
       for (int q = 0; q < BKV / 32; ++q)
         tmem_ld_32x32b_x32(tS + 32 * q, *reinterpret_cast<uint32_t(*)[32]>(sr + 32 * q));
       wait_ld_dep(sr);
+      if (r == 0 && X == 0) ATR(15, j);
       float *sf = reinterpret_cast<float *>(sr);
       if (j == qt) {  // diagonal tile: key k > query r is masked
 #pragma unroll
@@ -402,6 +402,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) attn_fwd_kernel(const FwdParam
 #pragma unroll
       for (int k = 3; k < BKV - 1; k += 2) mx = fmax3(mx, sf[k], sf[k + 1]);
       mx = fmaxf(mx, sf[BKV - 1]);
+      if (r == 0 && X == 0) ATR(7, j);
       const float mnew = mx * c;
       bool resc = false;
       float alpha = 1.0f;

@@ -46,6 +46,38 @@ __global__ void __launch_bounds__(1024, 1) fp_kernel(float *out, long long *cyc,
         xi[i] = __float_as_int(x[i]) ^ it;
       }
     }
+    if (OP == 5) {  // MUFU.EX2: 8 independent chains
+#pragma unroll
+      for (int i = 0; i < 8; ++i) asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(x[i]));
+    }
+    if (OP == 6) {  // F2FP.BF16.F32.PACK_AB (cvt.rn.bf16x2.f32): 8 per iteration, results fed back
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        uint32_t d;
+        asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(x[i]), "f"(x[(i + 1) & 7]));
+        x[i] = __uint_as_float(d);
+      }
+    }
+    if (OP == 7) {  // ex2.approx.f16x2 (2 results per instruction)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        uint32_t v = __float_as_uint(x[i]);
+        asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(v));
+        x[i] = __uint_as_float(v);
+      }
+    }
+    if (OP == 8) {  // cvt.rn.f16x2.f32
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        uint32_t d;
+        asm volatile("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(x[i]), "f"(x[(i + 1) & 7]));
+        x[i] = __uint_as_float(d);
+      }
+    }
+    if (OP == 9) {  // IADD + LOP (ALU pipe)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) xi[i] = (xi[i] + 0x7fff) ^ it;
+    }
     if (OP == 4) {  // packed f32x2 FMA: 4 instructions = 8 FMAs
 #pragma unroll
       for (int i = 0; i < 8; i += 2) {
@@ -595,6 +627,11 @@ int main() {
   run_fp<2>("fadd", d_out, d_cyc, 8);
   run_fp<3>("i2fp_chain", d_out, d_cyc, 8);
   run_fp<4>("ffma2_x2_fmas", d_out, d_cyc, 8);
+  run_fp<5>("mufu_ex2", d_out, d_cyc, 8);
+  run_fp<6>("cvt_bf16x2_f32 (instr)", d_out, d_cyc, 8);
+  run_fp<7>("ex2_f16x2 (instr)", d_out, d_cyc, 8);
+  run_fp<8>("cvt_f16x2_f32 (instr)", d_out, d_cyc, 8);
+  run_fp<9>("iadd_lop (2 ops)", d_out, d_cyc, 16);
   run_tmem<0>("tmem_ld_x32", d_out, d_cyc);
   run_tmem<1>("tmem_st_x8x4", d_out, d_cyc);
   run_tmem<2>("promote_exact_i2f", d_out, d_cyc);

@@ -41,8 +41,8 @@ if a.trace:
     L.jf_attn_set_trace(tr.data_ptr()); run(); run(); torch.cuda.synchronize(); L.jf_attn_set_trace(None)
     t = tr.view(16, 64).cpu()
     t0 = t[t > 0].min().item()
-    names = {0: "P:wait_cp", 1: "P:cp_done", 2: "P:kvfree", 3: "P:conv_done", 5: "M:kv_full", 6: "M:p_full",
-             8: "S:wait_s", 9: "S:s_full", 10: "S:exp_done", 11: "S:o_done", 12: "S:p_stored"}
+    names = {2: "P:kvfree", 3: "P:conv_done", 5: "M:S_issue", 6: "M:PV_issue",
+             8: "S:wait_s", 9: "S:s_full", 15: "S:s_loaded", 7: "S:max_done", 10: "S:exp_done", 11: "S:o_done", 12: "S:p_stored"}
     n = (s // 128) if True else 0
     print("tile " + " ".join(f"{v:>11s}" for v in names.values()))
     for j in range(n):
