@@ -2,7 +2,8 @@
 one launch of each hand-written pipeline -- the tcgen05 GEMM kernels (TMA-staged
 scales, MN-major operands, generic-shape kernel with partial tiles, int32
 partials, f16-widened operands), Add+stats, LayerNorm fwd/bwd, GELU fwd/bwd,
-the quantizer and the column sum.  Usage:
+the quantizer, the column sum, the fused INT8-boundary attention (forward and
+both backward kernels, head_dim 64 and 128) and the device Philox dropout mask.  Usage:
   compute-sanitizer --tool racecheck python tools/sanitize_driver.py
 """
 import os
@@ -42,6 +43,16 @@ def main():
     g = jf.gelu_forward(x)
     jf.gelu_backward(x, g)
     jf.column_sum(dy)
+    runtime.set_attention("fused")
+    for h, d in ((2, 64), (1, 128)):
+        core = jf.AttentionCore(h, d, dtype=torch.bfloat16)
+        qkv = q((256, 3 * h * d), seed=8)
+        assert core.fused(256)
+        core.forward_q(qkv, 1, 256)
+        core.backward_q(q((256, h * d), 0.1, seed=9), 1, 256)
+    runtime.set_attention("sdpa")
+    st_ = jf.DropoutState.generate(0.2, (5, 1), (256, 384))
+    jf.dropout_forward(x, st_)
     torch.cuda.synchronize()
     jf.check_errors()
     print("sanitize driver ok")
