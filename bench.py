@@ -75,6 +75,9 @@ def parse(argv=None):
     ap.add_argument("--nccl-algo", default="auto", choices=["auto", "ring", "tree", "nvls"],
                     help="N>1: NCCL_ALGO for the gradient all-reduce (NVLS = in-switch reduction on "
                          "NVSwitch); reported in the allreduce object")
+    ap.add_argument("--variants", type=int, default=1, choices=[0, 1],
+                    help="block workloads, 1 GPU: also time the opt-in variants (fast promotion, f16 operands, "
+                         "fused attention) and report them in a 'variants' object")
     ap.add_argument("--no-bf16", action="store_true", help="skip the cuBLAS BF16 block baseline")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle baseline")
     ap.add_argument("--cpu-tokens", type=int, default=128, help="token sample for the CPU baseline")
@@ -343,9 +346,13 @@ class BlockWorkload:
 
     def config(self):
         w = self.w
+        c, hid, n = self.c, w["hidden"], self.n
+        wq = 4 * c * c + 2 * c * hid                 # INT8 weight codes (qkv, proj, mlp1, mlp2)
+        act = n * (8 * c + 2 * hid)                  # INT8 activations saved in forward (approx.)
         return {"hidden": self.c, "heads": w["heads"], "mlp_hidden": w["hidden"], "seq_len": self.s,
                 "batch_per_gpu": self.b, "tokens_per_gpu": self.n,
-                "l2": "working set (201 MB INT8 weights + activations) larger than the 126 MB L2"}
+                "l2": (f"working set per step: {wq / 1e6:.0f} MB INT8 weights + {4 * wq / 1e6:.0f} MB FP32 weight "
+                       f"gradients written + ~{act / 1e6:.0f} MB INT8 activations, larger than the 126 MB L2")}
 
 
 class LinearWorkload:
@@ -575,7 +582,69 @@ def run_ours(args, world, rank, local):
                                operands=args.operands)
     if world > 1:
         out["allreduce"] = measure_allreduce(wl, world)
+    if args.variants and world == 1 and isinstance(wl, BlockWorkload):
+        out["variants"] = measure_variants(jf, wl, args)
     return out, wl, None, w
+
+
+# Opt-in configurations of the same block step, timed in the same process right after
+# the headline (same inputs, CUDA events on the stream, `steps` steps after 2 warm-ups).
+VARIANTS = [
+    ("fast_promotion", {"promotion": "fast"},
+     "acc = fma(P, sa*sb, acc) instead of the reference's fl(acc + fl(fl(P*sa)*sb)); "
+     "contract: FP32 rel <= 1e-3 of absmax, codes +-1 on <= 1e-5 (tests/test_gpu_kernels.py)"),
+    ("f16_operands", {"operands": "auto"},
+     "big GEMMs on kind::f16 over f16-widened codes (bit-identical; 16-bit operand copies in HBM)"),
+    ("fast_promotion_f16_operands", {"promotion": "fast", "operands": "auto"}, "both of the above"),
+    ("fused_attention", {"attention": "fused"},
+     "attention island as the hand-written tcgen05 kernels with the INT8 boundary fused in "
+     "(csrc/attn.cu) instead of cuDNN SDPA between boundary kernels"),
+]
+
+
+def measure_variants(jf, wl, args):
+    from paper_2403_12422_b200.qgemm import GemmTimer
+
+    rt = jf.runtime
+    base = {"promotion": rt.get_promotion(), "operands": rt.gemm_operands(), "attention": rt.attention()}
+    setters = {"promotion": jf.set_promotion, "operands": rt.set_gemm_operands, "attention": rt.set_attention}
+    res = {}
+    stream = torch.cuda.current_stream()
+    try:
+        for name, knobs, what in VARIANTS:
+            for k, v in knobs.items():
+                setters[k](v)
+            for _ in range(2):
+                wl.step()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(args.steps):
+                wl.step()
+            b.record(stream)
+            torch.cuda.synchronize()
+            jf.check_errors()
+            ms = a.elapsed_time(b) / args.steps
+            entry = {"value": round(wl.n / (ms / 1e3), 1), "unit": "tokens/s", "ms_per_step": round(ms, 4),
+                     "what": what}
+            if "promotion" in knobs or "operands" in knobs:
+                rt.set_overlap_wgrad(False)
+                with GemmTimer() as gt:
+                    for _ in range(args.steps):
+                        wl.step()
+                torch.cuda.synchronize()
+                rt.set_overlap_wgrad(bool(args.overlap_wgrad))
+                g = gt.summary()
+                tops = g["ops"] / (g["ms"] / 1e3) / 1e12
+                entry["gemm_tops"] = round(tops, 1)
+                entry["gemm_frac_of_int8_peak"] = round(tops / INT8_PEAK_TOPS, 4)
+            res[name] = entry
+            for k, v in base.items():
+                setters[k](v)
+    finally:
+        for k, v in base.items():
+            setters[k](v)
+    return res
 
 
 def roofline(gemm_tops: float, promotion: str, clocks_mhz=None, operands: str = "int8") -> dict:

@@ -67,6 +67,30 @@ int jf_dequantize_f32(const int8_t *q, const float *s, int64_t n, int64_t c, flo
 int jf_dequantize_bf16(const int8_t *q, const float *s, int64_t n, int64_t c, uint16_t *y,
                        jf_stream_t stream);
 
+/* Fused INT8-boundary attention (AttentionCore, qlayers.py:187-236, with the block's
+ * dequantize/quantize crossings qlayers.py:350-351 and :406-408 done inside the kernels).
+ * Causal, softmax scale 1/sqrt(head_dim); tcgen05 MMAs on bf16 operands (codes
+ * dequantized exactly, then rounded to bf16), FP32 accumulation; tolerance class.
+ * jf_attn_supported: 1 when seq % 256 == 0 and head_dim is 64 or 128.
+ * jf_attn_fwd_q: QKV codes/scales [n x 3c] (n = batch*seq, c = heads*head_dim) ->
+ *   O codes/scales [n x c]; also o_bf (bf16 O [n x c], for the backward's D_i) and
+ *   lse [batch, heads, seq] (log2 domain).
+ * jf_attn_bwd_q: + dO codes/scales [n x c] -> dQ|dK|dV codes/scales [n x 3c];
+ *   dsum [batch, heads, seq] is scratch (D_i = rowsum(dO * O)).  Two kernels, no
+ *   atomics: deterministic. */
+int jf_attn_supported(int64_t seq, int64_t head_dim);
+int jf_attn_fwd_q(const int8_t *qkv, const float *qkv_s, int64_t batch, int64_t seq, int64_t heads,
+                  int64_t head_dim, int8_t *o, float *o_s, uint16_t *o_bf, float *lse, int32_t *err,
+                  jf_stream_t stream);
+int jf_attn_bwd_q(const int8_t *qkv, const float *qkv_s, const int8_t *dout, const float *dout_s,
+                  const uint16_t *o_bf, const float *lse, float *dsum, int64_t batch, int64_t seq,
+                  int64_t heads, int64_t head_dim, int8_t *dqkv, float *dqkv_s, int32_t *err,
+                  jf_stream_t stream);
+/* diagnostics: MN-major UMMA descriptor strides (lbo, sbo) and a device buffer for CTA-0
+ * event clocks (long long[16*64]) of the attention kernels (null = off). */
+int jf_attn_set_mn_desc(uint32_t lbo, uint32_t sbo);
+int jf_attn_set_trace(long long *buf);
+
 /* The attention boundary (qlayers.py:350-351 forward, :406-408 backward).
  * jf_dequantize_qkv_heads: QKV codes [n x 3c] (n = batch*seq, c = heads*head_dim) -> q, k, v
  *   bf16, each contiguous [batch, heads, seq, head_dim] (head_dim % 16 == 0).
