@@ -648,8 +648,8 @@ def measure_variants(jf, wl, args):
 
 
 def roofline(gemm_tops: float, promotion: str, clocks_mhz=None, operands: str = "int8") -> dict:
-    """Dominant kernel = the block GEMM (gemm_i8s_kernel on the default int8 operand path,
-    gemm_f16s_kernel with the opt-in --operands auto/f16; ~87% of the step).
+    """Dominant kernel = the block GEMM (gemm_tc_kernel<kind::i8> on the default int8 operand path,
+    gemm_tc_kernel<kind::f16> with the opt-in --operands auto/f16; ~92% of the step).
 
     peak: B200 dense INT8 (datasheet 4.5 POPS; our raw kind::i8 microbenchmark
     measures 8178 MAC/clk/SM = 4.76 POPS at 1965 MHz).  The binding bound under
@@ -673,8 +673,8 @@ def roofline(gemm_tops: float, promotion: str, clocks_mhz=None, operands: str = 
         traffic, tr_src = t["dram_bytes_per_launch"], t["launch"] + " (" + t["source"] + ")"
     except (OSError, KeyError, ValueError):
         pass
-    kname = ("gemm_f16s_kernel (tcgen05 kind::f16 on f16-widened int8 codes)" if operands != "int8"
-             else "gemm_i8s_kernel (tcgen05 kind::i8)")
+    kname = ("gemm_tc_kernel<OP_F16> (tcgen05 kind::f16 on f16-widened int8 codes)" if operands != "int8"
+             else "gemm_tc_kernel<OP_I8> (tcgen05 kind::i8)")
     return {"kernel": kname, "bound": "tensor", "achieved": round(gemm_tops, 1),
             "peak": INT8_PEAK_TOPS, "unit": "TFLOP/s", "frac": round(gemm_tops / INT8_PEAK_TOPS, 4),
             "traffic": traffic, "traffic_launch": tr_src,

@@ -280,7 +280,7 @@ def _gemm_f16(kind, a16, sa, sa_st, b16, sb, sb_st, bias, m, n, k, promotion, ou
 
 def mn_major_ok(*dims: int) -> bool:
     """True when the GEMM reads MN-major operands as stored (every dim a multiple of 128):
-    dgrad then needs no W^T and wgrad no transposed dY / X (libjetfire gemm_i8s_kernel)."""
+    dgrad then needs no W^T and wgrad no transposed dY / X (libjetfire gemm_tc_kernel)."""
     return _rt.gemm_option("tma_scales") != 0 and all(d % 128 == 0 for d in dims)
 
 
