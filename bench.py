@@ -896,10 +896,74 @@ def cpu_linear_sample(w, tokens, reps=1):
             "seconds": round(t, 3), "host": host_info()}
 
 
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def _reference_package():
+    """The UNMODIFIED reference package installed by tools/install_reference.sh (git-ignored,
+    travels to the GPU box), or None.  Never /root/reference: that tree is not on the box."""
+    if not os.path.isdir(os.path.join(REF_DIR, "int8flow")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        import int8flow
+    except Exception:  # noqa: BLE001 -- fall back to the oracle port
+        return None
+    return int8flow if os.path.dirname(os.path.dirname(int8flow.__file__)) == REF_DIR else None
+
+
+def ref_block_sample(ref, w, tokens, reps=1):
+    """The reference's own TransformerBlock fwd+bwd (qlayers.py:329-427), its public API."""
+    rng = np.random.default_rng(0)
+    c, h, heads = w["c"], w["hidden"], w["heads"]
+    seq = min(tokens, w["seq"])
+    batch = max(1, tokens // seq)
+    blk = ref.TransformerBlock.initialize(rng, ref.BlockConfig(c_model=c, heads=heads, hidden=h))
+    xq = ref.quantize_per_block(rng.standard_normal((batch * seq, c)).astype(np.float32), 32)
+    dq = ref.quantize_per_block((0.1 * rng.standard_normal((batch * seq, c))).astype(np.float32), 32)
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        blk.forward(xq, batch, seq)
+        blk.backward(dq)
+        times.append(time.perf_counter() - t0)
+    t = min(times)
+    return {"value": round(batch * seq / t, 2), "unit": "tokens/s", "cores": os.cpu_count(), "kind": "reference",
+            "sample": f"unmodified reference int8flow {getattr(ref, '__version__', '')} from baseline/_ref: "
+                      f"TransformerBlock fwd+bwd, {batch}x{seq} tokens at hidden {c}/mlp {h}, threads=1 "
+                      f"(fastest), OpenBLAS threads = all host cores, best of {reps}",
+            "seconds": round(t, 3), "host": host_info()}
+
+
+def ref_linear_sample(ref, w, tokens, reps=1):
+    """The reference's own QuantLinear fwd+bwd (qlayers.py:149-181)."""
+    rng = np.random.default_rng(0)
+    c, d = w["c"], w["d"]
+    lin = ref.QuantLinear.initialize(rng, d, c)
+    xq = ref.quantize_per_block(rng.standard_normal((tokens, c)).astype(np.float32), 32)
+    dq = ref.quantize_per_block((0.1 * rng.standard_normal((tokens, d))).astype(np.float32), 32)
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        lin.forward(xq)
+        lin.backward(dq)
+        times.append(time.perf_counter() - t0)
+    t = min(times)
+    return {"value": round(tokens / t, 2), "unit": "tokens/s", "cores": os.cpu_count(), "kind": "reference",
+            "sample": f"unmodified reference int8flow from baseline/_ref: QuantLinear {c}->{d} fwd+bwd, "
+                      f"{tokens} tokens, OpenBLAS threads = all host cores, best of {reps}",
+            "seconds": round(t, 3), "host": host_info()}
+
+
 def cpu_sample(w, tokens):
+    """The reference's own implementation when baseline/_ref holds it (kind 'reference'),
+    else the oracle port (kind 'port', bit-identical on the golden fixtures)."""
+    ref = _reference_package()
     if "linear" in w:  # the CPU finishes this case quickly: a 1024-token sample (of 4096)
-        return cpu_linear_sample(w, max(tokens, 1024))
-    return cpu_block_sample(w, tokens)
+        tokens = max(tokens, 1024)
+        return ref_linear_sample(ref, w, tokens) if ref else cpu_linear_sample(w, tokens)
+    return ref_block_sample(ref, w, tokens) if ref else cpu_block_sample(w, tokens)
 
 
 def run_reference(args, world, rank):
