@@ -17,8 +17,8 @@ def test_roofline_fields():
     assert abs(r["frac"] - 480.0 / bench.INT8_PEAK_TOPS) < 1e-4
     pb = r["promotion_bound"]
     assert abs(pb["value"] - 128.0 / 3 * 64 * 148 * 1965e6 / 1e12) < 0.1
-    assert "gemm_i8s_kernel" in r["kernel"]
-    assert "gemm_f16s_kernel" in bench.roofline(480.0, "exact", operands="auto")["kernel"]
+    assert "gemm_tc_kernel<OP_I8>" in r["kernel"] and "measured_peak" in r
+    assert "gemm_tc_kernel<OP_F16>" in bench.roofline(480.0, "exact", operands="auto")["kernel"]
 
 
 def test_grad_shapes_block_and_linear():
