@@ -35,14 +35,14 @@ __global__ void __launch_bounds__(kTileThreads) add_stats_kernel(
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) v[i][j] = __fadd_rn(v[i][j], w2[i][j]);
+        for (int j = 0; j < 8; j += 2) fadd2_rn(v[i][j], v[i][j + 1], v[i][j], v[i][j + 1], w2[i][j], w2[i][j + 1]);
     }
   } else if (t.active) {
     // Add(x, zeros_like(x)): x + 0.0 (turns -0.0 into +0.0 exactly like numpy)
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 8; ++j) v[i][j] = __fadd_rn(v[i][j], 0.0f);
+      for (int j = 0; j < 8; j += 2) fadd2_rn(v[i][j], v[i][j + 1], v[i][j], v[i][j + 1], 0.0f, 0.0f);
   }
   if (t.active) {
 #pragma unroll
@@ -124,13 +124,17 @@ __global__ void __launch_bounds__(kTileThreads) ln_fwd_kernel(
       g[j] = __ldg(gamma + t.col() + j);
       bb[j] = __ldg(beta + t.col() + j);
     }
+    const float zero = opaque_zero();
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const float m = __ldg(mu + t.row(i)), is = __ldg(inv_std + t.row(i));
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const float xh = __fmul_rn(__fsub_rn(v[i][j], m), is);
-        v[i][j] = __fadd_rn(__fmul_rn(g[j], xh), bb[j]);
+      for (int j = 0; j < 8; j += 2) {  // packed, same roundings: fl(fl(g*fl(fl(x-m)*is)) + b)
+        float x0, x1;
+        fsub2_rn(x0, x1, v[i][j], v[i][j + 1], m, m);
+        fmul2_rn(x0, x1, x0, x1, is, is);
+        ffma2_rn(x0, x1, g[j], g[j + 1], x0, x1, zero, zero);  // rounded product: no contraction
+        fadd2_rn(v[i][j], v[i][j + 1], x0, x1, bb[j], bb[j + 1]);
       }
     }
   }
@@ -275,6 +279,7 @@ __global__ void __launch_bounds__(256) ln_bwd_rows_leaf_kernel(LnRowArgs A, int 
   for (int j = 0; j < 8; ++j) c1[j] = c2[j] = 0.f;
   if (valid) {
     const float mr = __ldg(A.mu + row), ir = __ldg(A.inv_std + row);
+    const float zero = opaque_zero();
     const int64_t cb = A.c >> 5;
     const int64_t col0 = (int64_t)leaf * leaf_len;
     const uint8_t *sx_ = wx + lr * row_bytes + leaf * stride;
@@ -299,19 +304,27 @@ __global__ void __launch_bounds__(256) ln_bwd_rows_leaf_kernel(LnRowArgs A, int 
       const uint32_t xw[4] = {xq.x ^ 0x80808080u, xq.y ^ 0x80808080u, xq.z ^ 0x80808080u, xq.w ^ 0x80808080u};
       const uint32_t dw[4] = {dq.x ^ 0x80808080u, dq.y ^ 0x80808080u, dq.z ^ 0x80808080u, dq.w ^ 0x80808080u};
 #pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        const float xv = deq_code(xw[e >> 2], e & 3, kx);
-        const float dv = deq_code(dw[e >> 2], e & 3, kd);
-        const float xh = __fmul_rn(__fsub_rn(xv, mr), ir);
-        const float dxh = __fmul_rn(dv, g[e]);
-        const float pr = __fmul_rn(dxh, xh);
+      for (int e = 0; e < 16; e += 2) {  // packed f32x2 pairs (chains j, j+1); same roundings
+        float xv0, xv1, dv0, dv1, xh0, xh1, dh0, dh1, pr0, pr1;
+        ffma2_rn(xv0, xv1, __uint_as_float(prmt_raw(xw[e >> 2], 0x4B000000u, 0x7404u | ((e & 3) << 4))),
+                 __uint_as_float(prmt_raw(xw[e >> 2], 0x4B000000u, 0x7404u | (((e + 1) & 3) << 4))), kx.s8, kx.s8,
+                 kx.c, kx.c);
+        ffma2_rn(dv0, dv1, __uint_as_float(prmt_raw(dw[e >> 2], 0x4B000000u, 0x7404u | ((e & 3) << 4))),
+                 __uint_as_float(prmt_raw(dw[e >> 2], 0x4B000000u, 0x7404u | (((e + 1) & 3) << 4))), kd.s8, kd.s8,
+                 kd.c, kd.c);
+        fsub2_rn(xh0, xh1, xv0, xv1, mr, mr);
+        fmul2_rn(xh0, xh1, xh0, xh1, ir, ir);
+        ffma2_rn(dh0, dh1, dv0, dv1, g[e], g[e + 1], zero, zero);  // rounded products (they feed adds)
+        ffma2_rn(pr0, pr1, dh0, dh1, xh0, xh1, zero, zero);
         const int j = e & 7;
         if (seg == 0 && e < 8) {  // r[j] = a[j]: the chain starts at its first element
-          c1[j] = dxh;
-          c2[j] = pr;
+          c1[j] = dh0;
+          c1[j + 1] = dh1;
+          c2[j] = pr0;
+          c2[j + 1] = pr1;
         } else {
-          c1[j] = __fadd_rn(c1[j], dxh);
-          c2[j] = __fadd_rn(c2[j], pr);
+          fadd2_rn(c1[j], c1[j + 1], c1[j], c1[j + 1], dh0, dh1);
+          fadd2_rn(c2[j], c2[j + 1], c2[j], c2[j + 1], pr0, pr1);
         }
       }
     }
@@ -412,20 +425,34 @@ __global__ void __launch_bounds__(kTileThreads) ln_bwd_tile_kernel(
       pg[j] = 0.f;
       pb[j] = 0.f;
     }
+    // packed f32x2, the reference's roundings in order; every product that feeds an
+    // add is an FFMA2 with an opaque +0 (ptxas must not contract it)
+    const float zero = opaque_zero();
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int64_t r = t.row(i);
       const float mr = __ldg(A.mu + r), ir = __ldg(A.inv_std + r);
       const float a1 = __ldg(m1 + r), a2 = __ldg(m2 + r);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const float xh = __fmul_rn(__fsub_rn(xv[i][j], mr), ir);
-        const float dxh = __fmul_rn(dv[i][j], g[j]);
-        const float t1 = __fsub_rn(dxh, a1);
-        const float t2 = __fmul_rn(xh, a2);
-        pg[j] = (i == 0) ? __fmul_rn(dv[i][j], xh) : __fadd_rn(pg[j], __fmul_rn(dv[i][j], xh));
-        pb[j] = (i == 0) ? dv[i][j] : __fadd_rn(pb[j], dv[i][j]);
-        xv[i][j] = __fmul_rn(ir, __fsub_rn(t1, t2));  // reuse xv as dx
+      for (int j = 0; j < 8; j += 2) {
+        float xh0, xh1, d0, d1, t0, t1, p0, p1;
+        fsub2_rn(xh0, xh1, xv[i][j], xv[i][j + 1], mr, mr);
+        fmul2_rn(xh0, xh1, xh0, xh1, ir, ir);                               // xhat
+        ffma2_rn(d0, d1, dv[i][j], dv[i][j + 1], g[j], g[j + 1], zero, zero); // dxhat
+        fsub2_rn(d0, d1, d0, d1, a1, a1);                                    // dxhat - m1
+        ffma2_rn(t0, t1, xh0, xh1, a2, a2, zero, zero);                      // xhat * m2
+        ffma2_rn(p0, p1, dv[i][j], dv[i][j + 1], xh0, xh1, zero, zero);      // dy * xhat
+        if (i == 0) {
+          pg[j] = p0;
+          pg[j + 1] = p1;
+          pb[j] = dv[i][j];
+          pb[j + 1] = dv[i][j + 1];
+        } else {
+          fadd2_rn(pg[j], pg[j + 1], pg[j], pg[j + 1], p0, p1);
+          fadd2_rn(pb[j], pb[j + 1], pb[j], pb[j + 1], dv[i][j], dv[i][j + 1]);
+        }
+        fsub2_rn(d0, d1, d0, d1, t0, t1);
+        fmul2_rn(xv[i][j], xv[i][j + 1], ir, ir, d0, d1);  // reuse xv as dx
       }
     }
 #pragma unroll
@@ -646,7 +673,8 @@ __global__ void __launch_bounds__(kTileThreads) gelu_bwd_kernel(
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) v[i][j] = __fmul_rn(d[i][j], __ldg(tb + k[i][j]));
+        for (int j = 0; j < 8; j += 2)
+          fmul2_rn(v[i][j], v[i][j + 1], d[i][j], d[i][j + 1], __ldg(tb + k[i][j]), __ldg(tb + k[i][j + 1]));
     }
     quant_store(t, v, dxq, dxs, red, err);
     return;
