@@ -83,6 +83,23 @@ JF_DEV void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t (&r)[32]) {
       : "memory");
 }
 
+JF_DEV void tmem_ld_32x32b_x16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+JF_DEV void tmem_st_32x32b_x16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+
 template <int N>
 JF_DEV void wait_ld_dep(uint32_t (&r)[N]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -110,6 +127,19 @@ JF_DEV float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+
+// 2^x on the FMA pipe (FA4's trick to relieve the SFU): x = n + f, |f| <= 1/2, 2^f by
+// a degree-3 polynomial (relative error < 7e-4, below the bf16 rounding of P), 2^n
+// added into the exponent.  x <= 8 or -inf.
+JF_DEV float ex2_poly(float x) {
+  x = fmaxf(x, -126.0f);
+  const float xr = __fadd_rn(x, 12582912.0f);  // 1.5 * 2^23 + rint(x)
+  const float f = __fsub_rn(x, __fsub_rn(xr, 12582912.0f));
+  float q = fmaf(f, 0.0555041086648216f, 0.2402265069591007f);
+  q = fmaf(q, f, 0.6931471805599453f);
+  q = fmaf(q, f, 1.0f);
+  return __int_as_float(__float_as_int(q) + (__float_as_int(xr) << 23));
 }
 
 JF_DEV uint32_t bf2(float lo, float hi) {
@@ -177,7 +207,8 @@ struct FwdParams {
   } while (0)
 
 // ── forward kernel: two query tiles (A = rows 0..127, B = rows 128..255) per CTA ──
-constexpr int kProdWarps = 3;                 // warps 8..10
+constexpr int kProdWarps = 7;                 // warps 8..14
+constexpr int kMmaWarp = 8 + kProdWarps;      // warp 15
 constexpr int kFwdThreads = 32 * (8 + kProdWarps + 1);
 
 template <int D>
@@ -223,7 +254,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) attn_fwd_kernel(const FwdParam
     }
     fence_barrier_init();
   }
-  if (warp == 11) tmem_alloc(&B.tmem, 512);
+  if (warp == kMmaWarp) tmem_alloc(&B.tmem, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -320,7 +351,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) attn_fwd_kernel(const FwdParam
       if (j + 1 < nB) scales(j + 1);
     }
     cp_async_wait<0>();
-  } else if (warp == 11) {
+  } else if (warp == kMmaWarp) {
     // ───────────── MMA issuer ─────────────
     // Issues whichever is ready: O_X += P_X(j) V_j (P in TMEM) before S_X(j) = Q_X K_j^T.
     // S_X(j) needs kv tile j and PV_X(j-1) issued: the tensor pipe runs MMAs in issue
@@ -386,22 +417,27 @@ __global__ void __launch_bounds__(kFwdThreads, 1) attn_fwd_kernel(const FwdParam
       mbar_wait(&B.s_full[X], j & 1);
       if (r == 0 && X == 0) ATR(9, j);
       tc_fence_after();
-      uint32_t sr[BKV];
+      // Two passes over TMEM in 32-column chunks (16 warps leave 128 registers per
+      // thread): pass 1 the row max, pass 2 exp2, row sum and P as bf16 pairs written
+      // back over the S columns already consumed (chunk q -> columns [16q, 16q + 16)).
+      const bool diag = j == qt;  // key k > query r masked
+      float mx = -INFINITY;
+#pragma unroll 1
+      for (int q = 0; q < BKV / 32; q += 2) {  // two 32-column loads in flight per wait
+        uint32_t sr[64];
+        tmem_ld_32x32b_x32(tS + 32 * q, *reinterpret_cast<uint32_t(*)[32]>(sr));
+        tmem_ld_32x32b_x32(tS + 32 * q + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
+        wait_ld_dep(sr);
+        const float *sf = reinterpret_cast<const float *>(sr);
+        float m0 = -INFINITY, m1 = -INFINITY;
 #pragma unroll
-      for (int q = 0; q < BKV / 32; ++q)
-        tmem_ld_32x32b_x32(tS + 32 * q, *reinterpret_cast<uint32_t(*)[32]>(sr + 32 * q));
-      wait_ld_dep(sr);
-      if (r == 0 && X == 0) ATR(15, j);
-      float *sf = reinterpret_cast<float *>(sr);
-      if (j == qt) {  // diagonal tile: key k > query r is masked
-#pragma unroll
-        for (int k = 0; k < BKV; ++k)
-          if (k > r) sf[k] = -INFINITY;
+        for (int k = 0; k < 64; k += 2) {
+          m0 = fmaxf(m0, (diag && 32 * q + k > r) ? -INFINITY : sf[k]);
+          m1 = fmaxf(m1, (diag && 32 * q + k + 1 > r) ? -INFINITY : sf[k + 1]);
+        }
+        mx = fmaxf(mx, fmaxf(m0, m1));
       }
-      float mx = fmax3(sf[0], sf[1], sf[2]);
-#pragma unroll
-      for (int k = 3; k < BKV - 1; k += 2) mx = fmax3(mx, sf[k], sf[k + 1]);
-      mx = fmaxf(mx, sf[BKV - 1]);
+      if (r == 0 && X == 0) ATR(15, j);
       if (r == 0 && X == 0) ATR(7, j);
       const float mnew = mx * c;
       bool resc = false;
@@ -414,19 +450,29 @@ __global__ void __launch_bounds__(kFwdThreads, 1) attn_fwd_kernel(const FwdParam
         resc = true;
       }
       float rs0 = 0.0f, rs1 = 0.0f;
-      uint32_t pk[BKV / 2];
+#pragma unroll 1
+      for (int q = 0; q < BKV / 32; ++q) {
+        uint32_t sr[32], pk[16];
+        tmem_ld_32x32b_x32(tS + 32 * q, sr);
+        wait_ld_dep(sr);
+        float *sf = reinterpret_cast<float *>(sr);
+        if (diag) {
 #pragma unroll
-      for (int k = 0; k < BKV; k += 2) {
-        float x0, x1;
-        ffma2_rn(x0, x1, sf[k], sf[k + 1], c, c, -m, -m);
-        const float p0 = ex2(x0), p1 = ex2(x1);
-        fadd2_rn(rs0, rs1, rs0, rs1, p0, p1);
-        pk[k / 2] = bf2(p0, p1);
+          for (int k = 0; k < 32; ++k)
+            if (32 * q + k > r) sf[k] = -INFINITY;
+        }
+#pragma unroll
+        for (int k = 0; k < 32; k += 2) {
+          float x0, x1;
+          ffma2_rn(x0, x1, sf[k], sf[k + 1], c, c, -m, -m);
+          // one pair in four on the FMA pipe: the two softmax tiles of a CTA share the SFU
+          const float p0 = (k % 8 == 6) ? ex2_poly(x0) : ex2(x0), p1 = (k % 8 == 6) ? ex2_poly(x1) : ex2(x1);
+          fadd2_rn(rs0, rs1, rs0, rs1, p0, p1);
+          pk[k / 2] = bf2(p0, p1);
+        }
+        tmem_st_32x32b_x16(tS + 16 * q, pk);
       }
       l = fmaf(l, alpha, rs0 + rs1);
-      // P_X(j) -> TMEM (columns [0, 64) of S_X): S_X(j) is fully read above
-      tmem_st_32x32b_x32(tS, *reinterpret_cast<uint32_t(*)[32]>(pk));
-      tmem_st_32x32b_x32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(pk + 32));
       if (r == 0 && X == 0) ATR(10, j);
       if (j > 0) {
         mbar_wait(&B.o_done[X], (j - 1) & 1);  // PV_X(j-1) done: O_X current
@@ -496,26 +542,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1) attn_fwd_kernel(const FwdParam
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 11) tmem_dealloc(tmem, 512);
+  if (warp == kMmaWarp) tmem_dealloc(tmem, 512);
 }
 
-
-JF_DEV void tmem_ld_32x32b_x16(uint32_t taddr, uint32_t (&r)[16]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-}
-JF_DEV void tmem_st_32x32b_x16(uint32_t taddr, const uint32_t (&r)[16]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
-      "{%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16};" ::"r"(taddr),
-      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
-      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
-      : "memory");
-}
 
 // Requantize one 32-column block of a TMEM row tile (thread = row, warp = 32-row block):
 // fp32 = TMEM value * mul -> 32x32 block absmax -> binary16 scale -> RNE codes.
