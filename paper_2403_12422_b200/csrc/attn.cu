@@ -696,6 +696,14 @@ JF_DEV void bwd_producer(int t, uint32_t sOwn, uint32_t sLoop, uint32_t s8, BwdB
   cp_async_wait<0>();
 }
 
+// Backward warp roles: 0-7 compute (warp w: TMEM lane quarter w % 4, column half w / 4),
+// 8-11 producers, 12 MMA issuer.  13 warps leave 128 registers per thread.
+constexpr int kBwdMma = 12;
+constexpr int kBwdThreads = 32 * (kBwdMma + 1);
+
+// The two compute warps that share a TMEM lane quarter (w, w + 4) meet here.
+JF_DEV void pair_bar(int quarter) { asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory"); }
+
 JF_DEV void bwd_init(BwdBars &B, int warp) {
   if (threadIdx.x == 0) {
     mbar_init(&B.own_full, 128);
@@ -704,11 +712,11 @@ JF_DEV void bwd_init(BwdBars &B, int warp) {
       mbar_init(&B.free_[i], 1);
     }
     mbar_init(&B.s_full, 1);
-    mbar_init(&B.p_full, 128);
+    mbar_init(&B.p_full, 256);
     mbar_init(&B.done, 1);
     fence_barrier_init();
   }
-  if (warp == 8) tmem_alloc(&B.tmem, 512);
+  if (warp == kBwdMma) tmem_alloc(&B.tmem, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -719,7 +727,7 @@ JF_DEV void bwd_init(BwdBars &B, int warp) {
 //   dQ += dS K_j (K_j read MN-major).  Also writes D_i = rowsum(dO * O) for the dK/dV kernel.
 // TMEM: S [0,128), dP [128,256), dQ [256, 256 + D).
 template <int D>
-__global__ void __launch_bounds__(288, 1) attn_bwd_dq_kernel(const BwdParams p) {
+__global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_dq_kernel(const BwdParams p) {
   using SM = BwdSmem<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -736,11 +744,11 @@ __global__ void __launch_bounds__(288, 1) attn_bwd_dq_kernel(const BwdParams p) 
   bwd_init(B, warp);
   const uint32_t tmem = B.tmem;
 
-  if (warp >= 4 && warp < 8) {
+  if (warp >= 8 && warp < kBwdMma) {
     const Src q{p.qkv, p.qkv_s, C3, (int64_t)h * D}, dO{p.dout, p.dout_s, C, (int64_t)h * D};
     const Src k{p.qkv, p.qkv_s, C3, C + (int64_t)h * D}, v{p.qkv, p.qkv_s, C3, 2 * C + (int64_t)h * D};
-    bwd_producer<D>(threadIdx.x - 128, sOwn, sLoop, s8, B, q, dO, row0, k, v, (int64_t)b * S, 0, n, p);
-  } else if (warp == 8) {
+    bwd_producer<D>(threadIdx.x - 256, sOwn, sLoop, s8, B, q, dO, row0, k, v, (int64_t)b * S, 0, n, p);
+  } else if (warp == kBwdMma) {
     constexpr uint32_t idS = idesc_16(BQ, BKV, 0, 0, 1);
     constexpr uint32_t idQ = idesc_16(BQ, D, 0, 1, 1);
     mbar_wait(&B.own_full, 0);
@@ -770,10 +778,10 @@ __global__ void __launch_bounds__(288, 1) attn_bwd_dq_kernel(const BwdParams p) 
       }
       __syncwarp();
     }
-  } else if (warp < 4) {
-    const int r = threadIdx.x;
+  } else if (warp < 8) {
+    const int r = (warp & 3) * 32 + lane, hf = warp >> 2;  // query row, column half
     const int64_t row = row0 + r;
-    const uint32_t lb = tmem + ((uint32_t)(warp * 32) << 16);
+    const uint32_t lb = tmem + ((uint32_t)((warp & 3) * 32) << 16);
     const int64_t hs = ((int64_t)b * H + h) * S + (int64_t)qt * BQ + r;
     // D_i = sum_d dO[i, d] * O[i, d] (dO dequantized exactly, O in bf16)
     float dsum = 0.0f;
@@ -801,19 +809,23 @@ __global__ void __launch_bounds__(288, 1) attn_bwd_dq_kernel(const BwdParams p) 
         }
       }
     }
-    p.dsum[hs] = dsum;
+    if (hf == 0) p.dsum[hs] = dsum;
     const float lse = p.lse[hs], c = p.scale_log2, sc = p.scale;
 #pragma unroll 1
     for (int j = 0; j < n; ++j) {
       mbar_wait(&B.s_full, j & 1);
       tc_fence_after();
 #pragma unroll 1
-      for (int q = 0; q < BKV / 32; ++q) {
+      for (int it = 0; it < 2; ++it) {
+        // half hf takes 32-column chunks hf and hf + 2; dS of chunk q goes to columns
+        // [16q, 16q + 16), which after the pair barrier both warps have read
+        const int q = hf + 2 * it;
         uint32_t sr[32], dr[32];
         tmem_ld_32x32b_x32(lb + 32 * q, sr);
         tmem_ld_32x32b_x32(lb + BKV + 32 * q, dr);
         wait_ld_dep(sr);
         wait_ld_dep(dr);
+        if (it == 0) pair_bar(warp & 3);
         uint32_t pk[16];
 #pragma unroll
         for (int k = 0; k < 32; k += 2) {
@@ -836,7 +848,7 @@ __global__ void __launch_bounds__(288, 1) attn_bwd_dq_kernel(const BwdParams p) 
     tc_fence_after();
     int flags = 0;
 #pragma unroll 1
-    for (int q = 0; q < D / 32; ++q) {
+    for (int q = hf * (D / 64); q < (hf + 1) * (D / 64); ++q) {
       const int64_t col = (int64_t)h * D + 32 * q;
       flags |= quant_tmem_block(lb + 2 * BKV + 32 * q, 1.0f, p.dqkv + row * C3 + col,
                                 p.dqkv_s + (row >> 5) * (C3 >> 5) + (col >> 5), lane);
@@ -845,7 +857,7 @@ __global__ void __launch_bounds__(288, 1) attn_bwd_dq_kernel(const BwdParams p) 
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 8) tmem_dealloc(tmem, 512);
+  if (warp == kBwdMma) tmem_dealloc(tmem, 512);
 }
 
 // dK/dV kernel: CTA = kv tile j of (b, h); loops over query tiles j..nq-1.
@@ -853,7 +865,7 @@ __global__ void __launch_bounds__(288, 1) attn_bwd_dq_kernel(const BwdParams p) 
 //   dS^T = P^T (dP^T - D_q) / sqrt(d); dV += P^T dO_i, dK += dS^T Q_i (A from TMEM,
 //   Q_i / dO_i read MN-major).  TMEM: S^T [0,128), dP^T [128,256), dV, dK after.
 template <int D>
-__global__ void __launch_bounds__(288, 1) attn_bwd_dkv_kernel(const BwdParams p) {
+__global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_dkv_kernel(const BwdParams p) {
   using SM = BwdSmem<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -871,11 +883,11 @@ __global__ void __launch_bounds__(288, 1) attn_bwd_dkv_kernel(const BwdParams p)
   bwd_init(B, warp);
   const uint32_t tmem = B.tmem;
 
-  if (warp >= 4 && warp < 8) {
+  if (warp >= 8 && warp < kBwdMma) {
     const Src k{p.qkv, p.qkv_s, C3, C + (int64_t)h * D}, v{p.qkv, p.qkv_s, C3, 2 * C + (int64_t)h * D};
     const Src q{p.qkv, p.qkv_s, C3, (int64_t)h * D}, dO{p.dout, p.dout_s, C, (int64_t)h * D};
-    bwd_producer<D>(threadIdx.x - 128, sOwn, sLoop, s8, B, k, v, row0, q, dO, (int64_t)b * S, kt, n, p);
-  } else if (warp == 8) {
+    bwd_producer<D>(threadIdx.x - 256, sOwn, sLoop, s8, B, k, v, row0, q, dO, (int64_t)b * S, kt, n, p);
+  } else if (warp == kBwdMma) {
     constexpr uint32_t idS = idesc_16(BKV, BQ, 0, 0, 1);
     constexpr uint32_t idG = idesc_16(BKV, D, 0, 1, 1);
     mbar_wait(&B.own_full, 0);
@@ -911,10 +923,10 @@ __global__ void __launch_bounds__(288, 1) attn_bwd_dkv_kernel(const BwdParams p)
       }
       __syncwarp();
     }
-  } else if (warp < 4) {
-    const int r = threadIdx.x;  // key row
+  } else if (warp < 8) {
+    const int r = (warp & 3) * 32 + lane, hf = warp >> 2;  // key row, query-column half
     const int64_t row = row0 + r;
-    const uint32_t lb = tmem + ((uint32_t)(warp * 32) << 16);
+    const uint32_t lb = tmem + ((uint32_t)((warp & 3) * 32) << 16);
     const float c = p.scale_log2, sc = p.scale;
     const int64_t hs0 = ((int64_t)b * H + h) * S;
 #pragma unroll 1
@@ -926,30 +938,37 @@ __global__ void __launch_bounds__(288, 1) attn_bwd_dkv_kernel(const BwdParams p)
       if (r == 0) ATR(8, j);
       tc_fence_after();
 #pragma unroll 1
-      for (int q = 0; q < BQ / 32; ++q) {
+      for (int it = 0; it < 2; ++it) {
+        // half hf takes 32-column chunks hf and hf + 2; P / dS of chunk q go to columns
+        // [16q, 16q + 16) of S^T / dP^T, which after the pair barrier both warps have read
+        const int q = hf + 2 * it;
         uint32_t sr[32], dr[32];
         tmem_ld_32x32b_x32(lb + 32 * q, sr);
         tmem_ld_32x32b_x32(lb + BQ + 32 * q, dr);
-        float lq[32], dq[32];
-#pragma unroll
-        for (int k = 0; k < 32; k += 4) {
-          *reinterpret_cast<float4 *>(lq + k) = __ldg(reinterpret_cast<const float4 *>(lse + 32 * q + k));
-          *reinterpret_cast<float4 *>(dq + k) = __ldg(reinterpret_cast<const float4 *>(dsv + 32 * q + k));
-        }
         wait_ld_dep(sr);
         wait_ld_dep(dr);
+        if (it == 0) pair_bar(warp & 3);
         uint32_t pk[16], dk[16];
 #pragma unroll
-        for (int k = 0; k < 32; k += 2) {
-          float pr[2], ds[2];
+        for (int k8 = 0; k8 < 32; k8 += 8) {  // lse / D of 8 query columns at a time
+          float lq[8], dq[8];
+          *reinterpret_cast<float4 *>(lq) = __ldg(reinterpret_cast<const float4 *>(lse + 32 * q + k8));
+          *reinterpret_cast<float4 *>(lq + 4) = __ldg(reinterpret_cast<const float4 *>(lse + 32 * q + k8 + 4));
+          *reinterpret_cast<float4 *>(dq) = __ldg(reinterpret_cast<const float4 *>(dsv + 32 * q + k8));
+          *reinterpret_cast<float4 *>(dq + 4) = __ldg(reinterpret_cast<const float4 *>(dsv + 32 * q + k8 + 4));
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const bool masked = j == 0 && 32 * q + k + e < r;  // query before key (diagonal tile)
-            pr[e] = masked ? 0.0f : ex2(fmaf(__uint_as_float(sr[k + e]), c, -lq[k + e]));
-            ds[e] = pr[e] * (__uint_as_float(dr[k + e]) - dq[k + e]) * sc;
+          for (int k = 0; k < 8; k += 2) {
+            float pr[2], ds[2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int kk = k8 + k + e;
+              const bool masked = j == 0 && 32 * q + kk < r;  // query before key (diagonal tile)
+              pr[e] = masked ? 0.0f : ex2(fmaf(__uint_as_float(sr[kk]), c, -lq[k + e]));
+              ds[e] = pr[e] * (__uint_as_float(dr[kk]) - dq[k + e]) * sc;
+            }
+            pk[(k8 + k) / 2] = bf2(pr[0], pr[1]);
+            dk[(k8 + k) / 2] = bf2(ds[0], ds[1]);
           }
-          pk[k / 2] = bf2(pr[0], pr[1]);
-          dk[k / 2] = bf2(ds[0], ds[1]);
         }
         tmem_st_32x32b_x16(lb + 16 * q, pk);
         tmem_st_32x32b_x16(lb + BQ + 16 * q, dk);
@@ -963,7 +982,7 @@ __global__ void __launch_bounds__(288, 1) attn_bwd_dkv_kernel(const BwdParams p)
     tc_fence_after();
     int flags = 0;
 #pragma unroll 1
-    for (int q = 0; q < D / 32; ++q) {
+    for (int q = hf * (D / 64); q < (hf + 1) * (D / 64); ++q) {
       const int64_t ck = C + (int64_t)h * D + 32 * q, cv = 2 * C + (int64_t)h * D + 32 * q;
       flags |= quant_tmem_block(lb + 2 * BQ + D + 32 * q, 1.0f, p.dqkv + row * C3 + ck,
                                 p.dqkv_s + (row >> 5) * (C3 >> 5) + (ck >> 5), lane);
@@ -974,7 +993,7 @@ __global__ void __launch_bounds__(288, 1) attn_bwd_dkv_kernel(const BwdParams p)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 8) tmem_dealloc(tmem, 512);
+  if (warp == kBwdMma) tmem_dealloc(tmem, 512);
 }
 
 }  // namespace attn
@@ -1036,14 +1055,14 @@ extern "C" int jf_attn_bwd_q(const int8_t *qkv, const float *qkv_s, const int8_t
     const int smem = BwdSmem<64>::kBytes;
     if (int rc = jf_set_smem_attr((const void *)attn_bwd_dq_kernel<64>, smem, "attn_bwd attr")) return rc;
     if (int rc = jf_set_smem_attr((const void *)attn_bwd_dkv_kernel<64>, smem, "attn_bwd attr")) return rc;
-    attn_bwd_dq_kernel<64><<<grid, 288, smem, st>>>(p);
-    attn_bwd_dkv_kernel<64><<<grid, 288, smem, st>>>(p);
+    attn_bwd_dq_kernel<64><<<grid, kBwdThreads, smem, st>>>(p);
+    attn_bwd_dkv_kernel<64><<<grid, kBwdThreads, smem, st>>>(p);
   } else {
     const int smem = BwdSmem<128>::kBytes;
     if (int rc = jf_set_smem_attr((const void *)attn_bwd_dq_kernel<128>, smem, "attn_bwd attr")) return rc;
     if (int rc = jf_set_smem_attr((const void *)attn_bwd_dkv_kernel<128>, smem, "attn_bwd attr")) return rc;
-    attn_bwd_dq_kernel<128><<<grid, 288, smem, st>>>(p);
-    attn_bwd_dkv_kernel<128><<<grid, 288, smem, st>>>(p);
+    attn_bwd_dq_kernel<128><<<grid, kBwdThreads, smem, st>>>(p);
+    attn_bwd_dkv_kernel<128><<<grid, kBwdThreads, smem, st>>>(p);
   }
   return jf_launch_check("attn_bwd");
 }
