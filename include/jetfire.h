@@ -224,6 +224,12 @@ int jf_adamw_quantize(float *p, const float *g, float *m, float *v, int64_t n, i
  * jf_adamw).  `tensors`: device array of {float *p; const float *g; float *m; float *v;
  * int64 count; float wd; int32 pad} (48 bytes each); chunk c covers elements
  * [chunk_start[c], chunk_start[c] + chunk_len) of tensor chunk_tensor[c]. */
+/* jf_adamw_quantize_multi: jf_adamw_quantize over several [n x c] matrices in one launch.
+ * `tensors`: device array of {float *p; const float *g; float *m; float *v; int8_t *q;
+ * float *s; int64 n, c; float wd; int32 pad; int64 tile_start} (80 bytes each), tile_start =
+ * the matrix's first 32x256 tile in a running count (ascending); total_tiles = the sum. */
+int jf_adamw_quantize_multi(const void *tensors, int32_t ntensors, int64_t total_tiles, float lr, double b1,
+                            double b2, float eps, float bc1, float bc2, int32_t *err, jf_stream_t stream);
 int jf_adamw_multi(const void *tensors, const int32_t *chunk_tensor, const int64_t *chunk_start,
                    int32_t nchunks, int64_t chunk_len, float lr, double b1, double b2, float eps,
                    float bc1, float bc2, jf_stream_t stream);

@@ -74,6 +74,8 @@ SIGNATURES = {
                                       _F32, _P]),
     "jf_adamw_quantize": (ctypes.c_int, [_P, _P, _P, _P, _I64, _I64, _F32, ctypes.c_double, ctypes.c_double, _F32,
                                          _F32, _F32, _F32, _P, _P, _P, _P]),
+    "jf_adamw_quantize_multi": (ctypes.c_int, [_P, _I32, _I64, _F32, ctypes.c_double, ctypes.c_double, _F32, _F32,
+                                               _F32, _P, _P]),
     "jf_cross_entropy_bf16": (ctypes.c_int, [_P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P]),
     "jf_dequantize_qkv_heads": (ctypes.c_int, [_P, _P, _I64, _I64, _I64, _I64, _P, _P, _P, _P]),
     "jf_quantize_heads_bf16": (ctypes.c_int, [_P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _P, _I64, _P, _I64,
@@ -138,9 +140,9 @@ def stream_handle() -> int:
 # kernels each C entry point enqueues (for bench.py's gpu_launches tally)
 KERNELS_PER_CALL = {
     "quantize": 1, "dequantize": 1, "transpose": 1, "gemm_fwd": 1, "gemm_dgrad": 1, "gemm_wgrad": 1,
-    "gemm_partials": 1, "add_stats": 1, "ln_fwd": 2, "ln_bwd": 4, "gelu_fwd": 1, "gelu_bwd": 1,
+    "gemm_partials": 1, "add_stats": 1, "ln_fwd": 2, "ln_bwd": 3, "gelu_fwd": 1, "gelu_bwd": 1,
     "colsum": 2, "dropout": 1, "philox_keep": 1, "gelu_tables": 1, "dequant_qkv_heads": 1, "quantize_heads": 1,
-    "cross_entropy": 1, "attn_fwd": 1, "attn_bwd": 2, "adamw": 1, "adamw_quantize": 1, "adamw_multi": 1, "widen_codes": 1, "gemm_f16": 1,
+    "cross_entropy": 1, "attn_fwd": 1, "attn_bwd": 2, "adamw": 1, "adamw_quantize": 1, "adamw_multi": 1, "adamw_quantize_multi": 1, "widen_codes": 1, "gemm_f16": 1,
 }
 launch_count = [0]
 

@@ -479,13 +479,17 @@ __global__ void __launch_bounds__(kTileThreads) ln_bwd_tile_kernel(
 // Sum per-strip partials: out[j] = sum_s part[s, j].  CTA = 32 columns x 8
 // warps; warp w sums strips [w*S/8, (w+1)*S/8) in order (loads unrolled so
 // they stay in flight), then the 8 warp sums are added in warp order.
-__global__ void __launch_bounds__(256) strip_reduce_kernel(const float *__restrict__ part,
-                                                           int64_t strips, int64_t c,
-                                                           float *out) {
-  __shared__ float ws[8][32];
+__global__ void __launch_bounds__(512) strip_reduce_kernel(const float *__restrict__ part0,
+                                                           const float *__restrict__ part1, int64_t strips,
+                                                           int64_t c, float *out0, float *out1) {
+  // blockIdx.y selects the array (LN backward reduces dgamma and dbeta in one launch);
+  // 16 warps split the strips in order, then the 16 warp sums are added in warp order.
+  __shared__ float ws[16][32];
+  const float *part = blockIdx.y ? part1 : part0;
+  float *out = blockIdx.y ? out1 : out0;
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   const int64_t j = (int64_t)blockIdx.x * 32 + l;
-  const int64_t s0 = strips * w / 8, s1 = strips * (w + 1) / 8;
+  const int64_t s0 = strips * w / 16, s1 = strips * (w + 1) / 16;
   float acc = 0.f;
   if (j < c) {
     int64_t s = s0;
@@ -503,7 +507,7 @@ __global__ void __launch_bounds__(256) strip_reduce_kernel(const float *__restri
   if (w == 0 && j < c) {
     float t = ws[0][l];
 #pragma unroll
-    for (int u = 1; u < 8; ++u) t = __fadd_rn(t, ws[u][l]);
+    for (int u = 1; u < 16; ++u) t = __fadd_rn(t, ws[u][l]);
     out[j] = t;
   }
 }
@@ -881,8 +885,7 @@ extern "C" int jf_ln_bwd(const int8_t *x, const float *xs, const float *mu, cons
   rc = jf_launch_check("ln_bwd_tile");
   if (rc) return rc;
   const unsigned g = (unsigned)((c + 31) / 32);
-  strip_reduce_kernel<<<g, 256, 0, st>>>(pg, n / 32, c, dgamma);
-  strip_reduce_kernel<<<g, 256, 0, st>>>(pb, n / 32, c, dbeta);
+  strip_reduce_kernel<<<dim3(g, 2), 512, 0, st>>>(pg, pb, n / 32, c, dgamma, dbeta);
   return jf_launch_check("ln_bwd_reduce");
 }
 
@@ -898,7 +901,7 @@ extern "C" int jf_colsum(const int8_t *q, const float *s, int64_t n, int64_t c, 
   colsum_tile_kernel<<<tile_grid(n, c), kTileThreads, 0, st>>>(q, s, n, c, part);
   int rc = jf_launch_check("colsum_tile");
   if (rc) return rc;
-  strip_reduce_kernel<<<(unsigned)((c + 31) / 32), 256, 0, st>>>(part, n / 32, c, out);
+  strip_reduce_kernel<<<dim3((unsigned)((c + 31) / 32), 1), 512, 0, st>>>(part, part, n / 32, c, out, out);
   return jf_launch_check("colsum_reduce");
 }
 

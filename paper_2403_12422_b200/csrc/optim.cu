@@ -39,12 +39,10 @@ __global__ void __launch_bounds__(256) adamw_kernel(float *p, const float *__res
   }
 }
 
-// Matrix update + per-block re-quantization: 32 x 256 tiles (tile.cuh).
-__global__ void __launch_bounds__(kTileThreads) adamw_quant_kernel(float *p, const float *__restrict__ g, float *m,
-                                                                   float *v, int64_t n, int64_t c, AdamArgs a,
-                                                                   int8_t *q, float *s, int32_t *err) {
-  __shared__ uint32_t red[64];
-  const TilePos t = tile_pos(n, c);
+// Matrix update + per-block re-quantization of one 32 x 256 tile (tile.cuh).
+JF_DEV void adamw_quant_tile(const TilePos &t, float *__restrict__ p, const float *__restrict__ g,
+                             float *__restrict__ m, float *__restrict__ v, int64_t c, const AdamArgs &a,
+                             int8_t *q, float *s, int32_t *err, uint32_t *red) {
   float w[4][8];
   if (t.active) {
 #pragma unroll
@@ -71,6 +69,61 @@ __global__ void __launch_bounds__(kTileThreads) adamw_quant_kernel(float *p, con
     }
   }
   quant_store(t, w, q, s, red, err);
+}
+
+__global__ void __launch_bounds__(kTileThreads) adamw_quant_kernel(float *__restrict__ p,
+                                                                   const float *__restrict__ g,
+                                                                   float *__restrict__ m, float *__restrict__ v,
+                                                                   int64_t n, int64_t c, AdamArgs a,
+                                                                   int8_t *q, float *s, int32_t *err) {
+  __shared__ uint32_t red[64];
+  adamw_quant_tile(tile_pos(n, c), p, g, m, v, c, a, q, s, err, red);
+}
+
+// All block weight matrices in one launch: a device table of tensors, each with the
+// global index of its first 32 x 256 tile; CTA = one tile (the tensor found by a
+// binary search over the tile starts).  Same per-tile work as adamw_quant_kernel, but
+// no per-matrix launch and no per-matrix wave tail (a 1024 x 1024 matrix alone is 128
+// tiles on 148 SMs).
+struct AdamQTensor {
+  float *p;
+  const float *g;
+  float *m;
+  float *v;
+  int8_t *q;
+  float *s;
+  int64_t n, c;
+  float wd;
+  int32_t pad;
+  int64_t tile_start;
+};
+static_assert(sizeof(AdamQTensor) == 80, "AdamQTensor layout (mirrored in model.py)");
+
+__global__ void __launch_bounds__(kTileThreads, 3) adamw_quant_multi_kernel(const AdamQTensor *__restrict__ tab,
+                                                                         int32_t ntensors, AdamArgs a,
+                                                                         int32_t *err) {
+  __shared__ uint32_t red[64];
+  const int64_t tile = blockIdx.x;
+  int lo = 0, hi = ntensors - 1;  // last tensor whose tile_start <= tile
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (__ldg(&tab[mid].tile_start) <= tile) lo = mid;
+    else hi = mid - 1;
+  }
+  const AdamQTensor &T = tab[lo];
+  const int64_t n = T.n, c = T.c, local = tile - T.tile_start;
+  const int64_t gx = (c + kTileCols - 1) / kTileCols;
+  TilePos t;
+  t.r0 = (local / gx) * kTileRows;
+  t.c0 = (local % gx) * kTileCols;
+  t.n = n;
+  t.c = c;
+  t.warp = threadIdx.x >> 5;
+  t.lane = threadIdx.x & 31;
+  t.active = t.col() < c;
+  AdamArgs aa = a;
+  aa.wd = T.wd;
+  adamw_quant_tile(t, T.p, T.g, T.m, T.v, c, aa, T.q, T.s, err, red);
 }
 
 // Many small tensors (biases, LayerNorm γ/β) in one launch: a table of tensors
@@ -143,6 +196,15 @@ extern "C" int jf_adamw_quantize(float *p, const float *g, float *m, float *v, i
   adamw_quant_kernel<<<tile_grid(n, c), kTileThreads, 0, (cudaStream_t)stream>>>(
       p, g, m, v, n, c, adam_args(lr, b1, b2, eps, wd, bc1, bc2), q, s, err);
   return jf_launch_check("adamw_quantize");
+}
+
+extern "C" int jf_adamw_quantize_multi(const void *tensors, int32_t ntensors, int64_t total_tiles, float lr,
+                                       double b1, double b2, float eps, float bc1, float bc2, int32_t *err,
+                                       jf_stream_t stream) {
+  if (ntensors <= 0 || total_tiles <= 0 || total_tiles > 0x7fffffff) return JF_ERR_ARG;
+  adamw_quant_multi_kernel<<<(unsigned)total_tiles, kTileThreads, 0, (cudaStream_t)stream>>>(
+      static_cast<const AdamQTensor *>(tensors), ntensors, adam_args(lr, b1, b2, eps, 0.0f, bc1, bc2), err);
+  return jf_launch_check("adamw_quantize_multi");
 }
 
 extern "C" int jf_adamw_multi(const void *tensors, const int32_t *chunk_tensor, const int64_t *chunk_start,

@@ -269,8 +269,10 @@ class AdamW:
             ev.record()
             _lib.check(L.jf_adamw_multi(dev.data_ptr(), chunk_t.data_ptr(), chunk_s.data_ptr(), chunk_t.numel(),
                                         self.CHUNK, self.lr, b1, b2, self.eps, bc1, bc2, st), "adamw_multi")
+        if self.qlin:
+            self._step_matrices(grads, L, b1, b2, bc1, bc2, st)
         for key, p in self.model.params.items():
-            if key in small:
+            if key in small or key in self.qlin:
                 continue
             g = grads[key].contiguous()
             wd = self.weight_decay if (key in self.model.decay_keys and self.weight_decay) else 0.0
@@ -291,6 +293,49 @@ class AdamW:
                 _lib.check(L.jf_adamw(p.data_ptr(), g.data_ptr(), self.m[key].data_ptr(), self.v[key].data_ptr(),
                                       p.numel(), self.lr, b1, b2, self.eps, wd, bc1, bc2, st), "adamw")
         _rt.maybe_check()
+
+
+    def _step_matrices(self, grads, L, b1, b2, bc1, bc2, st) -> None:
+        """Every block weight matrix in ONE jf_adamw_quantize_multi launch (update + in-place
+        INT8 requantization; per-matrix launches left the 1024-wide models' SMs idle)."""
+        import struct
+
+        from . import runtime as _rt
+        from .qtensor import empty_like_shape
+
+        keys = list(self.qlin)
+        dev0 = self.model.params[keys[0]].device
+        if getattr(self, "_qmulti", None) is None:
+            host = torch.empty((len(keys), 10), dtype=torch.int64).pin_memory()
+            devt = torch.empty((len(keys), 10), dtype=torch.int64, device=dev0)
+            ev = torch.cuda.Event()
+            ev.record()
+            self._qmulti = (host, devt, ev)
+        host, devt, ev = self._qmulti
+        ev.synchronize()  # the previous step's upload of the pinned table has finished
+        tab = host.numpy()
+        tiles = 0
+        for i, key in enumerate(keys):
+            p, lin = self.model.params[key], self.qlin[key]
+            g = grads[key]
+            if not g.is_contiguous():
+                g = grads[key] = g.contiguous()
+            n, c = p.shape
+            # the INT8 copy is rewritten in place (stable addresses: a captured CUDA graph
+            # of loss_and_grads keeps reading the live weights); derived copies go stale
+            wq = lin._weight_q
+            if wq is None:
+                wq = empty_like_shape(n, c, p.device)
+            wd = self.weight_decay if (key in self.model.decay_keys and self.weight_decay) else 0.0
+            wd_bits = struct.unpack("<I", struct.pack("<f", wd))[0]
+            tab[i] = (p.data_ptr(), g.data_ptr(), self.m[key].data_ptr(), self.v[key].data_ptr(),
+                      wq.values.data_ptr(), wq.scales.data_ptr(), n, c, wd_bits, tiles)
+            tiles += (n // 32) * ((c + 255) // 256)
+            lin.set_weight_q(wq)
+        devt.copy_(host, non_blocking=True)
+        ev.record()
+        _lib.check(L.jf_adamw_quantize_multi(devt.data_ptr(), len(keys), tiles, self.lr, b1, b2, self.eps, bc1,
+                                             bc2, _rt.err_ptr(), st), "adamw_quantize_multi")
 
 
 class GraphedTrainStep:
