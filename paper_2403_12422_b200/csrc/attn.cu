@@ -610,7 +610,7 @@ struct BwdSmem {
 };
 
 struct BwdBars {
-  uint64_t own_full, full[2], free_[2], s_full, p_full, done;
+  uint64_t own_full, full[2], free_[2], s_full[2], p_full[2], done;
   uint32_t tmem;
 };
 
@@ -618,19 +618,28 @@ struct BwdBars {
 // row tiles (rows own_row0..+127 of own0/own1) once, then `count` loop tiles
 // (rows row_b + 128*(first + j) of loop0/loop1) through the cp.async staging slot
 // into the 2-stage bf16 ring.
+// Backward warp roles: 0-7 compute (warp w: TMEM lane quarter w % 4, 64-column half w / 4),
+// 8-14 producers, 15 MMA issuer.  16 warps leave 128 registers per thread.
+constexpr int kBwdProd = 7;
+constexpr int kBwdMma = 8 + kBwdProd;
+constexpr int kBwdThreads = 32 * (kBwdMma + 1);
+
 template <int D>
 JF_DEV void bwd_producer(int t, uint32_t sOwn, uint32_t sLoop, uint32_t s8, BwdBars &B, Src own0, Src own1,
                          int64_t own_row0, Src l0, Src l1, int64_t row_b, int first, int count,
                          const BwdParams &p) {
   using SM = BwdSmem<D>;
-  constexpr int kC16 = D / 16, kChunks = BKV * kC16, kPer = kChunks / 128;
+  constexpr int kNP = 32 * kBwdProd;
+  constexpr int kC16 = D / 16, kChunks = BKV * kC16, kPer = (kChunks + kNP - 1) / kNP;
   auto issue = [&](int j) {
     const int64_t r0 = row_b + (int64_t)(first + j) * BKV;
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
-      const int ci = t + 128 * i, r = ci / kC16, c16 = ci % kC16;
-      cp_async16(s8 + 16 * ci, l0.q + (r0 + r) * l0.ld + l0.col + 16 * c16);
-      cp_async16(s8 + SM::kStage8 + 16 * ci, l1.q + (r0 + r) * l1.ld + l1.col + 16 * c16);
+      const int ci = t + kNP * i, r = ci / kC16, c16 = ci % kC16;
+      if (ci < kChunks) {
+        cp_async16(s8 + 16 * ci, l0.q + (r0 + r) * l0.ld + l0.col + 16 * c16);
+        cp_async16(s8 + SM::kStage8 + 16 * ci, l1.q + (r0 + r) * l1.ld + l1.col + 16 * c16);
+      }
     }
     cp_async_commit();
   };
@@ -639,7 +648,7 @@ JF_DEV void bwd_producer(int t, uint32_t sOwn, uint32_t sLoop, uint32_t s8, BwdB
     const int64_t r0 = row_b + (int64_t)(first + j) * BKV;
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
-      const int ci = t + 128 * i, r = ci / kC16, c16 = ci % kC16;
+      const int ci = min(t + kNP * i, kChunks - 1), r = ci / kC16, c16 = ci % kC16;
       sa[i] = __ldg(l0.s + ((r0 + r) >> 5) * (l0.ld >> 5) + ((l0.col + 16 * c16) >> 5));
       sb[i] = __ldg(l1.s + ((r0 + r) >> 5) * (l1.ld >> 5) + ((l1.col + 16 * c16) >> 5));
     }
@@ -650,7 +659,7 @@ JF_DEV void bwd_producer(int t, uint32_t sOwn, uint32_t sLoop, uint32_t s8, BwdB
     float a0[kPer], a1[kPer];
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
-      const int ci = t + 128 * i, r = ci / kC16, c16 = ci % kC16;
+      const int ci = min(t + kNP * i, kChunks - 1), r = ci / kC16, c16 = ci % kC16;
       const int64_t row = own_row0 + r;
       w0[i] = __ldg(reinterpret_cast<const uint4 *>(own0.q + row * own0.ld + own0.col + 16 * c16));
       w1[i] = __ldg(reinterpret_cast<const uint4 *>(own1.q + row * own1.ld + own1.col + 16 * c16));
@@ -659,9 +668,11 @@ JF_DEV void bwd_producer(int t, uint32_t sOwn, uint32_t sLoop, uint32_t s8, BwdB
     }
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
-      const int ci = t + 128 * i, r = ci / kC16, c16 = ci % kC16;
-      deq16_store(sOwn, r, 2 * c16, w0[i], a0[i]);
-      deq16_store(sOwn + SM::kTile, r, 2 * c16, w1[i], a1[i]);
+      const int ci = t + kNP * i, r = ci / kC16, c16 = ci % kC16;
+      if (ci < kChunks) {
+        deq16_store(sOwn, r, 2 * c16, w0[i], a0[i]);
+        deq16_store(sOwn + SM::kTile, r, 2 * c16, w1[i], a1[i]);
+      }
     }
     fence_proxy_async_smem();
     mbar_arrive(&B.own_full);
@@ -678,15 +689,18 @@ JF_DEV void bwd_producer(int t, uint32_t sOwn, uint32_t sLoop, uint32_t s8, BwdB
     uint4 w0[kPer], w1[kPer];
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
-      w0[i] = lds128(s8 + 16 * (t + 128 * i));
-      w1[i] = lds128(s8 + SM::kStage8 + 16 * (t + 128 * i));
+      const int ci = min(t + kNP * i, kChunks - 1);
+      w0[i] = lds128(s8 + 16 * ci);
+      w1[i] = lds128(s8 + SM::kStage8 + 16 * ci);
     }
     if (j + 1 < count) issue(j + 1);
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
-      const int ci = t + 128 * i, r = ci / kC16, c16 = ci % kC16;
-      deq16_store(t0, r, 2 * c16, w0[i], sa[i]);
-      deq16_store(t1, r, 2 * c16, w1[i], sb[i]);
+      const int ci = t + kNP * i, r = ci / kC16, c16 = ci % kC16;
+      if (ci < kChunks) {
+        deq16_store(t0, r, 2 * c16, w0[i], sa[i]);
+        deq16_store(t1, r, 2 * c16, w1[i], sb[i]);
+      }
     }
     fence_proxy_async_smem();
     if (t == 0) ATR(2, j);
@@ -696,23 +710,18 @@ JF_DEV void bwd_producer(int t, uint32_t sOwn, uint32_t sLoop, uint32_t s8, BwdB
   cp_async_wait<0>();
 }
 
-// Backward warp roles: 0-7 compute (warp w: TMEM lane quarter w % 4, column half w / 4),
-// 8-11 producers, 12 MMA issuer.  13 warps leave 128 registers per thread.
-constexpr int kBwdMma = 12;
-constexpr int kBwdThreads = 32 * (kBwdMma + 1);
-
-// The two compute warps that share a TMEM lane quarter (w, w + 4) meet here.
-JF_DEV void pair_bar(int quarter) { asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory"); }
 
 JF_DEV void bwd_init(BwdBars &B, int warp) {
   if (threadIdx.x == 0) {
-    mbar_init(&B.own_full, 128);
+    mbar_init(&B.own_full, 32 * kBwdProd);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&B.full[i], 128);
+      mbar_init(&B.full[i], 32 * kBwdProd);
       mbar_init(&B.free_[i], 1);
     }
-    mbar_init(&B.s_full, 1);
-    mbar_init(&B.p_full, 256);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&B.s_full[i], 1);
+      mbar_init(&B.p_full[i], 128);
+    }
     mbar_init(&B.done, 1);
     fence_barrier_init();
   }
@@ -749,37 +758,58 @@ __global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_dq_kernel(const BwdPa
     const Src k{p.qkv, p.qkv_s, C3, C + (int64_t)h * D}, v{p.qkv, p.qkv_s, C3, 2 * C + (int64_t)h * D};
     bwd_producer<D>(threadIdx.x - 256, sOwn, sLoop, s8, B, q, dO, row0, k, v, (int64_t)b * S, 0, n, p);
   } else if (warp == kBwdMma) {
-    constexpr uint32_t idS = idesc_16(BQ, BKV, 0, 0, 1);
+    // Key tile j in two 64-column halves x: S_x = Q K_j[x]^T and dP_x = dO V_j[x]^T (N = 64)
+    // into TMEM half x; compute warps of half x write dS_x (bf16) over S_x; then
+    // dQ += dS_x K_j[x] (TS-MMA, K = 64).  Order S_0 S_1 | G_0 S_0' | G_1 S_1' ...: the
+    // next tile's S_x follows this tile's G_x in the in-order tensor pipe.
+    constexpr uint32_t idS = idesc_16(BQ, 64, 0, 0, 1);
     constexpr uint32_t idQ = idesc_16(BQ, D, 0, 1, 1);
-    mbar_wait(&B.own_full, 0);
-#pragma unroll 1
-    for (int j = 0; j < n; ++j) {
+    const uint32_t a_full = smem_u32(&B.full[0]), a_p = smem_u32(&B.p_full[0]);
+    auto issue_s = [&](int j, int x) {
       const int st = j & 1;
       const uint32_t tk = sLoop + 2 * st * SM::kTile, tv = tk + SM::kTile;
-      mbar_wait(&B.full[st], (j >> 1) & 1);
+      if (x == 0) ctl_wait(a_full + 8 * st, (j >> 1) & 1);
       tc_fence_after();
       if (elect_one()) {
-#pragma unroll
-        for (int k = 0; k < D / 16; ++k) mma_bf16_ss(tmem, kdesc(sOwn, k), kdesc(tk, k), idS, k > 0 ? 1u : 0u);
 #pragma unroll
         for (int k = 0; k < D / 16; ++k)
-          mma_bf16_ss(tmem + BKV, kdesc(sOwn + SM::kTile, k), kdesc(tv, k), idS, k > 0 ? 1u : 0u);
-        mma_commit(&B.s_full);
+          mma_bf16_ss(tmem + 64 * x, kdesc(sOwn, k), kdesc(tk + 8192 * x, k), idS, k > 0 ? 1u : 0u);
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k)
+          mma_bf16_ss(tmem + BKV + 64 * x, kdesc(sOwn + SM::kTile, k), kdesc(tv + 8192 * x, k), idS, k > 0 ? 1u : 0u);
+        mma_commit(&B.s_full[x]);
       }
       __syncwarp();
-      mbar_wait(&B.p_full, j & 1);
+    };
+    auto issue_g = [&](int j, int x) {
+      const int st = j & 1;
+      const uint32_t tk = sLoop + 2 * st * SM::kTile;
+      ctl_wait(a_p + 8 * x, j & 1);
       tc_fence_after();
       if (elect_one()) {
 #pragma unroll
-        for (int k = 0; k < BKV / 16; ++k)
-          mma_bf16_ts(tmem + 2 * BKV, tmem + 8 * k, mndesc(tk, k, p.mn_lbo, p.mn_sbo), idQ, (j > 0 || k > 0) ? 1u : 0u);
-        mma_commit(&B.free_[st]);
-        if (j == n - 1) mma_commit(&B.done);
+        for (int k = 0; k < 4; ++k)
+          mma_bf16_ts(tmem + 2 * BKV, tmem + 64 * x + 8 * k, mndesc(tk, 4 * x + k, p.mn_lbo, p.mn_sbo), idQ,
+                      (j > 0 || x > 0 || k > 0) ? 1u : 0u);
+        if (x == 1) {
+          mma_commit(&B.free_[st]);
+          if (j == n - 1) mma_commit(&B.done);
+        }
       }
       __syncwarp();
+    };
+    mbar_wait(&B.own_full, 0);
+    issue_s(0, 0);
+    issue_s(0, 1);
+#pragma unroll 1
+    for (int j = 0; j < n; ++j) {
+      issue_g(j, 0);
+      if (j + 1 < n) issue_s(j + 1, 0);
+      issue_g(j, 1);
+      if (j + 1 < n) issue_s(j + 1, 1);
     }
   } else if (warp < 8) {
-    const int r = (warp & 3) * 32 + lane, hf = warp >> 2;  // query row, column half
+    const int r = (warp & 3) * 32 + lane, hf = warp >> 2;  // query row, key-column half
     const int64_t row = row0 + r;
     const uint32_t lb = tmem + ((uint32_t)((warp & 3) * 32) << 16);
     const int64_t hs = ((int64_t)b * H + h) * S + (int64_t)qt * BQ + r;
@@ -811,38 +841,35 @@ __global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_dq_kernel(const BwdPa
     }
     if (hf == 0) p.dsum[hs] = dsum;
     const float lse = p.lse[hs], c = p.scale_log2, sc = p.scale;
+    const uint32_t tS = lb + 64 * hf, tP = lb + BKV + 64 * hf;
 #pragma unroll 1
     for (int j = 0; j < n; ++j) {
-      mbar_wait(&B.s_full, j & 1);
+      mbar_wait(&B.s_full[hf], j & 1);
       tc_fence_after();
 #pragma unroll 1
-      for (int it = 0; it < 2; ++it) {
-        // half hf takes 32-column chunks hf and hf + 2; dS of chunk q goes to columns
-        // [16q, 16q + 16), which after the pair barrier both warps have read
-        const int q = hf + 2 * it;
+      for (int q = 0; q < 2; ++q) {  // 32-column chunks of this half (key columns 64 hf + 32 q ..)
         uint32_t sr[32], dr[32];
-        tmem_ld_32x32b_x32(lb + 32 * q, sr);
-        tmem_ld_32x32b_x32(lb + BKV + 32 * q, dr);
+        tmem_ld_32x32b_x32(tS + 32 * q, sr);
+        tmem_ld_32x32b_x32(tP + 32 * q, dr);
         wait_ld_dep(sr);
         wait_ld_dep(dr);
-        if (it == 0) pair_bar(warp & 3);
         uint32_t pk[16];
 #pragma unroll
         for (int k = 0; k < 32; k += 2) {
           float pr[2];
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            const bool masked = j == qt && 32 * q + k + e > r;
+            const bool masked = j == qt && 64 * hf + 32 * q + k + e > r;
             const float pe = masked ? 0.0f : ex2(fmaf(__uint_as_float(sr[k + e]), c, -lse));
             pr[e] = pe * (__uint_as_float(dr[k + e]) - dsum) * sc;
           }
           pk[k / 2] = bf2(pr[0], pr[1]);
         }
-        tmem_st_32x32b_x16(lb + 16 * q, pk);  // dS over the already-read S columns
+        tmem_st_32x32b_x16(tS + 16 * q, pk);  // dS over this half's already-read S columns
       }
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(&B.p_full);
+      mbar_arrive(&B.p_full[hf]);
     }
     mbar_wait(&B.done, 0);
     tc_fence_after();
@@ -888,40 +915,62 @@ __global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_dkv_kernel(const BwdP
     const Src q{p.qkv, p.qkv_s, C3, (int64_t)h * D}, dO{p.dout, p.dout_s, C, (int64_t)h * D};
     bwd_producer<D>(threadIdx.x - 256, sOwn, sLoop, s8, B, k, v, row0, q, dO, (int64_t)b * S, kt, n, p);
   } else if (warp == kBwdMma) {
-    constexpr uint32_t idS = idesc_16(BKV, BQ, 0, 0, 1);
+    // Query tile i in two 64-column halves x: S^T_x = K Q_i[x]^T, dP^T_x = V dO_i[x]^T (N = 64)
+    // into TMEM half x; compute warps of half x write P^T_x / dS^T_x (bf16) over them; then
+    // dV += P^T_x dO_i[x], dK += dS^T_x Q_i[x] (TS-MMAs, K = 64).
+    constexpr uint32_t idS = idesc_16(BKV, 64, 0, 0, 1);
     constexpr uint32_t idG = idesc_16(BKV, D, 0, 1, 1);
-    mbar_wait(&B.own_full, 0);
-#pragma unroll 1
-    for (int j = 0; j < n; ++j) {
+    const uint32_t a_full = smem_u32(&B.full[0]), a_p = smem_u32(&B.p_full[0]);
+    auto issue_s = [&](int j, int x) {
       const int st = j & 1;
       const uint32_t tq = sLoop + 2 * st * SM::kTile, tdo = tq + SM::kTile;
-      mbar_wait(&B.full[st], (j >> 1) & 1);
-      if (lane == 0) ATR(4, j);
+      if (x == 0) ctl_wait(a_full + 8 * st, (j >> 1) & 1);
+      if (lane == 0 && x == 0) ATR(4, j);
       tc_fence_after();
       if (elect_one()) {
-#pragma unroll
-        for (int k = 0; k < D / 16; ++k) mma_bf16_ss(tmem, kdesc(sOwn, k), kdesc(tq, k), idS, k > 0 ? 1u : 0u);
 #pragma unroll
         for (int k = 0; k < D / 16; ++k)
-          mma_bf16_ss(tmem + BQ, kdesc(sOwn + SM::kTile, k), kdesc(tdo, k), idS, k > 0 ? 1u : 0u);
-        mma_commit(&B.s_full);
+          mma_bf16_ss(tmem + 64 * x, kdesc(sOwn, k), kdesc(tq + 8192 * x, k), idS, k > 0 ? 1u : 0u);
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k)
+          mma_bf16_ss(tmem + BQ + 64 * x, kdesc(sOwn + SM::kTile, k), kdesc(tdo + 8192 * x, k), idS,
+                      k > 0 ? 1u : 0u);
+        mma_commit(&B.s_full[x]);
       }
       __syncwarp();
-      mbar_wait(&B.p_full, j & 1);
-      if (lane == 0) ATR(5, j);
+    };
+    auto issue_g = [&](int j, int x) {
+      const int st = j & 1;
+      const uint32_t tq = sLoop + 2 * st * SM::kTile, tdo = tq + SM::kTile;
+      ctl_wait(a_p + 8 * x, j & 1);
+      if (lane == 0 && x == 0) ATR(5, j);
       tc_fence_after();
       if (elect_one()) {
+        const uint32_t acc0 = (j > 0 || x > 0) ? 1u : 0u;
 #pragma unroll
-        for (int k = 0; k < BQ / 16; ++k)
-          mma_bf16_ts(tmem + 2 * BQ, tmem + 8 * k, mndesc(tdo, k, p.mn_lbo, p.mn_sbo), idG, (j > 0 || k > 0) ? 1u : 0u);
+        for (int k = 0; k < 4; ++k)
+          mma_bf16_ts(tmem + 2 * BQ, tmem + 64 * x + 8 * k, mndesc(tdo, 4 * x + k, p.mn_lbo, p.mn_sbo), idG,
+                      (acc0 || k > 0) ? 1u : 0u);
 #pragma unroll
-        for (int k = 0; k < BQ / 16; ++k)
-          mma_bf16_ts(tmem + 2 * BQ + D, tmem + BQ + 8 * k, mndesc(tq, k, p.mn_lbo, p.mn_sbo), idG,
-                      (j > 0 || k > 0) ? 1u : 0u);
-        mma_commit(&B.free_[st]);
-        if (j == n - 1) mma_commit(&B.done);
+        for (int k = 0; k < 4; ++k)
+          mma_bf16_ts(tmem + 2 * BQ + D, tmem + BQ + 64 * x + 8 * k, mndesc(tq, 4 * x + k, p.mn_lbo, p.mn_sbo),
+                      idG, (acc0 || k > 0) ? 1u : 0u);
+        if (x == 1) {
+          mma_commit(&B.free_[st]);
+          if (j == n - 1) mma_commit(&B.done);
+        }
       }
       __syncwarp();
+    };
+    mbar_wait(&B.own_full, 0);
+    issue_s(0, 0);
+    issue_s(0, 1);
+#pragma unroll 1
+    for (int j = 0; j < n; ++j) {
+      issue_g(j, 0);
+      if (j + 1 < n) issue_s(j + 1, 0);
+      issue_g(j, 1);
+      if (j + 1 < n) issue_s(j + 1, 1);
     }
   } else if (warp < 8) {
     const int r = (warp & 3) * 32 + lane, hf = warp >> 2;  // key row, query-column half
@@ -929,25 +978,22 @@ __global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_dkv_kernel(const BwdP
     const uint32_t lb = tmem + ((uint32_t)((warp & 3) * 32) << 16);
     const float c = p.scale_log2, sc = p.scale;
     const int64_t hs0 = ((int64_t)b * H + h) * S;
+    const uint32_t tS = lb + 64 * hf, tP = lb + BQ + 64 * hf;
 #pragma unroll 1
     for (int j = 0; j < n; ++j) {
       const int qt = kt + j;
-      const float *lse = p.lse + hs0 + (int64_t)qt * BQ, *dsv = p.dsum + hs0 + (int64_t)qt * BQ;
+      const float *lse = p.lse + hs0 + (int64_t)qt * BQ + 64 * hf, *dsv = p.dsum + hs0 + (int64_t)qt * BQ + 64 * hf;
       if (r == 0) ATR(7, j);
-      mbar_wait(&B.s_full, j & 1);
+      mbar_wait(&B.s_full[hf], j & 1);
       if (r == 0) ATR(8, j);
       tc_fence_after();
 #pragma unroll 1
-      for (int it = 0; it < 2; ++it) {
-        // half hf takes 32-column chunks hf and hf + 2; P / dS of chunk q go to columns
-        // [16q, 16q + 16) of S^T / dP^T, which after the pair barrier both warps have read
-        const int q = hf + 2 * it;
+      for (int q = 0; q < 2; ++q) {  // 32-column chunks of this half (query columns 64 hf + 32 q ..)
         uint32_t sr[32], dr[32];
-        tmem_ld_32x32b_x32(lb + 32 * q, sr);
-        tmem_ld_32x32b_x32(lb + BQ + 32 * q, dr);
+        tmem_ld_32x32b_x32(tS + 32 * q, sr);
+        tmem_ld_32x32b_x32(tP + 32 * q, dr);
         wait_ld_dep(sr);
         wait_ld_dep(dr);
-        if (it == 0) pair_bar(warp & 3);
         uint32_t pk[16], dk[16];
 #pragma unroll
         for (int k8 = 0; k8 < 32; k8 += 8) {  // lse / D of 8 query columns at a time
@@ -962,7 +1008,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_dkv_kernel(const BwdP
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
               const int kk = k8 + k + e;
-              const bool masked = j == 0 && 32 * q + kk < r;  // query before key (diagonal tile)
+              const bool masked = j == 0 && 64 * hf + 32 * q + kk < r;  // query before key (diagonal tile)
               pr[e] = masked ? 0.0f : ex2(fmaf(__uint_as_float(sr[kk]), c, -lq[k + e]));
               ds[e] = pr[e] * (__uint_as_float(dr[kk]) - dq[k + e]) * sc;
             }
@@ -970,13 +1016,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_dkv_kernel(const BwdP
             dk[(k8 + k) / 2] = bf2(ds[0], ds[1]);
           }
         }
-        tmem_st_32x32b_x16(lb + 16 * q, pk);
-        tmem_st_32x32b_x16(lb + BQ + 16 * q, dk);
+        tmem_st_32x32b_x16(tS + 16 * q, pk);
+        tmem_st_32x32b_x16(tP + 16 * q, dk);
       }
       tmem_wait_st();
       tc_fence_before();
       if (r == 0) ATR(9, j);
-      mbar_arrive(&B.p_full);
+      mbar_arrive(&B.p_full[hf]);
     }
     mbar_wait(&B.done, 0);
     tc_fence_after();
