@@ -983,6 +983,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_dkv_kernel(const BwdP
     for (int j = 0; j < n; ++j) {
       const int qt = kt + j;
       const float *lse = p.lse + hs0 + (int64_t)qt * BQ + 64 * hf, *dsv = p.dsum + hs0 + (int64_t)qt * BQ + 64 * hf;
+      if (j + 1 < n && lane < 4) {  // the next query tile's lse / D lines (2 x 256 B) into L1
+        const float *nx = (lane < 2 ? lse : dsv) + BQ + 32 * (lane & 1);
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(nx));
+      }
       if (r == 0) ATR(7, j);
       mbar_wait(&B.s_full[hf], j & 1);
       if (r == 0) ATR(8, j);

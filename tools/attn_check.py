@@ -94,8 +94,8 @@ if a.trace:
     L.jf_attn_set_trace(tr.data_ptr()); runb(); torch.cuda.synchronize(); L.jf_attn_set_trace(None)
     t = tr.view(16, 64).cpu()
     t0 = t[t > 0].min().item()
-    names = {0: "P:cp_done", 1: "P:free", 2: "P:conv_done", 4: "M:full", 5: "M:p_full", 7: "C:wait_s", 8: "C:s_full",
-             9: "C:p_done"}
+    names = {0: "P:cp_done", 1: "P:free", 2: "P:conv_done", 4: "M:S0_issue", 5: "M:G0_issue", 7: "C:wait_s",
+             8: "C:s_full", 9: "C:p_done"}
     print("bwd (dkv CTA 0; dq kernel ran first and shares events 0-2) tile " + " ".join(f"{v:>11s}" for v in names.values()))
     for j in range(s // 128):
         print(f"{j:4d} " + " ".join(f"{(t[e, j].item() - t0) if t[e, j] > 0 else -1:11d}" for e in names))
