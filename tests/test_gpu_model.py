@@ -299,3 +299,55 @@ def test_loss_curve_matches_reference_run_training(jf, golden):
     act = ref > 0.1
     gref = g["grad_norm"][act]
     assert np.abs(np.array(gnorms)[act] - gref).max() <= 0.1 * gref.max()
+
+
+def test_adamw_quantize_multi_equals_per_matrix(jf):
+    """jf_adamw_quantize_multi (one launch over several matrices, AdamW.step's path) ==
+    jf_adamw_quantize per matrix, bit for bit: masters, moments, INT8 codes and scales,
+    for mixed shapes (tile counts not multiples of anything) and per-matrix weight decay."""
+    import struct
+
+    from paper_2403_12422_b200 import _lib
+    from paper_2403_12422_b200.qtensor import empty_like_shape
+
+    L = _lib.lib()
+    st = _lib.stream_handle()
+    g = torch.Generator(device="cuda").manual_seed(3)
+    shapes = [(96, 160), (1024, 1024), (32, 32), (256, 4096), (4096, 288)]
+    wds = [0.0, 0.1, 0.0, 0.05, 0.2]
+    lr, b1, b2, eps, bc1, bc2 = 1e-3, 0.9, 0.999, 1e-8, 0.19, 0.0029
+    mats = []
+    for (n, c), wd in zip(shapes, wds):
+        p = torch.randn(n, c, generator=g, device="cuda")
+        gr = 0.01 * torch.randn(n, c, generator=g, device="cuda")
+        m = 0.001 * torch.randn(n, c, generator=g, device="cuda")
+        v = 1e-6 * torch.rand(n, c, generator=g, device="cuda")
+        mats.append((p, gr, m, v, wd))
+    # per-matrix reference
+    ref = []
+    for p, gr, m, v, wd in mats:
+        pr, mr, vr = p.clone(), m.clone(), v.clone()
+        q = empty_like_shape(*p.shape, p.device)
+        assert L.jf_adamw_quantize(pr.data_ptr(), gr.data_ptr(), mr.data_ptr(), vr.data_ptr(), *p.shape, lr, b1, b2,
+                                   eps, wd, bc1, bc2, q.values.data_ptr(), q.scales.data_ptr(),
+                                   jf.runtime.err_ptr(), st) == 0
+        ref.append((pr, mr, vr, q))
+    # one multi launch
+    tab = torch.empty((len(mats), 10), dtype=torch.int64)
+    outs, tiles = [], 0
+    for i, (p, gr, m, v, wd) in enumerate(mats):
+        pc, mc, vc = p.clone(), m.clone(), v.clone()
+        q = empty_like_shape(*p.shape, p.device)
+        n, c = p.shape
+        tab[i] = torch.tensor([pc.data_ptr(), gr.data_ptr(), mc.data_ptr(), vc.data_ptr(), q.values.data_ptr(),
+                               q.scales.data_ptr(), n, c, struct.unpack("<I", struct.pack("<f", wd))[0], tiles])
+        tiles += (n // 32) * ((c + 255) // 256)
+        outs.append((pc, mc, vc, q))
+    dtab = tab.cuda()
+    assert L.jf_adamw_quantize_multi(dtab.data_ptr(), len(mats), tiles, lr, b1, b2, eps, bc1, bc2,
+                                     jf.runtime.err_ptr(), st) == 0
+    torch.cuda.synchronize()
+    jf.check_errors()
+    for (pr, mr, vr, qr), (pc, mc, vc, qc) in zip(ref, outs):
+        assert torch.equal(pr, pc) and torch.equal(mr, mc) and torch.equal(vr, vc)
+        assert torch.equal(qr.values, qc.values) and torch.equal(qr.scales, qc.scales)
