@@ -11,16 +11,19 @@
 // is written to HBM (the only FP side outputs are the per-row log-sum-exp and,
 // for the backward's D_i = rowsum(dO * O), O itself in bf16).
 //
-// Forward (attn_fwd_kernel), one CTA per (128 query rows, head, batch), 9 warps:
-//   warps 0-3  softmax: thread = query row = TMEM lane.  tcgen05.ld of the S row,
-//              online softmax in the log2 domain with conditional rescaling (O in
-//              TMEM is rescaled only when the running max grows by > 2^8), P in
-//              bf16 to shared memory; epilogue O / l -> 32x32 requantization.
-//   warps 4-7  producers: INT8 Q (once), K, V tiles (128 rows) from HBM, exact
-//              dequantization fl(code * s) -> bf16 into SW128 K-major tiles.
-//   warp 8     MMA issuer: S_j = Q K_j^T (tcgen05 kind::f16, bf16 in, f32 in TMEM,
-//              double-buffered) issued ahead of O += P_{j-1} V_{j-1} (V read
-//              MN-major from the same tile layout).
+// Forward (attn_fwd_kernel): one CTA per two 128-row query tiles (A, B) of a head, 16 warps:
+//   warps 0-7   softmax, 4 per query tile: thread = query row = TMEM lane.  Two passes
+//               over 32-column TMEM chunks of S (row max; then exp2, row sum, P as bf16
+//               pairs written back over S); online softmax in the log2 domain, O in TMEM
+//               rescaled only when the running max grows by > 2^8; epilogue O / l ->
+//               32x32 requantization straight to INT8 codes + scales.
+//   warps 8-14  producers: INT8 Q (once), K, V tiles (128 rows) through a cp.async
+//               staging slot, exact dequantization fl(code * s) -> bf16 SW128 tiles.
+//   warp 15     MMA issuer, static schedule: S_X = Q_X K_j^T (SS), O_X += P_X V_j (TS:
+//               P from TMEM, V read MN-major).
+// Backward: attn_bwd_dq_kernel (per query tile; also D_i = rowsum(dO * O)) and
+// attn_bwd_dkv_kernel (per key tile); each loop tile in two 64-column halves so the
+// softmax-gradient pass on one half overlaps the other half's MMAs; no atomics.
 // Numerics: tolerance class: the reference island is FP32; here the
 // dequantized operands and P are rounded to bf16, accumulation is FP32.
 #include <math.h>
@@ -83,14 +86,6 @@ JF_DEV void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t (&r)[32]) {
       : "memory");
 }
 
-JF_DEV void tmem_ld_32x32b_x16(uint32_t taddr, uint32_t (&r)[16]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-}
 JF_DEV void tmem_st_32x32b_x16(uint32_t taddr, const uint32_t (&r)[16]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
@@ -169,11 +164,6 @@ JF_DEV void deq16_store(uint32_t tile, int r, int c8, uint4 w, float s) {
   sts128(tile + sw_off(r, c8 + 1), o[4], o[5], o[6], o[7]);
 }
 
-JF_DEV float fmax3(float a, float b, float c) {
-  float d;
-  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
-  return d;
-}
 
 // K-major SW128 operand: rows = M/N index, 64 K-elements per 128-byte row.  K step
 // of 16 elements = +32 bytes inside the row; the second 64-column half is +kHalf.
