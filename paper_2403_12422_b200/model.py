@@ -23,6 +23,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
+from .runtime import traced as _rt_traced
 from . import _lib
 from .qlayers import BlockConfig, TransformerBlock
 from .qtensor import quantize_per_block
@@ -116,6 +117,7 @@ class JetfireLM:
         b16[:v] = b
         return w16, b16
 
+    @_rt_traced("jf.model.loss_and_grads")
     def loss_and_grads(self, x: torch.Tensor, y: torch.Tensor, mask: torch.Tensor | None = None,
                        grad_hook=None):
         """(loss, grads) for token ids x, targets y [batch, seq] (trainer.py:373-427).
@@ -241,6 +243,7 @@ class AdamW:
             self._multi = (chunk_t, chunk_s, host, dev, ev)
         return self._multi
 
+    @_rt_traced("jf.AdamW.step")
     def step(self, grads: dict) -> None:
         from .qtensor import empty_like_shape
         from . import runtime as _rt

@@ -214,6 +214,7 @@ def _prep(mode, quantize, out):
     return out
 
 
+@_rt.traced("jf.gemm_fwd")
 def block_mm_forward(xq: BlockQuantTensor, wq: BlockQuantTensor, cfg: TileConfig | None = None,
                      mode: ExecMode = ExecMode.INT8_DATA_FLOW, counters: AccessCounters | None = None,
                      *, bias=None, threads: int = 1, quantize: bool = True,
@@ -284,6 +285,7 @@ def mn_major_ok(*dims: int) -> bool:
     return _rt.gemm_option("tma_scales") != 0 and all(d % 128 == 0 for d in dims)
 
 
+@_rt.traced("jf.gemm_dgrad")
 def block_mm_grad_input(dyq: BlockQuantTensor, wq: BlockQuantTensor, cfg: TileConfig | None = None,
                         mode: ExecMode = ExecMode.INT8_DATA_FLOW,
                         counters: AccessCounters | None = None, *, threads: int = 1,
@@ -324,6 +326,7 @@ def block_mm_grad_input(dyq: BlockQuantTensor, wq: BlockQuantTensor, cfg: TileCo
     return _finish(yq, yf, mode, out)
 
 
+@_rt.traced("jf.gemm_wgrad")
 def block_mm_grad_weight(dyq: BlockQuantTensor, xq: BlockQuantTensor, cfg: TileConfig | None = None,
                          mode: ExecMode = ExecMode.INT8_DATA_FLOW,
                          counters: AccessCounters | None = None, *, threads: int = 1,

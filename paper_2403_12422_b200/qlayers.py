@@ -153,12 +153,14 @@ class QuantLinear:
             quantize_per_block(self.master_weight, self.block, out=self._weight_q)
         self.drop_derived()
 
+    @_rt.traced("jf.QuantLinear.forward")
     def forward(self, xq: BlockQuantTensor, counters: AccessCounters | None = None,
                 threads: int = 1) -> BlockQuantTensor:
         self.saved_input = xq
         return block_mm_forward(xq, self.weight_q, cfg=self.cfg, counters=counters, bias=self.bias,
                                 threads=threads, w16=self.weight_f16(xq.rows))
 
+    @_rt.traced("jf.QuantLinear.backward")
     def backward(self, dyq: BlockQuantTensor, counters: AccessCounters | None = None,
                  threads: int = 1, defer_wgrad: bool = False):
         """(dX quantized, dW FP32 = deq(requant(dY^T X)), dbias FP32).
@@ -274,6 +276,7 @@ class AttentionCore:
         _rt.maybe_check()
         return dqkv
 
+    @_rt.traced("jf.attention.forward")
     def forward_q(self, qkv_q: BlockQuantTensor, batch: int, seq: int) -> BlockQuantTensor:
         """deq(QKV) -> SDPA -> quantize (qlayers.py:350-351), per-head layouts end to end:
         the codes are dequantized straight into contiguous [b, h, s, d] q/k/v and the
@@ -299,6 +302,7 @@ class AttentionCore:
         _quantize_heads(o.detach(), out, 0)
         return out
 
+    @_rt.traced("jf.attention.backward")
     def backward_q(self, dattn_q: BlockQuantTensor, batch: int, seq: int) -> BlockQuantTensor:
         """deq(dO) -> SDPA backward -> quantize dQ|dK|dV into one [N, 3C] tensor (qlayers.py:406-408)."""
         if self._saved is None:
@@ -395,6 +399,7 @@ class TransformerBlock:
         for lin in (self.qkv, self.proj, self.mlp1, self.mlp2):
             lin.mark_updated()
 
+    @_rt.traced("jf.TransformerBlock.forward")
     def forward(self, xq: BlockQuantTensor, batch: int, seq: int, *, dropout_seed: int = 0,
                 train: bool = True, counters: AccessCounters | None = None,
                 threads: int = 1) -> BlockQuantTensor:
@@ -431,6 +436,7 @@ class TransformerBlock:
             self.mlp1.saved_input, m1, self.mlp2.saved_input])
         return out
 
+    @_rt.traced("jf.TransformerBlock.backward")
     def backward(self, dyq: BlockQuantTensor, counters: AccessCounters | None = None,
                  threads: int = 1, grad_hook=None):
         """(dX, grads) as qlayers.py:385-427.  ``grad_hook(grads, names)`` (optional) is called

@@ -102,6 +102,7 @@ def gelu_tables(device=None) -> torch.Tensor:
 
 
 
+@_rt.traced("jf.gelu_fwd")
 def gelu_forward(xq: BlockQuantTensor, counters: AccessCounters | None = None) -> BlockQuantTensor:
     """y = x * CDF(x), requantized per block — kernel K9 (qnonlinear.py:150-158)."""
     nc = xq.rows * xq.cols
@@ -115,6 +116,7 @@ def gelu_forward(xq: BlockQuantTensor, counters: AccessCounters | None = None) -
     return y
 
 
+@_rt.traced("jf.gelu_bwd")
 def gelu_backward(xq: BlockQuantTensor, dyq: BlockQuantTensor,
                   counters: AccessCounters | None = None) -> BlockQuantTensor:
     """dX = dY * (x pdf(x) + CDF(x)) — kernel K10 (qnonlinear.py:161-175)."""
@@ -187,12 +189,14 @@ def _apply_dropout(tq: BlockQuantTensor, state: DropoutState) -> BlockQuantTenso
     return y
 
 
+@_rt.traced("jf.dropout_fwd")
 def dropout_forward(xq, state: DropoutState, counters: AccessCounters | None = None):
     nc = xq.rows * xq.cols
     count_elementwise(counters, ExecMode.INT8_DATA_FLOW, nc, nc)
     return _apply_dropout(xq, state)
 
 
+@_rt.traced("jf.dropout_bwd")
 def dropout_backward(dyq, state: DropoutState, counters: AccessCounters | None = None):
     nc = dyq.rows * dyq.cols
     count_elementwise(counters, ExecMode.INT8_DATA_FLOW, nc, nc)
@@ -202,6 +206,7 @@ def dropout_backward(dyq, state: DropoutState, counters: AccessCounters | None =
 # ── Add with statistics ─────────────────────────────────────────────────
 
 
+@_rt.traced("jf.add_stats")
 def add_forward(x1q: BlockQuantTensor, x2q: BlockQuantTensor | None, stats_width: int = 64,
                 counters: AccessCounters | None = None) -> tuple[BlockQuantTensor, RowStats]:
     """y = x1 + x2 in FP32, requantized, plus stats of the FP32 y — kernel K6.
@@ -237,6 +242,7 @@ def add_forward(x1q: BlockQuantTensor, x2q: BlockQuantTensor | None, stats_width
 # ── LayerNorm ───────────────────────────────────────────────────────────
 
 
+@_rt.traced("jf.ln_fwd")
 def layernorm_forward(xq: BlockQuantTensor, stats: RowStats, params: NormParams,
                       counters: AccessCounters | None = None):
     """Normalize rows using the Add-provided statistics — kernel K7 (qnonlinear.py:300-330)."""
@@ -263,6 +269,7 @@ def layernorm_forward(xq: BlockQuantTensor, stats: RowStats, params: NormParams,
     return y, LayerNormContext(xq, mu, inv_std)
 
 
+@_rt.traced("jf.ln_bwd")
 def layernorm_backward(ctx: LayerNormContext, dyq: BlockQuantTensor, params: NormParams,
                        counters: AccessCounters | None = None):
     """Three-term LayerNorm gradient — kernel K8 (qnonlinear.py:333-355).

@@ -10,6 +10,8 @@ synchronizes and checks; in ``deferred`` mode the check happens at
 
 from __future__ import annotations
 
+import functools
+import os
 import threading
 
 import torch
@@ -195,3 +197,35 @@ def maybe_check() -> None:
     # (no host sync while a CUDA graph is being captured: the error word is read after replay)
     if _config["error_check"] == "eager" and not torch.cuda.is_current_stream_capturing():
         check_errors()
+
+
+# ── NVTX ranges (SURVEY.md §5 tracing) ──────────────────────────────────────
+# Off by default (one dict lookup per op).  ``set_nvtx(True)`` or JF_NVTX=1 wraps every
+# public op (quantizer, the three GEMMs, Add+stats, LayerNorm, GELU, dropout, the
+# attention island, QuantLinear / TransformerBlock fwd+bwd, the model step and AdamW) in
+# a named range, so an nsys timeline or ``ncu --nvtx`` attributes kernels to operators.
+_nvtx = {"on": os.environ.get("JF_NVTX", "0") == "1"}
+
+
+def set_nvtx(flag: bool) -> None:
+    _nvtx["on"] = bool(flag)
+
+
+def nvtx_enabled() -> bool:
+    return _nvtx["on"]
+
+
+def traced(name: str):
+    """Decorator: run ``fn`` inside NVTX range ``name`` when NVTX is on."""
+    def deco(fn):
+        @functools.wraps(fn)
+        def wrapper(*args, **kwargs):
+            if not _nvtx["on"]:
+                return fn(*args, **kwargs)
+            torch.cuda.nvtx.range_push(name)
+            try:
+                return fn(*args, **kwargs)
+            finally:
+                torch.cuda.nvtx.range_pop()
+        return wrapper
+    return deco

@@ -583,3 +583,22 @@ def test_jqt1_matches_reference_blob(jf):
     assert xq.to_bytes() == ref
     back = jf.BlockQuantTensor.from_bytes(ref)
     assert torch.equal(back.values, xq.values) and torch.equal(back.scales, xq.scales)
+
+
+def test_nvtx_ranges_on_gpu(jf):
+    """With NVTX ranges on, a QuantLinear fwd+bwd runs and gives identical bits."""
+    rng = np.random.default_rng(12)
+    x = cu(rng.standard_normal((64, 96)).astype(np.float32))
+    w = (rng.standard_normal((128, 96)) / 10).astype(np.float32)
+    outs = []
+    for on in (False, True):
+        jf.runtime.set_nvtx(on)
+        try:
+            lin = jf.QuantLinear(w, np.zeros(128, np.float32))
+            y = lin.forward(jf.quantize_per_block(x))
+            dx, dw, db = lin.backward(y)
+            outs.append((y.values.clone(), dx.values.clone(), dw.clone()))
+        finally:
+            jf.runtime.set_nvtx(False)
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)

@@ -152,3 +152,30 @@ def test_philox_restatement_matches_numpy(seed):
     key = tuple(int(w) for w in np.random.Philox(key=seed).state["state"]["key"])
     want = np.random.Generator(np.random.Philox(key=seed)).random(37)
     assert np.array_equal(O.philox_random(key, 37), want)
+
+
+def test_nvtx_ranges_wrap_ops_when_enabled(monkeypatch):
+    """runtime.set_nvtx(True) wraps the public ops in named NVTX ranges (SURVEY.md §5);
+    off by default, and the wrapped functions keep their names and signatures."""
+    import inspect
+
+    import paper_2403_12422_b200 as jf
+    from paper_2403_12422_b200 import runtime
+
+    pushed = []
+    monkeypatch.setattr(torch.cuda.nvtx, "range_push", lambda n: pushed.append(n))
+    monkeypatch.setattr(torch.cuda.nvtx, "range_pop", lambda: pushed.append("pop"))
+
+    @runtime.traced("jf.test_op")
+    def op(a, b=2):
+        return a + b
+
+    assert not runtime.nvtx_enabled()
+    assert op(1) == 3 and pushed == []
+    runtime.set_nvtx(True)
+    try:
+        assert op(1, b=5) == 6 and pushed == ["jf.test_op", "pop"]
+    finally:
+        runtime.set_nvtx(False)
+    assert jf.block_mm_forward.__name__ == "block_mm_forward"
+    assert "wq" in inspect.signature(jf.block_mm_forward).parameters
