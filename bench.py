@@ -584,7 +584,77 @@ def run_ours(args, world, rank, local):
         out["allreduce"] = measure_allreduce(wl, world)
     if args.variants and world == 1 and isinstance(wl, BlockWorkload):
         out["variants"] = measure_variants(jf, wl, args)
+    if world == 1 and isinstance(wl, BlockWorkload):
+        out["eltwise"] = measure_eltwise(jf, wl)
     return out, wl, None, w
+
+
+def hbm_peak():
+    """HBM denominator: MEASURED_PEAKS.json's copy bandwidth (driver-written), else the
+    profiling guide's fallback."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            v = float(json.load(f)["hbm_gbs"])
+        return v, "MEASURED_PEAKS.json hbm_gbs (of measured)"
+    except (OSError, KeyError, ValueError, TypeError):
+        return 6650.0, "B200_PROFILING.md fallback 6.65 TB/s (of fallback; MEASURED_PEAKS.json absent)"
+
+
+def measure_eltwise(jf, wl, iters=10):
+    """The memory-bound kernels at this block's shapes (n tokens x C, n x MLP): device time
+    per call from a replayed CUDA graph of `iters` calls (launch overhead excluded), GB/s of
+    ALGORITHMIC bytes (int8 codes + s = 4/1024 B of scale per element, + row stats) and the
+    fraction of HBM bandwidth.  Inputs (16-64 MB) may stay partly L2-resident across calls."""
+    n, c, h = wl.n, wl.c, wl.w["hidden"]
+    S = 4.0 / 1024
+    peak, src = hbm_peak()
+    g = torch.Generator(device="cuda").manual_seed(7)
+    x32 = torch.randn((n, c), generator=g, device="cuda")
+    a = jf.quantize_per_block(x32)
+    b = jf.quantize_per_block(torch.randn((n, c), generator=g, device="cuda"))
+    gq = jf.quantize_per_block(torch.randn((n, h), generator=g, device="cuda"))
+    dg = jf.quantize_per_block(0.1 * torch.randn((n, h), generator=g, device="cuda"))
+    y, st = jf.add_forward(a, b, 64)
+    prm = jf.NormParams(torch.ones(c, device="cuda"), torch.zeros(c, device="cuda"))
+    _, ctx = jf.layernorm_forward(y, st, prm)
+
+    def timed(fn):
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for _ in range(2):
+                fn()
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            for _ in range(iters):
+                fn()
+        graph.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        graph.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / iters
+
+    rows = [("quantize_f32", c, 5 + S, lambda: jf.quantize_per_block(x32), 0),
+            ("add_stats", c, 3 + 3 * S + 0.125, lambda: jf.add_forward(a, b, 64), 0),
+            ("ln_fwd", c, 2 + 2 * S + 0.125, lambda: jf.layernorm_forward(y, st, prm), 8 * n),
+            ("ln_bwd", c, 3 + 3 * S, lambda: jf.layernorm_backward(ctx, b, prm), 8 * n),
+            ("gelu_fwd", h, 2 + 2 * S, lambda: jf.gelu_forward(gq), 0),
+            ("gelu_bwd", h, 3 + 3 * S, lambda: jf.gelu_backward(gq, dg), 0),
+            ("colsum", h, 1 + S, lambda: jf.column_sum(dg), 0)]
+    out = {"hbm_peak_GB_s": peak, "peak_source": src,
+           "timing": f"CUDA-graph replay of {iters} calls, device time per call; algorithmic bytes"}
+    for name, cols, bpe, fn, extra in rows:
+        ms = timed(fn)
+        gbs = (n * cols * bpe + extra) / 1e9 / (ms / 1e3)
+        out[name] = {"shape": [n, cols], "us": round(ms * 1e3, 2), "GB_s": round(gbs, 1),
+                     "frac_hbm": round(gbs / peak, 3)}
+    jf.check_errors()
+    return out
 
 
 # Opt-in configurations of the same block step, timed in the same process right after
