@@ -55,6 +55,43 @@ __global__ void __launch_bounds__(kTileThreads) add_stats_kernel(
   const int64_t valid_w = min((int64_t)tile_w, c - t.c0);
   const int nblk = (int)(valid_w / width);
   const int64_t cw = c / width;
+  if (width == 64 && 2 * 32 * nblk <= kTileThreads) {
+    // pairwise_leaf(64) unrolled, both sums in one pass over shared memory, two threads
+    // per (row, block): thread half h owns numpy's chains 4h..4h+3 (r[j] = a[j], then
+    // r[j] += a[j + 8i] in order); ((r0+r1)+(r2+r3)) + ((r4+r5)+(r6+r7)) across the pair.
+    const int item = threadIdx.x >> 1, hh = threadIdx.x & 1;
+    const int row = item & 31, blk = item >> 5;
+    const bool ok = item < 32 * nblk;
+    float r1[4], r2[4];
+    if (ok) {
+      const float *pb = ysm + row * 257 + blk * 64 + 4 * hh;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float a0 = pb[j];
+        r1[j] = a0;
+        r2[j] = __fmul_rn(a0, a0);
+      }
+#pragma unroll
+      for (int i = 8; i < 64; i += 8)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float a0 = pb[i + j];
+          r1[j] = __fadd_rn(r1[j], a0);
+          r2[j] = __fadd_rn(r2[j], __fmul_rn(a0, a0));
+        }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) r1[j] = r2[j] = 0.f;
+    }
+    float h1 = __fadd_rn(__fadd_rn(r1[0], r1[1]), __fadd_rn(r1[2], r1[3]));
+    float h2 = __fadd_rn(__fadd_rn(r2[0], r2[1]), __fadd_rn(r2[2], r2[3]));
+    const float o1 = __shfl_xor_sync(0xffffffffu, h1, 1), o2 = __shfl_xor_sync(0xffffffffu, h2, 1);
+    if (ok && hh == 0) {
+      const int64_t oi = (t.r0 + row) * cw + t.c0 / width + blk;
+      mean[oi] = __fdiv_rn(__fadd_rn(h1, o1), (float)width);
+      sumsq[oi] = __fadd_rn(h2, o2);
+    }
+  } else
   for (int item = threadIdx.x; item < 32 * nblk; item += kTileThreads) {
     const int row = item & 31, blk = item >> 5;
     const float *base = ysm + row * 257 + blk * width;
