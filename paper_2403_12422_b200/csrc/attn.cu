@@ -679,9 +679,11 @@ JF_DEV void bwd_producer(int t, uint32_t sOwn, uint32_t sLoop, uint32_t s8, BwdB
     uint4 w0[kPer], w1[kPer];
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
-      const int ci = min(t + kNP * i, kChunks - 1);
-      w0[i] = lds128(s8 + 16 * ci);
-      w1[i] = lds128(s8 + SM::kStage8 + 16 * ci);
+      const int ci = t + kNP * i;  // only this thread's own chunks: the slot is its cp.async target
+      if (ci < kChunks) {
+        w0[i] = lds128(s8 + 16 * ci);
+        w1[i] = lds128(s8 + SM::kStage8 + 16 * ci);
+      }
     }
     if (j + 1 < count) issue(j + 1);
 #pragma unroll
