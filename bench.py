@@ -11,10 +11,17 @@ One step = forward + backward of one TransformerBlock in the INT8 data flow
 ``value``: inputs already quantized in HBM.  ``e2e``: host pinned FP32 x and
 dY copied in, quantized, fwd+bwd, dX (codes+scales) copied back, per step.
 
+The line also carries ``roofline`` (the block GEMM vs the INT8 peak, our measured
+kind::i8 ceiling and the exact-promotion bound), ``variants`` (fast promotion,
+f16-widened operands, the fused INT8-boundary attention: same block, same run),
+``eltwise`` (per-kernel GB/s and HBM fraction of the memory-bound kernels),
+``bf16_baseline`` (the same block in torch BF16), ``cpu_baseline`` and ``clocks``.
+
 Multi-GPU (torchrun): data parallel over the token batch, per-rank batch
 fixed (weak scaling); the one exchange step is an NCCL all-reduce of the
-FP32 parameter gradients.  ``--impl reference`` times the CPU oracle port of
-the reference (numpy) on a bounded token sample of the same block.
+FP32 parameter gradients.  ``--impl reference`` times the reference's own
+implementation (the unmodified package in baseline/_ref, or the oracle port
+when absent) on the box's host cores, on a bounded token sample of the block.
 """
 
 from __future__ import annotations
