@@ -85,12 +85,13 @@ def test_fused_attention_deterministic(jf, fused):
         assert torch.equal(x, y)
 
 
-def test_fused_attention_config4_vs_torch_fp32(jf, fused):
-    """BASELINE config 4's attention shape (batch 2, seq 2048, 32 heads x 128) against a
-    torch FP32 SDPA of the same dequantized inputs (the numpy oracle's 2048^2 x 64
-    probability tensor does not fit a test's budget)."""
-    rng = np.random.default_rng(4)
-    b, s, h, d = 2, 2048, 32, 128
+@pytest.mark.parametrize("b,s,h,d", [(2, 2048, 32, 128), (8, 1024, 16, 64)])
+def test_fused_attention_config4_vs_torch_fp32(jf, fused, b, s, h, d):
+    """BASELINE config 4's attention shape (batch 2, seq 2048, 32 heads x 128) and the
+    GPT-2-medium shape (batch 8, seq 1024, 16 heads x 64) against a torch FP32 SDPA of the
+    same dequantized inputs (the numpy oracle's seq^2 x heads probability tensor does not
+    fit a test's budget)."""
+    rng = np.random.default_rng(4 + d)
     c = h * d
     qkv, dattn = _inputs(jf, rng, b, s, h, d)
     core = jf.AttentionCore(h, d, dtype=torch.bfloat16)
