@@ -118,10 +118,12 @@ JF_DEV float absmax3_nan(float a, float b, float c) {
   return d;
 }
 
-// +0.0f read through a volatile global: a value neither NVVM nor ptxas can fold, used
-// as the addend that turns a packed product into an FFMA2 (no mul/add contraction).
-__device__ float g_opaque_zero = 0.0f;
-JF_DEV float opaque_zero() { return *reinterpret_cast<volatile float *>(&g_opaque_zero); }
+// +0.0f from constant memory: a value neither NVVM nor ptxas can fold (the host could
+// rewrite it), used as the addend that turns a packed product into an FFMA2 (no mul/add
+// contraction).  A constant-cache hit -- not the uncached L2 round trip a volatile
+// global read costs on every tile's critical path.
+__constant__ float c_opaque_zero = 0.0f;
+JF_DEV float opaque_zero() { return c_opaque_zero; }
 
 // 8 codes (two words) -> v[0..7], exact: PRMT into a 2^23 mantissa + packed FFMA2.
 JF_DEV void deq8_packed(uint32_t w0, uint32_t w1, DeqScale k, float *v) {

@@ -146,6 +146,34 @@ __global__ void __launch_bounds__(256) ln_moments_kernel(const float *__restrict
   }
 }
 
+// 8 consecutive floats; kVec: as two 16-byte loads (p 16-byte aligned)
+template <bool kVec>
+JF_DEV void ldg8(const float *__restrict__ p, float (&d)[8]) {
+  if (kVec) {
+    const float4 a = __ldg(reinterpret_cast<const float4 *>(p)), b = __ldg(reinterpret_cast<const float4 *>(p) + 1);
+    d[0] = a.x, d[1] = a.y, d[2] = a.z, d[3] = a.w, d[4] = b.x, d[5] = b.y, d[6] = b.z, d[7] = b.w;
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) d[j] = __ldg(p + j);
+  }
+}
+
+// 4 consecutive floats (the warp's 4 rows of a per-row vector; p 16-byte aligned if kVec)
+template <bool kVec>
+JF_DEV void ldg4(const float *__restrict__ p, float (&d)[4]) {
+  if (kVec) {
+    const float4 a = __ldg(reinterpret_cast<const float4 *>(p));
+    d[0] = a.x, d[1] = a.y, d[2] = a.z, d[3] = a.w;
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) d[j] = __ldg(p + j);
+  }
+}
+
+// kVec: gamma, beta, mu, inv_std 16-byte aligned (per-lane float4 loads instead of 16 strided
+// scalar loads that touch 8 cache lines per warp each).  mu / inv_std of the warp's 4
+// rows are one broadcast float4 each (kVec also requires mu / inv_std 16-byte aligned).
+template <bool kVec>
 __global__ void __launch_bounds__(kTileThreads) ln_fwd_kernel(
     const int8_t *__restrict__ x, const float *__restrict__ xs, const float *__restrict__ mu,
     const float *__restrict__ inv_std, const float *__restrict__ gamma,
@@ -156,15 +184,15 @@ __global__ void __launch_bounds__(kTileThreads) ln_fwd_kernel(
   load_deq(t, x, xs, v);
   if (t.active) {
     float g[8], bb[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      g[j] = __ldg(gamma + t.col() + j);
-      bb[j] = __ldg(beta + t.col() + j);
-    }
+    ldg8<kVec>(gamma + t.col(), g);
+    ldg8<kVec>(beta + t.col(), bb);
+    float mv[4], sv[4];
+    ldg4<kVec>(mu + t.row(0), mv);
+    ldg4<kVec>(inv_std + t.row(0), sv);
     const float zero = opaque_zero();
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const float m = __ldg(mu + t.row(i)), is = __ldg(inv_std + t.row(i));
+      const float m = mv[i], is = sv[i];
 #pragma unroll
       for (int j = 0; j < 8; j += 2) {  // packed, same roundings: fl(fl(g*fl(fl(x-m)*is)) + b)
         float x0, x1;
@@ -444,11 +472,12 @@ __global__ void __launch_bounds__(256) ln_bwd_rows_kernel(LnRowArgs A, int depth
 
 // Pass B (32x256 tiles): dx = inv_std * ((dxhat - m1) - xhat*m2) -> requant,
 // plus per-strip column partials of dgamma = sum(dy*xhat), dbeta = sum(dy).
+template <bool kVec>
 __global__ void __launch_bounds__(kTileThreads) ln_bwd_tile_kernel(
     LnRowArgs A, const float *__restrict__ m1, const float *__restrict__ m2, int8_t *dxq,
     float *dxs, float *part_g, float *part_b, int32_t *err) {
   __shared__ uint32_t red[64];
-  __shared__ float colg[8][256], colb[8][256];
+  __shared__ __align__(16) float colg[8][256], colb[8][256];
   const TilePos t = tile_pos(A.n, A.c);
   float xv[4][8], dv[4][8];
   load_deq(t, A.x, A.xs, xv);
@@ -456,20 +485,22 @@ __global__ void __launch_bounds__(kTileThreads) ln_bwd_tile_kernel(
   float pg[8], pb[8];
   if (t.active) {
     float g[8];
+    ldg8<kVec>(A.gamma + t.col(), g);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      g[j] = __ldg(A.gamma + t.col() + j);
-      pg[j] = 0.f;
-      pb[j] = 0.f;
-    }
+    for (int j = 0; j < 8; ++j) pg[j] = pb[j] = 0.f;
+    // the warp's 4 rows of each per-row vector: one broadcast 16-byte load each
+    const int64_t r0 = t.row(0);
+    float muv[4], isv[4], m1v[4], m2v[4];
+    ldg4<kVec>(A.mu + r0, muv);
+    ldg4<kVec>(A.inv_std + r0, isv);
+    ldg4<kVec>(m1 + r0, m1v);
+    ldg4<kVec>(m2 + r0, m2v);
     // packed f32x2, the reference's roundings in order; every product that feeds an
     // add is an FFMA2 with an opaque +0 (ptxas must not contract it)
     const float zero = opaque_zero();
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const int64_t r = t.row(i);
-      const float mr = __ldg(A.mu + r), ir = __ldg(A.inv_std + r);
-      const float a1 = __ldg(m1 + r), a2 = __ldg(m2 + r);
+      const float mr = muv[i], ir = isv[i], a1 = m1v[i], a2 = m2v[i];
 #pragma unroll
       for (int j = 0; j < 8; j += 2) {
         float xh0, xh1, d0, d1, t0, t1, p0, p1;
@@ -492,11 +523,12 @@ __global__ void __launch_bounds__(kTileThreads) ln_bwd_tile_kernel(
         fmul2_rn(xv[i][j], xv[i][j + 1], ir, ir, d0, d1);  // reuse xv as dx
       }
     }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      colg[t.warp][8 * t.lane + j] = pg[j];
-      colb[t.warp][8 * t.lane + j] = pb[j];
-    }
+    float4 *cg4 = reinterpret_cast<float4 *>(&colg[t.warp][8 * t.lane]);
+    float4 *cb4 = reinterpret_cast<float4 *>(&colb[t.warp][8 * t.lane]);
+    cg4[0] = make_float4(pg[0], pg[1], pg[2], pg[3]);
+    cg4[1] = make_float4(pg[4], pg[5], pg[6], pg[7]);
+    cb4[0] = make_float4(pb[0], pb[1], pb[2], pb[3]);
+    cb4[1] = make_float4(pb[4], pb[5], pb[6], pb[7]);
   }
   quant_store(t, xv, dxq, dxs, red, err);  // contains __syncthreads
   // rows in order: warp 0 rows 0..3, warp 1 rows 4..7, ... (sequential over warps)
@@ -823,6 +855,10 @@ using namespace jf;
 int jf_launch_check(const char *what);
 int jf_set_smem_attr(const void *func, int bytes, const char *what);
 
+static bool aligned16(const void *a, const void *b) {
+  return ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15) == 0;
+}
+
 static bool ok_shape(int64_t n, int64_t c) { return n > 0 && c > 0 && n % 32 == 0 && c % 32 == 0; }
 
 static int gcd_i(int a, int b) { return b ? gcd_i(b, a % b) : a; }
@@ -853,8 +889,10 @@ extern "C" int jf_ln_fwd(const int8_t *x, const float *xs, const float *mean, co
       mean, sumsq, n, c, nb, eps, mu, inv_std);
   int rc = jf_launch_check("ln_moments");
   if (rc) return rc;
-  ln_fwd_kernel<<<tile_grid(n, c), kTileThreads, 0, (cudaStream_t)stream>>>(
-      x, xs, mu, inv_std, gamma, beta, n, c, yq, ys, err);
+  const bool vec = aligned16(gamma, beta) && aligned16(mu, inv_std);
+  auto kern = vec ? ln_fwd_kernel<true> : ln_fwd_kernel<false>;
+  kern<<<tile_grid(n, c), kTileThreads, 0, (cudaStream_t)stream>>>(x, xs, mu, inv_std, gamma, beta, n, c,
+                                                                   yq, ys, err);
   return jf_launch_check("ln_fwd");
 }
 
@@ -918,7 +956,9 @@ extern "C" int jf_ln_bwd(const int8_t *x, const float *xs, const float *mu, cons
     ln_bwd_rows_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(A, depth, perfect, m1, m2);
   int rc = jf_launch_check("ln_bwd_rows");
   if (rc) return rc;
-  ln_bwd_tile_kernel<<<tile_grid(n, c), kTileThreads, 0, st>>>(A, m1, m2, dxq, dxs, pg, pb, err);
+  const bool vec = aligned16(gamma, ws) && aligned16(mu, inv_std);
+  auto tk = vec ? ln_bwd_tile_kernel<true> : ln_bwd_tile_kernel<false>;
+  tk<<<tile_grid(n, c), kTileThreads, 0, st>>>(A, m1, m2, dxq, dxs, pg, pb, err);
   rc = jf_launch_check("ln_bwd_tile");
   if (rc) return rc;
   const unsigned g = (unsigned)((c + 31) / 32);
