@@ -506,13 +506,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1) attn_fwd_kernel(const FwdParam
       }
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) am = max(am, __shfl_xor_sync(0xffffffffu, am, off));
-      const float sc = block_scale(am, flags);
+      int bf = 0;
+      const float sc = block_scale(am, bf);
       const float rc = __frcp_rn(sc);
+      flags |= bf;
       uint32_t w[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k)
-        w[k] = pack4(quant_code_fast(v[4 * k], sc, rc), quant_code_fast(v[4 * k + 1], sc, rc),
-                     quant_code_fast(v[4 * k + 2], sc, rc), quant_code_fast(v[4 * k + 3], sc, rc));
+      quant_codes32(v, sc, rc, quant_fast_ok(bf, sc), opaque_zero(), w);
       const int64_t col = (int64_t)h * D + 32 * q;
       uint4 *dst = reinterpret_cast<uint4 *>(p.o + row * C + col);
       dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
@@ -555,10 +554,7 @@ JF_DEV int quant_tmem_block(uint32_t taddr, float mul, int8_t *q, float *sdst, i
   const float sc = block_scale(am, flags);
   const float rc = __frcp_rn(sc);
   uint32_t w[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k)
-    w[k] = pack4(quant_code_fast(v[4 * k], sc, rc), quant_code_fast(v[4 * k + 1], sc, rc),
-                 quant_code_fast(v[4 * k + 2], sc, rc), quant_code_fast(v[4 * k + 3], sc, rc));
+  quant_codes32(v, sc, rc, quant_fast_ok(flags, sc), opaque_zero(), w);
   reinterpret_cast<uint4 *>(q)[0] = make_uint4(w[0], w[1], w[2], w[3]);
   reinterpret_cast<uint4 *>(q)[1] = make_uint4(w[4], w[5], w[6], w[7]);
   if (lane == 0) *sdst = sc;

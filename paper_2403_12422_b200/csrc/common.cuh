@@ -518,4 +518,43 @@ JF_DEV void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d
                : "memory");
 }
 
+
+// Codes of one row of a 32x32 block, 32 values v (scale sc, rc = fl(1/sc)), without
+// XU-pipe ops: per 8 values y = fl(v * rc) (an FFMA2 with the opaque +0 `zero`, so it
+// is a rounded product) and t = fl(y + 1.5*2^23) in packed ops; the code bytes are t's
+// low bytes (t = 1.5*2^23 + rint(y) exactly, |y| < 2^22).  That equals the reference's
+// clip(rint(v / sc)) when the scale is a normal binary16 value (`fast_ok`; then
+// |v/sc| <= 127 * (1 + 2^-11) < 127.5 and the clip is a no-op) and no y lies within 3e-5
+// of a half-integer (|y - fl(v/sc)| <= 2.3e-5, quant_code_fast's argument); otherwise
+// those 8 values take quant_code_fast (FRND + F2I + IEEE division on the rare path).
+JF_DEV void quant_codes32(const float *v, float sc, float rc, bool fast_ok, float zero, uint32_t (&w)[8]) {
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    float tt[8], emax = 0.0f;
+#pragma unroll
+    for (int j = 0; j < 8; j += 2) {
+      float y0, y1, u0, u1, e0, e1;
+      ffma2_rn(y0, y1, v[8 * h + j], v[8 * h + j + 1], rc, rc, zero, zero);
+      fadd2_rn(tt[j], tt[j + 1], y0, y1, 12582912.0f, 12582912.0f);
+      fsub2_rn(u0, u1, tt[j], tt[j + 1], 12582912.0f, 12582912.0f);
+      fsub2_rn(e0, e1, y0, y1, u0, u1);
+      emax = absmax3_nan(emax, e0, e1);
+    }
+    if (fast_ok && emax < 0.49997f) {
+      w[2 * h] = prmt(prmt(__float_as_uint(tt[0]), __float_as_uint(tt[1]), 0x0040u),
+                      prmt(__float_as_uint(tt[2]), __float_as_uint(tt[3]), 0x0040u), 0x5410u);
+      w[2 * h + 1] = prmt(prmt(__float_as_uint(tt[4]), __float_as_uint(tt[5]), 0x0040u),
+                          prmt(__float_as_uint(tt[6]), __float_as_uint(tt[7]), 0x0040u), 0x5410u);
+    } else {
+#pragma unroll
+      for (int k = 2 * h; k < 2 * h + 2; ++k)
+        w[k] = pack4(quant_code_fast(v[4 * k], sc, rc), quant_code_fast(v[4 * k + 1], sc, rc),
+                     quant_code_fast(v[4 * k + 2], sc, rc), quant_code_fast(v[4 * k + 3], sc, rc));
+    }
+  }
+}
+
+// flags == 0 and a normal binary16 scale: quant_codes32's fast path may apply
+JF_DEV bool quant_fast_ok(int flags, float sc) { return flags == 0 && sc >= 6.103515625e-05f; }
+
 }  // namespace jf

@@ -164,48 +164,24 @@ JF_DEV int finish_block(const Params &p, float *acc, int64_t I, int64_t J, int l
   int f = 0;
   const float sc = block_scale(m, f);
   const float rc = __frcp_rn(sc);
-  // Requantization without XU-pipe ops (quant_store_ld's scheme, tile.cuh): per 8
-  // columns y = fl(x * rc) and t = fl(y + 1.5*2^23) in packed ops, the code bytes are
-  // t's low bytes; exact when the scale is a normal binary16 value and no y is within
-  // 3e-5 of a half-integer -- otherwise those 8 take quant_code_fast (FRND + F2I per
-  // element, quarter rate: it was the exposed part of every tile's epilogue).
-  const bool fast_ok = f == 0 && sc >= 6.103515625e-05f;
+  // XU-free requantization (common.cuh quant_codes32; the per-element FRND + F2I of
+  // quant_code_fast, quarter rate, was the exposed part of every tile's epilogue)
   uint32_t w[8];
-#pragma unroll
-  for (int h = 0; h < 4; ++h) {
-    float tt[8], emax = 0.0f;
-#pragma unroll
-    for (int j = 0; j < 8; j += 2) {
-      float y0, y1, u0, u1, e0, e1;
-      ffma2_rn(y0, y1, acc[8 * h + j], acc[8 * h + j + 1], rc, rc, p.zero, p.zero);
-      fadd2_rn(tt[j], tt[j + 1], y0, y1, 12582912.0f, 12582912.0f);
-      fsub2_rn(u0, u1, tt[j], tt[j + 1], 12582912.0f, 12582912.0f);
-      fsub2_rn(e0, e1, y0, y1, u0, u1);
-      emax = absmax3_nan(emax, e0, e1);
-    }
-    if (fast_ok && emax < 0.49997f) {
-      w[2 * h] = prmt(prmt(__float_as_uint(tt[0]), __float_as_uint(tt[1]), 0x0040u),
-                      prmt(__float_as_uint(tt[2]), __float_as_uint(tt[3]), 0x0040u), 0x5410u);
-      w[2 * h + 1] = prmt(prmt(__float_as_uint(tt[4]), __float_as_uint(tt[5]), 0x0040u),
-                          prmt(__float_as_uint(tt[6]), __float_as_uint(tt[7]), 0x0040u), 0x5410u);
-    } else {
-#pragma unroll
-      for (int k = 2 * h; k < 2 * h + 2; ++k)
-        w[k] = pack4(quant_code_fast(acc[4 * k], sc, rc), quant_code_fast(acc[4 * k + 1], sc, rc),
-                     quant_code_fast(acc[4 * k + 2], sc, rc), quant_code_fast(acc[4 * k + 3], sc, rc));
-    }
-  }
+  quant_codes32(acc, sc, rc, quant_fast_ok(f, sc), p.zero, w);
   int8_t *dq = p.yq + row * p.N + col0;
   reinterpret_cast<uint4 *>(dq)[0] = make_uint4(w[0], w[1], w[2], w[3]);
   reinterpret_cast<uint4 *>(dq)[1] = make_uint4(w[4], w[5], w[6], w[7]);
   if (lane == 0) p.ys[I * (p.N >> 5) + J] = sc;
-  if (p.out_kind == OUT_INT8_DEQ) {
+  if (p.out_kind == OUT_INT8_DEQ) {  // fl(code * sc), exact, PRMT + FFMA2 (no I2F)
     float *dst = p.yf + row * p.N + col0;
+    const DeqScale k8 = deq_scale(sc);
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
-      *reinterpret_cast<float4 *>(dst + 4 * k) =
-          make_float4(__fmul_rn(code_at(w[k], 0), sc), __fmul_rn(code_at(w[k], 1), sc),
-                      __fmul_rn(code_at(w[k], 2), sc), __fmul_rn(code_at(w[k], 3), sc));
+    for (int k = 0; k < 4; ++k) {
+      float d[8];
+      deq8_packed(w[2 * k], w[2 * k + 1], k8, d);
+      *reinterpret_cast<float4 *>(dst + 8 * k) = make_float4(d[0], d[1], d[2], d[3]);
+      *reinterpret_cast<float4 *>(dst + 8 * k + 4) = make_float4(d[4], d[5], d[6], d[7]);
+    }
   }
   return lane == 0 ? f : 0;
 }
