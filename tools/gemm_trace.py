@@ -19,7 +19,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2403_12422_b200 import _lib  # noqa: E402
 
-SHAPES = {"proj": (4096, 4096, 4096), "mlp1": (4096, 4096, 16384)}
+SHAPES = {"proj": (4096, 4096, 4096), "mlp1": (4096, 4096, 16384), "g2mlp1": (8192, 1024, 4096)}
 NAMES = ["iss_wait", "iss_free", "iss_done", "w2_wait", "w2_full", "w2_data", "w2_done", "w17_done"]
 
 
@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--shape", default="mlp1")
     ap.add_argument("--mode", default="fast")
     ap.add_argument("--operands", default="int8")
+    ap.add_argument("--dump", action="store_true", help="per-chunk periods and per-stage-position breakdown")
     a = ap.parse_args()
     _lib.load_library(os.path.join(ROOT, "paper_2403_12422_b200", "libjetfire_trace.so"))
     import paper_2403_12422_b200 as jf
@@ -66,6 +67,24 @@ def main():
            "iss_between_chunks": round(float((t[0, rng.start + 1:rng.stop + 1] - t[2, rng])[(t[2, rng] > 0)].mean()), 1),
            "w2_wait_tfull": round(float((t[4, rng] - t[3, rng])[(t[4, rng] > 0) & (t[3, rng] > 0)].mean()), 1),
            "w2_ld": round(float((t[5, rng] - t[4, rng])[(t[5, rng] > 0) & (t[4, rng] > 0)].mean()), 1)}
+    if a.dump:
+        # per chunk: mean promotion end over the 16 warps, delta to the previous chunk
+        d = t[8:24, :]
+        okc = (d > 0).all(axis=0)
+        m = d.mean(axis=0)
+        out["chunk_period_clk"] = [round(float(m[i] - m[i - 1]), 0) if okc[i] and okc[i - 1] else None
+                                   for i in range(1, 256)]
+        # warp 2 per position in the 4-chunk stage (medians over chunks 8..239):
+        # [previous promotion end -> tfull wait start, tfull wait, TMEM load, promotion]
+        w2d = t[8, :]
+        pos = {}
+        for i in range(8, 240):
+            if min(t[3, i], t[4, i], t[5, i], w2d[i], w2d[i - 1]) <= 0:
+                continue
+            pos.setdefault(i % 4, []).append((t[3, i] - w2d[i - 1], t[4, i] - t[3, i], t[5, i] - t[4, i],
+                                              w2d[i] - t[5, i]))
+        out["w2_by_stage_pos"] = {k: [round(float(x), 0) for x in np.median(np.array(v), axis=0)]
+                                  for k, v in sorted(pos.items())}
     print(json.dumps(out))
 
 
