@@ -1,6 +1,6 @@
 """Small-shape driver for compute-sanitizer (memcheck / racecheck / synccheck):
 one launch of each hand-written pipeline -- the tcgen05 GEMM kernels (TMA-staged
-scales, MN-major operands, generic-shape kernel with partial tiles, int32
+scales, MN-major operands, a second tile per CTA, generic-shape kernel with partial tiles, int32
 partials, f16-widened operands), Add+stats, LayerNorm fwd/bwd, GELU fwd/bwd,
 the quantizer, the column sum, the fused INT8-boundary attention (forward and
 both backward kernels, head_dim 64 and 128) and the device Philox dropout mask.  Usage:
@@ -30,6 +30,9 @@ def main():
         jf.block_mm_grad_input(dy, w)                                      # i8s, MN-major B
         jf.block_mm_grad_weight(dy, x, quantize=False)                     # i8s, MN-major A and B
     runtime.set_promotion("exact")
+    # more output tiles (256) than SMs: CTAs run a tile's epilogue and then a second tile
+    xb, wb = q((2048, 128), seed=10), q((2048, 128), 0.1, seed=11)
+    jf.block_mm_forward(xb, wb, bias=torch.zeros(2048, device="cuda"))
     xg, wg = q((160, 96), seed=4), q((224, 96), seed=5)                    # generic kernel, partial tiles
     jf.block_mm_forward(xg, wg)
     jf.block_partials(xg.values, wg.values, 1)                            # int32 partials
