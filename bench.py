@@ -591,7 +591,8 @@ def run_ours(args, world, rank, local):
         out["allreduce"] = measure_allreduce(wl, world)
     if args.variants and world == 1 and isinstance(wl, BlockWorkload):
         out["variants"] = measure_variants(jf, wl, args)
-    if world == 1 and isinstance(wl, BlockWorkload):
+    # (JF_BENCH_ELTWISE=0: skip the side measurement, e.g. for an ncu launch list of the step alone)
+    if world == 1 and isinstance(wl, BlockWorkload) and os.environ.get("JF_BENCH_ELTWISE", "1") != "0":
         out["eltwise"] = measure_eltwise(jf, wl)
     return out, wl, None, w
 

@@ -55,8 +55,8 @@ for s in $STEPS; do
       timeout 900 python bench.py --operands auto --no-cpu > "$OUT/bench_exact_auto.json" 2> "$OUT/bench_exact_auto.err"
       timeout 900 python bench.py --promotion fast --no-cpu --no-bf16 > "$OUT/bench_fast_int8.json" 2> "$OUT/bench_fast_int8.err" ;;
     launches)
-      timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-        --log-file "$OUT/launches.csv" python bench.py --steps 1 --warmup 1 --no-bf16 --no-cpu \
+      JF_BENCH_ELTWISE=0 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+        --log-file "$OUT/launches.csv" python bench.py --steps 1 --warmup 1 --no-bf16 --no-cpu --variants 0 \
         > "$OUT/launches.log" 2>&1 ;;
     ncu)
       timeout 1200 ncu --set full --clock-control none --import-source on -k regex:gemm_ -s 4 -c 1 \
