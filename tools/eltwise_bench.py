@@ -71,6 +71,21 @@ def main():
     report("gelu_bwd", n, h, 3 + 3 * S, timed(lambda: jf.gelu_backward(g, dg)))
     report("colsum", n, h, 1 + S, timed(lambda: jf.column_sum(dg)))
     report("transpose_codes", n, h, 2, timed(lambda: dg.transposed()))
+    # attention-island boundary at the config-4 shape (batch 2, seq 2048, 32 heads x 128):
+    # QKV codes -> three bf16 [b, h, s, d] tensors, and a bf16 [b, h, s, d] -> codes
+    from paper_2403_12422_b200 import _lib
+    from paper_2403_12422_b200.qlayers import _quantize_heads
+    from paper_2403_12422_b200.qtensor import empty_like_shape
+    bt, sq, hh, hd = 2, 2048, 32, 128
+    qkv = jf.quantize_per_block(torch.randn(bt * sq, 3 * hh * hd, device="cuda"))
+    heads = [torch.empty((bt, hh, sq, hd), dtype=torch.bfloat16, device="cuda") for _ in range(3)]
+    L = _lib.lib()
+    deq = lambda: L.jf_dequantize_qkv_heads(qkv.values.data_ptr(), qkv.scales.data_ptr(), bt, sq, hh, hd,  # noqa: E731
+                                            heads[0].data_ptr(), heads[1].data_ptr(), heads[2].data_ptr(),
+                                            _lib.stream_handle())
+    report("dequant_qkv_heads", bt * sq, 3 * hh * hd, 3 + S, timed(deq))
+    out = empty_like_shape(bt * sq, hh * hd, "cuda")
+    report("quantize_heads", bt * sq, hh * hd, 3 + S, timed(lambda: _quantize_heads(heads[0], out, 0)))
     jf.check_errors()
 
 
