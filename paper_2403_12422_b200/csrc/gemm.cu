@@ -686,8 +686,7 @@ bool jf_make_tmap_f16(CUtensorMap *map, const void *ptr, int64_t rows, int64_t c
                       int box_cols, int box_rows);
 
 // Launch options (diagnostics / A-B experiments; results are bit-identical for every
-// option).  Defaults are the measured best.  JF_GEMM_COLS / JF_GEMM_PIPE set them at
-// load time, jf_gemm_set_option() at run time.
+// option), set at run time by jf_gemm_set_option().  Defaults are the measured best.
 struct GemmOptions {
   int tma_scales = 1;  // 0: every shape on the generic kernel
 };

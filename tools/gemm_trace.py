@@ -51,11 +51,9 @@ def main():
     period = float(np.diff(done.mean(axis=0)).mean())
     # lag of each promotion warp behind the earliest one, per chunk (clk), averaged
     lag = (done - done.min(axis=0)).mean(axis=1)
-    sp = [(w + 2) % 4 for w in range(16)]
-    by_sp = {f"sp{q}": round(float(np.mean([lag[w] for w in range(16) if sp[w] == q])), 1) for q in range(4)}
     iss = t[0:3, rng]
     oki = (iss > 0).all(axis=0)
-    sp = [((w + 2) % 4) if os.environ.get("JF_GEMM_MULTI", "1") == "0" else (w % 4) for w in range(16)]
+    sp = [(w + 2) % 4 for w in range(16)]  # promotion warp w is CTA warp w + 2
     by_sp = {f"sp{q}": round(float(np.mean([lag[w] for w in range(16) if sp[w] == q])), 1) for q in range(4)}
     out = {"shape": a.shape, "mode": a.mode, "operands": a.operands, "period_clk": round(period, 1),
            "lag_by_subpartition": by_sp, "lag_by_warp": [round(float(v), 1) for v in lag],

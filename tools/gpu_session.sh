@@ -25,22 +25,10 @@ for s in $STEPS; do
           > "$OUT/sanitize_$tool.txt" 2>&1
         echo "exit $?" >> "$OUT/sanitize_$tool.txt"
       done ;;
-    gemmab)
-      # correctness + kernel time of every (cols, pipe) promotion layout, int8 and f16 operands
-      for cfg in ${GEMMAB_CFGS:-32_0 32_1 64_0 64_1}; do
-        set -- ${cfg%_*} ${cfg#*_}
-        JF_GEMM_COLS=$1 JF_GEMM_MULTI=$2 timeout 600 python -m pytest tests/test_gpu_kernels.py -k "gemm or partials" \
-          -m gpu -x -q > "$OUT/gemm_tests_c$1_p$2.log" 2>&1; echo "exit $?" >> "$OUT/gemm_tests_c$1_p$2.log"
-        for ops in int8 f16; do
-          JF_GEMM_COLS=$1 JF_GEMM_MULTI=$2 timeout 600 python tools/gemm_bench.py --shapes mlp1,proj --operands $ops \
-            > "$OUT/gemm_bench_c$1_p$2_$ops.jsonl" 2>&1
-        done
-      done ;;
     trace)
-      for mu in 0 1; do for m in exact fast; do for ops in int8 f16; do
-        JF_GEMM_MULTI=$mu timeout 300 python tools/gemm_trace.py --shape mlp1 --mode $m --operands $ops \
-          >> "$OUT/gemm_trace.txt" 2>&1
-      done; done; done ;;
+      for m in exact fast; do for ops in int8 f16; do
+        timeout 300 python tools/gemm_trace.py --shape mlp1 --mode $m --operands $ops --dump >> "$OUT/gemm_trace.txt" 2>&1
+      done; done ;;
     micro)
       timeout 300 ./paper_2403_12422_b200/microbench > "$OUT/microbench.jsonl" 2>&1 ;;
     gemm)
