@@ -465,6 +465,50 @@ def test_gemm_output_overflow_flag(jf):
                               lambda: O.mm_forward(q, small, q, small)) is None
 
 
+def _tie_operands(rng, scale):
+    """X [256 x 128]: two unit codes per row (columns i % 128 and (i + 1) % 128), so
+    X . W^T sums two weight codes; W [256 x 128] random codes with one 127 + 127 pair per
+    32 x 32 output block.  Every block's absmax is then 254 * scale^2, its binary16 scale
+    exactly 2 * scale^2, and every odd sum an exact half-integer tie of x / s."""
+    n, k, d = 256, 128, 256
+    x = np.zeros((n, k), np.int8)
+    i = np.arange(n)
+    x[i, i % k] = 1
+    x[i, (i + 1) % k] = 1
+    w = rng.integers(-126, 127, (d, k)).astype(np.int8)
+    for bi in range(0, n, 32):
+        for bj in range(0, d, 32):
+            w[bj, bi % k] = 127
+            w[bj, (bi + 1) % k] = 127
+    xs = np.full((n // 32, k // 32), scale, np.float32)
+    ws = np.full((d // 32, k // 32), scale, np.float32)
+    return x, xs, w, ws
+
+
+@pytest.mark.parametrize("scale", [1.0, 2.0 ** -10])
+def test_gemm_epilogue_ties_and_subnormal_scales(jf, scale):
+    """The GEMM epilogue's requantization (quant_codes32): its packed fast path gives way
+    to the exact per-element path for exact half-integer ties (scale 1: half of all
+    outputs, rounded half-to-even like numpy's rint) and for subnormal binary16 block
+    scales (scale 2^-10: s = 2^-19), in every GEMM direction -- bit-exact vs the oracle."""
+    rng = np.random.default_rng(11)
+    x, xs, w, ws = _tie_operands(rng, scale)
+    X, W = bqt(jf, x, xs), bqt(jf, w, ws)
+    rq, rs = O.mm_forward(x, xs, w, ws)
+    assert np.all(rs == np.float32(2.0 * scale * scale))  # the construction holds
+    assert same_q(jf.block_mm_forward(X, W), rq, rs)
+    # dX = dY W: dY = x (as [n x d'] with d' = 128), W^T = w.T ([128 x 256])
+    rq, rs = O.mm_grad_input(x, xs, np.ascontiguousarray(w.T), np.ascontiguousarray(ws.T))
+    assert same_q(jf.block_mm_grad_input(X, bqt(jf, np.ascontiguousarray(w.T), np.ascontiguousarray(ws.T))), rq, rs)
+    # dW = dY^T X: dY = w ([256 x 128] read transposed), X = x
+    rq, rs = O.mm_grad_weight(np.ascontiguousarray(x.T), np.ascontiguousarray(xs.T), np.ascontiguousarray(w.T),
+                              np.ascontiguousarray(ws.T))
+    got = jf.block_mm_grad_weight(bqt(jf, np.ascontiguousarray(x.T), np.ascontiguousarray(xs.T)),
+                                  bqt(jf, np.ascontiguousarray(w.T), np.ascontiguousarray(ws.T)))
+    assert same_q(got, rq, rs)
+    jf.check_errors()
+
+
 def test_add_overflow_flag(jf):
     q = np.full((64, 128), 127, np.int8)
     s = np.full((2, 4), 65504.0, np.float32)  # 2 * 127 * 65504 / 127 > 65504
