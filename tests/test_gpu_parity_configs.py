@@ -509,6 +509,35 @@ def test_gemm_epilogue_ties_and_subnormal_scales(jf, scale):
     jf.check_errors()
 
 
+@pytest.mark.parametrize("scale", [1.0, 2.0 ** -16])
+def test_tile_requantization_ties_and_subnormal_scales(jf, scale):
+    """quant_store_ld (every memory-bound kernel's requantization) on its exact path:
+    values that are odd multiples of `scale` with a block absmax of 254 * scale make
+    the binary16 scale exactly 2 * scale and half of all x / s exact half-integer ties
+    (numpy rint: half-to-even); scale 2^-16 also makes every block scale subnormal (2^-15).
+    Through the FP32 quantizer and through the residual Add."""
+    rng = np.random.default_rng(12)
+    n, c = 64, 512
+    v = rng.integers(-127, 128, (n, c)).astype(np.float32) * 2 + 1  # odd, |v| <= 255
+    v = np.clip(v, -253, 253)
+    v[::32, ::32] = 254  # one 254 per 32 x 32 block
+    x = (v * np.float32(scale)).astype(np.float32)
+    rq, rs = O.quantize(x)
+    assert np.all(rs == np.float32(2 * scale))
+    assert same_q(jf.quantize_per_block(cu(x)), rq, rs)
+    # Add: a + b with a = odd codes, b = zero codes (scale 1 * scale) -> the same sums
+    a = rng.integers(-126, 127, (n, c)).astype(np.int8)
+    b = rng.integers(-126, 127, (n, c)).astype(np.int8)
+    a[::32, ::32] = 127
+    b[::32, ::32] = 127
+    sa = np.full((n // 32, c // 32), scale, np.float32)
+    rq, rs, rm, rss = O.add_forward(a, sa, b, sa, 64)
+    assert np.all(rs == np.float32(2 * scale))
+    y, st = jf.add_forward(bqt(jf, a, sa), bqt(jf, b, sa), 64)
+    assert same_q(y, rq, rs)
+    jf.check_errors()
+
+
 def test_add_overflow_flag(jf):
     q = np.full((64, 128), 127, np.int8)
     s = np.full((2, 4), 65504.0, np.float32)  # 2 * 127 * 65504 / 127 > 65504
