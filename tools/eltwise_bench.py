@@ -47,9 +47,14 @@ def report(name, n, c, bpe, ms, extra=0):
 
 
 def main():
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--shape", default="config4", choices=["config4", "gpt2"],
+                    help="config4: 4096 tokens x 4096 (GELU 16384); gpt2: 8192 tokens x 1024 (GELU 4096)")
+    a = ap.parse_args()
     jf.require_cuda()
     jf.set_error_check("deferred")
-    n, c, h = 4096, 4096, 16384
+    n, c, h = (4096, 4096, 16384) if a.shape == "config4" else (8192, 1024, 4096)
     x32 = torch.randn(n, c, device="cuda")
     xb = x32.to(torch.bfloat16)
     a = jf.quantize_per_block(x32)
@@ -76,7 +81,7 @@ def main():
     from paper_2403_12422_b200 import _lib
     from paper_2403_12422_b200.qlayers import _quantize_heads
     from paper_2403_12422_b200.qtensor import empty_like_shape
-    bt, sq, hh, hd = 2, 2048, 32, 128
+    bt, sq, hh, hd = (2, 2048, 32, 128) if a.shape == "config4" else (8, 1024, 16, 64)
     qkv = jf.quantize_per_block(torch.randn(bt * sq, 3 * hh * hd, device="cuda"))
     heads = [torch.empty((bt, hh, sq, hd), dtype=torch.bfloat16, device="cuda") for _ in range(3)]
     L = _lib.lib()
